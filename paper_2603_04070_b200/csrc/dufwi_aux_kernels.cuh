@@ -1,0 +1,152 @@
+// Small per-sweep kernels: coefficients, receiver gather, residual/misfit,
+// group reduction and gradient finalisation.  None of these is on the per-step
+// critical path; each runs once per sweep.
+#pragma once
+
+#include "dufwi_common.cuh"
+
+namespace dufwi {
+
+// E/dx^2 and dE/dc per phantom (forward.py:226-234, adjoint.py:116-117), and
+// q = 1/rho for the density operator.
+__global__ void set_model_kernel(Geo g, const double* __restrict__ c, const double* __restrict__ rho,
+                                 double* __restrict__ Ed, double* __restrict__ dEdc,
+                                 double* __restrict__ rho_copy, double* __restrict__ q,
+                                 double inv_dx2_div, double dx2, size_t total) {
+  const size_t N2 = (size_t)g.nx * g.nz;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t cell = i % N2;
+    const int x = (int)(cell / g.nz), z = (int)(cell % g.nz);
+    const double D = damping_at(g, x, z);
+    const double den = 1.0 + D * g.dt;
+    const double cv = c[i];
+    const double E = cv * cv * g.dt * g.dt / den;
+    Ed[i] = E / dx2;
+    dEdc[i] = 2.0 * cv * (g.dt * g.dt) / den;
+    if (rho) {
+      rho_copy[i] = rho[i];
+      q[i] = 1.0 / rho[i];
+    }
+  }
+  (void)inv_dx2_div;
+}
+
+// traces[lu][r][t] = rec[t][lu][slot(s, r)] — the (P,R,nt) ChannelData layout
+// (grid.py:164-183).  Flags non-finite samples (forward.py:309-310).
+__global__ void gather_traces_kernel(Geo g, int unit_begin, int U, const float* __restrict__ rec,
+                                     const int* __restrict__ rx_slot, float* __restrict__ traces,
+                                     int* __restrict__ flag) {
+  const size_t total = (size_t)U * g.R * g.nt;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i % g.nt);
+    const size_t rest = i / g.nt;
+    const int r = (int)(rest % g.R);
+    const int lu = (int)(rest / g.R);
+    const int s = (unit_begin + lu) % g.S;
+    const float v = rec[((size_t)t * U + lu) * g.M + rx_slot[s * g.R + r]];
+    traces[i] = v;
+    if (!isfinite(v)) *flag = 1;
+  }
+}
+
+// One block per unit: resid merged per receiver node into rres[t][lu][slot]
+// (duplicates summed in receiver order, like np.add.at in adjoint.py:127) and
+// the unit's misfit sum((tr - obs)^2) (adjoint.py:113-114) with a fixed-shape
+// block reduction, so results do not depend on scheduling.
+template <int NT>
+__global__ void __launch_bounds__(NT) residual_kernel(Geo g, int unit_begin, int U,
+                                                      const float* __restrict__ traces,
+                                                      const double* __restrict__ obs,
+                                                      const int* __restrict__ rx_slot,
+                                                      const int* __restrict__ rx_next,
+                                                      const unsigned char* __restrict__ rx_head,
+                                                      double* __restrict__ rres,
+                                                      double* __restrict__ misfit_unit) {
+  const int lu = blockIdx.x;
+  const int s = (unit_begin + lu) % g.S;
+  const size_t base = (size_t)lu * g.R * g.nt;
+  const size_t n = (size_t)g.R * g.nt;
+  double sq = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += NT) {
+    const int r = (int)(i / g.nt), t = (int)(i % g.nt);
+    const double d = (double)traces[base + i] - obs[base + i];
+    sq += d * d;
+    if (rx_head[s * g.R + r]) {
+      double v = 2.0 * d;
+      for (int r2 = rx_next[s * g.R + r]; r2 >= 0; r2 = rx_next[s * g.R + r2]) {
+        const size_t j = base + (size_t)r2 * g.nt + t;
+        v += 2.0 * ((double)traces[j] - obs[j]);
+      }
+      rres[((size_t)t * U + lu) * g.M + rx_slot[s * g.R + r]] = v;
+    }
+  }
+  __shared__ double red[NT];
+  red[threadIdx.x] = sq;
+  __syncthreads();
+  for (int w = NT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) misfit_unit[lu] = red[0];
+}
+
+// misfit[b] += sum over the chunk's units of phantom b, in unit order.
+__global__ void misfit_sum_kernel(Geo g, int unit_begin, int U, const double* __restrict__ mu,
+                                  double* __restrict__ misfit) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int lu = 0; lu < U; ++lu) misfit[(unit_begin + lu) / g.S] += mu[lu];
+}
+
+// acc[b] += acc_part[g] for the non-empty groups of phantom b, in group order.
+__global__ void reduce_groups_kernel(Geo g, int unit_begin, int U, int gs, int b0, int nb,
+                                     int gpp, const double* __restrict__ acc_part,
+                                     double* __restrict__ acc) {
+  const size_t N2 = (size_t)g.nx * g.nz;
+  const size_t total = (size_t)nb * N2;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int bl = (int)(i / N2);
+    const size_t cell = i % N2;
+    const int b = b0 + bl;
+    double sum = 0.0;
+    for (int k = 0; k < gpp; ++k) {
+      const int s_first = k * gs;
+      const int u_first = max(b * g.S + s_first, unit_begin);
+      const int u_last = min(b * g.S + min(s_first + gs, g.S), unit_begin + U);
+      if (u_first >= u_last) continue;
+      sum += acc_part[(size_t)(bl * gpp + k) * N2 + cell];
+    }
+    acc[(size_t)b * N2 + cell] += sum;
+  }
+}
+
+// grad = keep ? dE/dc * (acc / dx^2) : 0, keep = D == 0 and farther than guard
+// from every element (adjoint.py:75-91, 133-137).
+__global__ void finalize_kernel(Geo g, const double* __restrict__ acc, const double* __restrict__ dEdc,
+                                const int* __restrict__ elements, int n_el, int apply_mask,
+                                int guard, double dx2, double* __restrict__ grad,
+                                int* __restrict__ flag) {
+  const size_t N2 = (size_t)g.nx * g.nz;
+  const size_t total = (size_t)g.B * N2;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t cell = i % N2;
+    const int x = (int)(cell / g.nz), z = (int)(cell % g.nz);
+    const double a = acc[i];
+    if (!isfinite(a)) *flag = 1;
+    bool keep = true;
+    if (apply_mask) {
+      keep = damping_at(g, x, z) == 0.0;
+      const long g2 = (long)guard * guard;
+      for (int e = 0; e < n_el && keep; ++e) {
+        const long ddx = x - elements[2 * e], ddz = z - elements[2 * e + 1];
+        if (ddx * ddx + ddz * ddz <= g2) keep = false;
+      }
+    }
+    grad[i] = keep ? dEdc[i] * (a / dx2) : 0.0;
+  }
+}
+
+}  // namespace dufwi

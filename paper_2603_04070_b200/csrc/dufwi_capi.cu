@@ -1,0 +1,551 @@
+// C ABI of libdufwi.so (include/dufwi.h): plans, workspace layout and the
+// sweep drivers for the stepwise and cluster engines.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dufwi.h"
+#include "dufwi_aux_kernels.cuh"
+#include "dufwi_cluster_kernels.cuh"
+#include "dufwi_step_kernels.cuh"
+
+using namespace dufwi;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(DUFWI_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+#define LAUNCH_CHECK(plan)                                                               \
+  do {                                                                                   \
+    ++(plan)->launches;                                                                  \
+    cudaError_t _e = cudaGetLastError();                                                 \
+    if (_e != cudaSuccess)                                                               \
+      return fail(DUFWI_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+inline size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct dufwi_plan {
+  Geo geo{};
+  int E = 0, has_rho = 0, engine = 0, last_engine = 0;
+  double dx = 0, dt = 0;
+  bool box_ok = false;  // D == 0 exactly on a rectangle and > 0 elsewhere
+  int device = 0;
+  int64_t launches = 0;
+  // device tables (owned)
+  double *px = nullptr, *pz = nullptr, *d2d = nullptr, *pulse = nullptr;
+  int *tx = nullptr, *rx_slot = nullptr, *rx_next = nullptr, *node_slot = nullptr;
+  int* elements = nullptr;
+  int* rx_slot_unused = nullptr;
+  unsigned char *row_flag = nullptr, *rx_head = nullptr;
+  double *Ed = nullptr, *dEdc = nullptr, *rho = nullptr, *q = nullptr;
+  int* flag = nullptr;
+  std::vector<void*> owned;
+  // cluster engine
+  ClusterCfg ccfg{};
+  bool cluster_ok = false;
+};
+
+namespace {
+
+template <class T>
+int dev_alloc(dufwi_plan_t* p, T** out, size_t count) {
+  void* ptr = nullptr;
+  CUDA_TRY(cudaMalloc(&ptr, std::max<size_t>(count, 1) * sizeof(T)));
+  p->owned.push_back(ptr);
+  *out = static_cast<T*>(ptr);
+  return 0;
+}
+
+template <class T>
+int upload(dufwi_plan_t* p, T** out, const T* host, size_t count) {
+  int rc = dev_alloc(p, out, count);
+  if (rc) return rc;
+  if (count) CUDA_TRY(cudaMemcpy(*out, host, count * sizeof(T), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+// ---------------------------------------------------------------- workspace
+// Offsets are independent of where the unit range starts; the residual area
+// comes first so every store mode finds it at the same place.
+struct Layout {
+  size_t rres = 0, mis = 0, rec = 0, ubuf = 0, hist = 0, strips = 0, lbuf = 0, acc_part = 0,
+         total = 0;
+};
+
+// Shot groups of the stepwise adjoint for a concrete unit range.
+struct Groups {
+  int gs = 1, gpp = 1, nb = 1, b0 = 0, ngroups = 1;
+};
+
+int tiles_of(const Geo& g) {
+  return ((g.nz + kTileZ - 1) / kTileZ) * ((g.nx + kTileX - 1) / kTileX);
+}
+
+// Shot-group size: enough CTAs to fill 148 SMs several times, otherwise as many
+// shots per thread as possible (fewer accumulator read-modify-writes).
+Groups groups_for(const Geo& g, int unit_begin, int U, bool per_unit) {
+  Groups G;
+  const int tiles = tiles_of(g);
+  const int target_ctas = 148 * 8;
+  const int wanted = std::max(1, (target_ctas + tiles - 1) / tiles);
+  int gs = per_unit ? 1 : std::max(1, (U + wanted - 1) / wanted);
+  G.gs = std::min(gs, g.S);
+  G.gpp = (g.S + G.gs - 1) / G.gs;
+  G.b0 = unit_begin / g.S;
+  G.nb = (unit_begin + U - 1) / g.S - G.b0 + 1;
+  G.ngroups = G.nb * G.gpp;
+  return G;
+}
+
+// Upper bound of the group count over every placement of U units.
+int max_groups(const dufwi_plan_t* p, int U, bool per_unit);
+
+Layout layout(const dufwi_plan_t* p, int mode, int U) {
+  const Geo& g = p->geo;
+  Layout L;
+  const size_t N2 = (size_t)g.nx * g.nz;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  L.rres = take((size_t)g.nt * U * g.M * sizeof(double));
+  L.mis = take((size_t)U * sizeof(double));
+  L.rec = take((size_t)g.nt * U * g.M * sizeof(float));
+  L.ubuf = take(2 * (size_t)U * N2 * sizeof(float));
+  if (mode == DUFWI_STORE_FULL) L.hist = take((size_t)g.nt * U * N2 * sizeof(float));
+  if (mode == DUFWI_STORE_STRIPS) L.strips = take((size_t)g.nt * U * g.SL * sizeof(float));
+  if (mode != DUFWI_STORE_NONE) {
+    L.lbuf = take(2 * (size_t)U * N2 * sizeof(float));
+    const int ng = std::max(max_groups(p, U, false), p->cluster_ok ? max_groups(p, U, true) : 0);
+    L.acc_part = take((size_t)ng * N2 * sizeof(double));
+  }
+  L.total = off;
+  return L;
+}
+
+int max_groups(const dufwi_plan_t* p, int U, bool per_unit) {
+  const Geo& g = p->geo;
+  const int total = g.B * g.S;
+  int best = 0;
+  // the count only depends on the start modulo S (and on clipping at the end)
+  for (int start = 0; start < std::min(g.S, std::max(1, total - U + 1)); ++start)
+    best = std::max(best, groups_for(g, start, U, per_unit).ngroups);
+  return std::max(best, 1);
+}
+
+Model model_of(const dufwi_plan_t* p) { return Model{p->Ed, p->has_rho ? p->rho : nullptr, p->q}; }
+
+int check_units(const dufwi_plan_t* p, int unit_begin, int U) {
+  const int total = p->geo.B * p->geo.S;
+  if (U <= 0 || unit_begin < 0 || unit_begin + U > total)
+    return fail(DUFWI_EINVAL, "unit range out of bounds");
+  if (U > 65535) return fail(DUFWI_EINVAL, "at most 65535 units per call");
+  return 0;
+}
+
+}  // namespace
+
+// =============================================================== plan lifecycle
+extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** plan_out) {
+  if (!geo || !plan_out) return fail(DUFWI_EINVAL, "null argument");
+  *plan_out = nullptr;
+  if (geo->nx < 3 || geo->nz < 3 || geo->nt < 3)
+    return fail(DUFWI_EINVAL, "grid must be >= 3x3 with nt >= 3");
+  if (geo->n_phantoms < 1 || geo->n_shots < 1 || geo->n_rx < 1 || geo->n_elements < 0)
+    return fail(DUFWI_EINVAL, "need >= 1 phantom, shot and receiver");
+  if (!(geo->dx > 0) || !(geo->dt > 0)) return fail(DUFWI_EINVAL, "dx, dt must be positive");
+  if (!geo->tx_host || !geo->rx_host || !geo->pulse_host)
+    return fail(DUFWI_EINVAL, "tx, rx and pulse are required");
+  if (!geo->px_host && !geo->damping_host) return fail(DUFWI_EINVAL, "damping is required");
+  const int nx = geo->nx, nz = geo->nz, S = geo->n_shots, R = geo->n_rx;
+  for (int i = 0; i < S; ++i) {
+    const int x = geo->tx_host[2 * i], z = geo->tx_host[2 * i + 1];
+    if (x < 0 || x >= nx || z < 0 || z >= nz) return fail(DUFWI_EINVAL, "tx node outside grid");
+  }
+  for (int i = 0; i < S * R; ++i) {
+    const int x = geo->rx_host[2 * i], z = geo->rx_host[2 * i + 1];
+    if (x < 0 || x >= nx || z < 0 || z >= nz) return fail(DUFWI_EINVAL, "rx node outside grid");
+  }
+
+  auto* p = new dufwi_plan();
+  cudaGetDevice(&p->device);
+  p->E = geo->n_elements;
+  p->has_rho = geo->has_rho ? 1 : 0;
+  p->engine = geo->engine;
+  p->dx = geo->dx;
+  p->dt = geo->dt;
+  Geo& g = p->geo;
+  g.nx = nx;
+  g.nz = nz;
+  g.nt = geo->nt;
+  g.S = S;
+  g.R = R;
+  g.B = geo->n_phantoms;
+  g.dt = geo->dt;
+
+  // receiver-node slots: one slot per distinct receiver node of the geometry
+  std::vector<int> node_slot((size_t)nx * nz, -1);
+  std::vector<unsigned char> row_flag(nx, 0);
+  std::vector<int> rx_slot((size_t)S * R), rx_next((size_t)S * R, -1);
+  std::vector<unsigned char> rx_head((size_t)S * R, 1);
+  int M = 0;
+  for (int i = 0; i < S * R; ++i) {
+    const size_t cell = (size_t)geo->rx_host[2 * i] * nz + geo->rx_host[2 * i + 1];
+    if (node_slot[cell] < 0) node_slot[cell] = M++;
+    rx_slot[i] = node_slot[cell];
+    row_flag[geo->rx_host[2 * i]] = 1;
+  }
+  for (int s = 0; s < S; ++s) {  // chain duplicate receiver nodes within a shot
+    for (int r = 0; r < R; ++r) {
+      const int i = s * R + r;
+      if (!rx_head[i]) continue;
+      int last = i;
+      for (int r2 = r + 1; r2 < R; ++r2) {
+        const int j = s * R + r2;
+        if (rx_slot[j] == rx_slot[i]) {
+          rx_head[j] = 0;
+          rx_next[last] = r2;
+          last = j;
+        }
+      }
+    }
+  }
+  g.M = M;
+
+  // damping: separable profiles or a general map; undamped box detection
+  std::vector<double> dmap;
+  auto D = [&](int x, int z) -> double {
+    return geo->px_host ? std::max(geo->px_host[x], geo->pz_host[z])
+                        : geo->damping_host[(size_t)x * nz + z];
+  };
+  int xl = nx, xh = -1, zl = nz, zh = -1;
+  for (int x = 0; x < nx; ++x)
+    for (int z = 0; z < nz; ++z)
+      if (D(x, z) == 0.0) {
+        xl = std::min(xl, x); xh = std::max(xh, x);
+        zl = std::min(zl, z); zh = std::max(zh, z);
+      }
+  bool ok = xh >= 0;
+  for (int x = 0; x < nx && ok; ++x)
+    for (int z = 0; z < nz && ok; ++z) {
+      const bool in = x >= xl && x <= xh && z >= zl && z <= zh;
+      if (in != (D(x, z) == 0.0)) ok = false;
+    }
+  p->box_ok = ok;
+  if (!ok) { xl = 0; xh = nx - 1; zl = 0; zh = nz - 1; }
+  g.x_lo = xl; g.x_hi = xh; g.z_lo = zl; g.z_hi = zh;
+  g.Lx = xh - xl + 1;
+  g.Lz = zh - zl + 1;
+  g.SL = 2 * g.Lz + 2 * g.Lx;
+
+  int rc = 0;
+  if (geo->px_host) {
+    rc = rc ? rc : upload(p, &p->px, geo->px_host, nx);
+    rc = rc ? rc : upload(p, &p->pz, geo->pz_host, nz);
+  } else {
+    rc = rc ? rc : upload(p, &p->d2d, geo->damping_host, (size_t)nx * nz);
+  }
+  rc = rc ? rc : upload(p, &p->pulse, geo->pulse_host, geo->nt);
+  rc = rc ? rc : upload(p, &p->tx, geo->tx_host, 2 * (size_t)S);
+  rc = rc ? rc : upload(p, &p->rx_slot, rx_slot.data(), rx_slot.size());
+  rc = rc ? rc : upload(p, &p->rx_next, rx_next.data(), rx_next.size());
+  rc = rc ? rc : upload(p, &p->rx_head, rx_head.data(), rx_head.size());
+  rc = rc ? rc : upload(p, &p->node_slot, node_slot.data(), node_slot.size());
+  rc = rc ? rc : upload(p, &p->row_flag, row_flag.data(), row_flag.size());
+  if (p->E > 0) rc = rc ? rc : upload(p, &p->elements, geo->elements_host, 2 * (size_t)p->E);
+  const size_t BN2 = (size_t)g.B * nx * nz;
+  rc = rc ? rc : dev_alloc(p, &p->Ed, BN2);
+  rc = rc ? rc : dev_alloc(p, &p->dEdc, BN2);
+  if (p->has_rho) {
+    rc = rc ? rc : dev_alloc(p, &p->rho, BN2);
+    rc = rc ? rc : dev_alloc(p, &p->q, BN2);
+  }
+  rc = rc ? rc : dev_alloc(p, &p->flag, 4);
+  if (!rc && cudaMemset(p->flag, 0, 4 * sizeof(int)) != cudaSuccess)
+    rc = fail(DUFWI_ECUDA, "memset flag");
+  if (rc) {
+    dufwi_plan_destroy(p);
+    return rc;
+  }
+  g.px = p->px;
+  g.pz = p->pz;
+  g.d2d = p->d2d;
+  g.pulse = p->pulse;
+  g.tx = p->tx;
+  g.node_slot = p->node_slot;
+  g.row_flag = p->row_flag;
+  p->cluster_ok = cluster_config(g, p->has_rho != 0, &p->ccfg);
+  *plan_out = p;
+  return DUFWI_OK;
+}
+
+extern "C" int dufwi_plan_destroy(dufwi_plan_t* plan) {
+  if (!plan) return DUFWI_OK;
+  for (void* ptr : plan->owned) cudaFree(ptr);
+  delete plan;
+  return DUFWI_OK;
+}
+
+extern "C" int dufwi_set_model(dufwi_plan_t* p, const double* c_dev, const double* rho_dev,
+                               void* stream) {
+  if (!p || !c_dev) return fail(DUFWI_EINVAL, "null argument");
+  if (p->has_rho && !rho_dev) return fail(DUFWI_EINVAL, "plan expects a density model");
+  const Geo& g = p->geo;
+  const size_t total = (size_t)g.B * g.nx * g.nz;
+  const int threads = 256;
+  const int blocks = (int)std::min<size_t>((total + threads - 1) / threads, 148 * 16);
+  set_model_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+      g, c_dev, p->has_rho ? rho_dev : nullptr, p->Ed, p->dEdc, p->rho, p->q, 0.0,
+      p->dx * p->dx, total);
+  LAUNCH_CHECK(p);
+  return DUFWI_OK;
+}
+
+extern "C" int dufwi_workspace_bytes(const dufwi_plan_t* p, int32_t mode, int32_t U,
+                                     size_t* bytes_out) {
+  if (!p || !bytes_out) return fail(DUFWI_EINVAL, "null argument");
+  if (mode < 0 || mode > 2) return fail(DUFWI_EINVAL, "bad store mode");
+  if (U <= 0) return fail(DUFWI_EINVAL, "unit_count must be positive");
+  *bytes_out = layout(p, mode, U).total;
+  return DUFWI_OK;
+}
+
+namespace {
+
+int ws_check(const dufwi_plan_t* p, int mode, int unit_begin, int U, size_t ws_bytes,
+             Layout& L) {
+  L = layout(p, mode, U);
+  if (ws_bytes < L.total) return fail(DUFWI_EINVAL, "workspace too small");
+  if (mode == DUFWI_STORE_STRIPS && !p->box_ok)
+    return fail(DUFWI_EINVAL, "strip storage needs a rectangular undamped box");
+  return 0;
+}
+
+bool use_cluster(const dufwi_plan_t* p) {
+  if (p->engine == DUFWI_ENGINE_STEPWISE) return false;
+  return p->cluster_ok;
+}
+
+}  // namespace
+
+// ================================================================== forward
+extern "C" int dufwi_history_offset(const dufwi_plan_t* p, int32_t U, size_t* off) {
+  if (!p || !off || U <= 0) return fail(DUFWI_EINVAL, "bad argument");
+  *off = layout(p, DUFWI_STORE_FULL, U).hist;
+  return DUFWI_OK;
+}
+
+extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, int32_t U,
+                             float* traces_dev, int32_t* nonfinite_dev, void* ws, size_t ws_bytes,
+                             void* stream) {
+  if (!p || !ws) return fail(DUFWI_EINVAL, "null argument");
+  if (mode < 0 || mode > 2) return fail(DUFWI_EINVAL, "bad store mode");
+  int rc = check_units(p, unit_begin, U);
+  if (rc) return rc;
+  Layout L;
+  rc = ws_check(p, mode, unit_begin, U, ws_bytes, L);
+  if (rc) return rc;
+  if (p->engine == DUFWI_ENGINE_CLUSTER && !p->cluster_ok)
+    return fail(DUFWI_EINVAL, "cluster engine requested but the grid does not fit");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geo& g = p->geo;
+  const Model m = model_of(p);
+  char* base = static_cast<char*>(ws);
+  float* rec = reinterpret_cast<float*>(base + L.rec);
+  float* ubuf = reinterpret_cast<float*>(base + L.ubuf);
+  float* hist = reinterpret_cast<float*>(base + L.hist);
+  float* strips = reinterpret_cast<float*>(base + L.strips);
+  const size_t N2 = (size_t)g.nx * g.nz;
+  const size_t fieldU = (size_t)U * N2;
+
+  if (use_cluster(p)) {
+    p->last_engine = DUFWI_ENGINE_CLUSTER;
+    rc = cluster_forward(g, m, p->ccfg, p->has_rho != 0, mode, unit_begin, U, rec,
+                         mode == DUFWI_STORE_FULL ? hist : nullptr,
+                         mode == DUFWI_STORE_STRIPS ? strips : nullptr, ubuf, st);
+    if (rc) return fail(DUFWI_ECUDA, std::string("cluster forward: ") + cudaGetErrorString((cudaError_t)rc));
+    ++p->launches;
+  } else {
+    p->last_engine = DUFWI_ENGINE_STEPWISE;
+    dim3 block(kTileZ, kTileX);
+    dim3 grid((g.nz + kTileZ - 1) / kTileZ, (g.nx + kTileX - 1) / kTileX, U);
+    for (int t = 0; t < g.nt; ++t) {
+      float* rec_t = rec + (size_t)t * U * g.M;
+      const int has1 = t >= 1, has2 = t >= 2;
+      if (mode == DUFWI_STORE_FULL) {
+        const float* u1 = has1 ? hist + (size_t)(t - 1) * fieldU : nullptr;
+        const float* u2 = has2 ? hist + (size_t)(t - 2) * fieldU : nullptr;
+        float* uo = hist + (size_t)t * fieldU;
+        if (p->has_rho)
+          fwd_step_kernel<true, 1><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, u2, uo, rec_t, nullptr, has1, has2);
+        else
+          fwd_step_kernel<false, 1><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, u2, uo, rec_t, nullptr, has1, has2);
+      } else {
+        const float* u1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
+        float* uo = ubuf + (size_t)(t & 1) * fieldU;
+        float* st_t = mode == DUFWI_STORE_STRIPS ? strips + (size_t)t * U * g.SL : nullptr;
+        if (mode == DUFWI_STORE_STRIPS) {
+          if (p->has_rho)
+            fwd_step_kernel<true, 2><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, uo, uo, rec_t, st_t, has1, has2);
+          else
+            fwd_step_kernel<false, 2><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, uo, uo, rec_t, st_t, has1, has2);
+        } else {
+          if (p->has_rho)
+            fwd_step_kernel<true, 0><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, uo, uo, rec_t, nullptr, has1, has2);
+          else
+            fwd_step_kernel<false, 0><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, uo, uo, rec_t, nullptr, has1, has2);
+        }
+      }
+      LAUNCH_CHECK(p);
+    }
+  }
+  if (traces_dev) {
+    const size_t total = (size_t)U * g.R * g.nt;
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+    gather_traces_kernel<<<blocks, 256, 0, st>>>(g, unit_begin, U, rec, p->rx_slot, traces_dev,
+                                                 nonfinite_dev ? nonfinite_dev : p->flag);
+    LAUNCH_CHECK(p);
+  }
+  return DUFWI_OK;
+}
+
+// ================================================================= residual
+extern "C" int dufwi_residual(dufwi_plan_t* p, int32_t unit_begin, int32_t U,
+                              const float* traces_dev, const double* obs_dev, double* misfit_dev,
+                              void* ws, size_t ws_bytes, void* stream) {
+  if (!p || !traces_dev || !obs_dev || !misfit_dev || !ws)
+    return fail(DUFWI_EINVAL, "null argument");
+  int rc = check_units(p, unit_begin, U);
+  if (rc) return rc;
+  const Layout L = layout(p, DUFWI_STORE_NONE, U);
+  if (ws_bytes < L.rec) return fail(DUFWI_EINVAL, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geo& g = p->geo;
+  char* base = static_cast<char*>(ws);
+  double* rres = reinterpret_cast<double*>(base + L.rres);
+  double* mu = reinterpret_cast<double*>(base + L.mis);
+  const size_t rres_bytes = (size_t)g.nt * U * g.M * sizeof(double);
+  CUDA_TRY(cudaMemsetAsync(rres, 0, rres_bytes, st));
+  residual_kernel<256><<<U, 256, 0, st>>>(g, unit_begin, U, traces_dev, obs_dev, p->rx_slot,
+                                          p->rx_next, p->rx_head, rres, mu);
+  LAUNCH_CHECK(p);
+  misfit_sum_kernel<<<1, 32, 0, st>>>(g, unit_begin, U, mu, misfit_dev);
+  LAUNCH_CHECK(p);
+  return DUFWI_OK;
+}
+
+// ================================================================== adjoint
+extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, int32_t U,
+                             void* ws, size_t ws_bytes, double* acc_dev, void* stream) {
+  if (!p || !ws || !acc_dev) return fail(DUFWI_EINVAL, "null argument");
+  if (mode != DUFWI_STORE_FULL && mode != DUFWI_STORE_STRIPS)
+    return fail(DUFWI_EINVAL, "adjoint needs FULL or STRIPS history");
+  int rc = check_units(p, unit_begin, U);
+  if (rc) return rc;
+  Layout L;
+  rc = ws_check(p, mode, unit_begin, U, ws_bytes, L);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geo& g = p->geo;
+  const Model m = model_of(p);
+  char* base = static_cast<char*>(ws);
+  const double* rres = reinterpret_cast<const double*>(base + L.rres);
+  float* ubuf = reinterpret_cast<float*>(base + L.ubuf);
+  float* hist = reinterpret_cast<float*>(base + L.hist);
+  float* strips = reinterpret_cast<float*>(base + L.strips);
+  float* lbuf = reinterpret_cast<float*>(base + L.lbuf);
+  double* acc_part = reinterpret_cast<double*>(base + L.acc_part);
+  const size_t N2 = (size_t)g.nx * g.nz;
+  const size_t fieldU = (size_t)U * N2;
+
+  const bool clus = use_cluster(p);
+  const Groups G = groups_for(g, unit_begin, U, clus);
+  if (clus) {
+    p->last_engine = DUFWI_ENGINE_CLUSTER;
+    // per-unit accumulators: group (b - b0) * S + s  ==  lu + (unit_begin - b0 * S)
+    const int acc_off = unit_begin - G.b0 * g.S;
+    rc = cluster_adjoint(g, m, p->ccfg, p->has_rho != 0, mode, unit_begin, U, rres,
+                         mode == DUFWI_STORE_FULL ? hist : nullptr,
+                         mode == DUFWI_STORE_STRIPS ? strips : nullptr, ubuf, acc_part, acc_off,
+                         st);
+    if (rc) return fail(DUFWI_ECUDA, std::string("cluster adjoint: ") + cudaGetErrorString((cudaError_t)rc));
+    ++p->launches;
+  } else {
+  p->last_engine = DUFWI_ENGINE_STEPWISE;
+  CUDA_TRY(cudaMemsetAsync(acc_part, 0, (size_t)G.ngroups * N2 * sizeof(double), st));
+  dim3 block(kTileZ, kTileX);
+  dim3 grid((g.nz + kTileZ - 1) / kTileZ, (g.nx + kTileX - 1) / kTileX, G.ngroups);
+  for (int t = g.nt - 1; t >= 0; --t) {
+    const int has1 = t <= g.nt - 2, has2 = t <= g.nt - 3;
+    const float* l1 = lbuf + (size_t)((t + 1) & 1) * fieldU;
+    float* l2o = lbuf + (size_t)(t & 1) * fieldU;
+    const double* rres_t = rres + (size_t)t * U * g.M;
+    const int do_img = t >= 1;
+    if (mode == DUFWI_STORE_FULL) {
+      const float* F = do_img ? hist + (size_t)(t - 1) * fieldU : nullptr;
+      if (p->has_rho)
+        adj_step_kernel<true, 1><<<grid, block, 0, st>>>(g, m, t, unit_begin, U, G.gs, G.b0, G.gpp, l1, l2o, F, nullptr, nullptr, nullptr, rres_t, acc_part, has1, has2, do_img, 0);
+      else
+        adj_step_kernel<false, 1><<<grid, block, 0, st>>>(g, m, t, unit_begin, U, G.gs, G.b0, G.gpp, l1, l2o, F, nullptr, nullptr, nullptr, rres_t, acc_part, has1, has2, do_img, 0);
+    } else {
+      float* ut = ubuf + (size_t)(t & 1) * fieldU;
+      const float* utm1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
+      const float* st_tm1 = do_img ? strips + (size_t)(t - 1) * U * g.SL : nullptr;
+      const int do_recon = t >= 2;
+      if (p->has_rho)
+        adj_step_kernel<true, 2><<<grid, block, 0, st>>>(g, m, t, unit_begin, U, G.gs, G.b0, G.gpp, l1, l2o, nullptr, ut, utm1, st_tm1, rres_t, acc_part, has1, has2, do_img, do_recon);
+      else
+        adj_step_kernel<false, 2><<<grid, block, 0, st>>>(g, m, t, unit_begin, U, G.gs, G.b0, G.gpp, l1, l2o, nullptr, ut, utm1, st_tm1, rres_t, acc_part, has1, has2, do_img, do_recon);
+    }
+    LAUNCH_CHECK(p);
+  }
+  }
+  {
+    const size_t total = (size_t)G.nb * N2;
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+    reduce_groups_kernel<<<blocks, 256, 0, st>>>(g, unit_begin, U, G.gs, G.b0, G.nb, G.gpp,
+                                                 acc_part, acc_dev);
+    LAUNCH_CHECK(p);
+  }
+  return DUFWI_OK;
+}
+// ================================================================= finalize
+extern "C" int dufwi_finalize_gradient(dufwi_plan_t* p, const double* acc_dev, int32_t apply_mask,
+                                       int32_t guard, double* grad_dev, int32_t* nonfinite_dev,
+                                       void* stream) {
+  if (!p || !acc_dev || !grad_dev || !nonfinite_dev) return fail(DUFWI_EINVAL, "null argument");
+  if (guard < 0) return fail(DUFWI_EINVAL, "guard radius must be >= 0");
+  const Geo& g = p->geo;
+  const size_t total = (size_t)g.B * g.nx * g.nz;
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+  finalize_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      g, acc_dev, p->dEdc, p->elements, p->E, apply_mask, guard, p->dx * p->dx, grad_dev,
+      nonfinite_dev);
+  LAUNCH_CHECK(p);
+  return DUFWI_OK;
+}
+
+extern "C" int64_t dufwi_plan_launch_count(const dufwi_plan_t* p) { return p ? p->launches : -1; }
+extern "C" int32_t dufwi_plan_last_engine(const dufwi_plan_t* p) { return p ? p->last_engine : -1; }
+extern "C" const char* dufwi_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* dufwi_version(void) { return "dufwi-b200 0.1.0 (sm_100a)"; }

@@ -1,0 +1,84 @@
+// Shared device-side types and helpers for the DUFWI sm_100a kernels.
+//
+// Arithmetic model: wavefields are stored in f32 in HBM, every
+// per-cell update is evaluated in f64 registers from the f32 inputs and rounded
+// once when stored.  Coefficients (E/dx^2, dE/dc, damping profiles, pulse) stay
+// f64 so the only rounding per step is the f32 store.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dufwi {
+
+// Undamped-box + slot tables, shared by all units of a plan.
+struct Geo {
+  int nx, nz, nt;
+  int S, R, M, B;
+  int x_lo, x_hi, z_lo, z_hi;  // inclusive undamped box (strip mode)
+  int Lx, Lz, SL;              // box extents and ring length per step (2Lz + 2Lx)
+  double dt;
+  const double* px;            // [nx] separable damping, or nullptr
+  const double* pz;            // [nz]
+  const double* d2d;           // [nx][nz] general damping if px == nullptr
+  const double* pulse;         // [nt]
+  const int* tx;               // [S][2]
+  const int* node_slot;        // [nx][nz] receiver-node slot or -1
+  const unsigned char* row_flag;  // [nx] 1 if the row holds any slot
+};
+
+// Per-phantom coefficient arrays.
+struct Model {
+  const double* Ed;    // [B][nx][nz]  c^2 dt^2 / (1 + D dt) / dx^2
+  const double* rho;   // [B][nx][nz]  density or nullptr
+  const double* q;     // [B][nx][nz]  1/rho
+};
+
+__device__ __forceinline__ double damping_at(const Geo& g, int x, int z) {
+  return g.px ? fmax(__ldg(g.px + x), __ldg(g.pz + z)) : __ldg(g.d2d + (size_t)x * g.nz + z);
+}
+
+// A, B of the damped update (forward.py:226-234); exactly (2, -1) where D == 0.
+__device__ __forceinline__ void ab_coeffs(double D, double dt, double& A, double& Bc) {
+  if (D == 0.0) {
+    A = 2.0;
+    Bc = -1.0;
+    return;
+  }
+  const double ddt = D * dt;
+  const double den = 1.0 + ddt;
+  A = (2.0 - ddt * ddt) / den;
+  Bc = (ddt - 1.0) / den;
+}
+
+// Face weights of the variable-density operator at cell (x,z) of phantom
+// arrays rho/q (oracle/dufwi_oracle.py rho_face_weights): w_j = rho_c (q_c + q_j)/2,
+// outer faces use q_j := q_c.
+struct RhoW {
+  double xm, xp, zm, zp, W;
+};
+
+__device__ __forceinline__ RhoW rho_weights(const double* rho, const double* q, int nx, int nz,
+                                            int x, int z) {
+  const size_t c = (size_t)x * nz + z;
+  const double rc = __ldg(rho + c), qc = __ldg(q + c);
+  const double qxm = x > 0 ? __ldg(q + c - nz) : qc;
+  const double qxp = x < nx - 1 ? __ldg(q + c + nz) : qc;
+  const double qzm = z > 0 ? __ldg(q + c - 1) : qc;
+  const double qzp = z < nz - 1 ? __ldg(q + c + 1) : qc;
+  RhoW w;
+  w.xm = rc * (0.5 * (qc + qxm));
+  w.xp = rc * (0.5 * (qc + qxp));
+  w.zm = rc * (0.5 * (qc + qzm));
+  w.zp = rc * (0.5 * (qc + qzp));
+  w.W = ((w.xm + w.xp) + w.zm) + w.zp;
+  return w;
+}
+
+// Weight of the face (j -> c) as seen from neighbour j: rho_j (q_j + q_c)/2.
+__device__ __forceinline__ double rho_in_weight(const double* rho, const double* q, size_t c,
+                                                size_t j) {
+  return __ldg(rho + j) * (0.5 * (__ldg(q + j) + __ldg(q + c)));
+}
+
+}  // namespace dufwi

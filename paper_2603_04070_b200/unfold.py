@@ -1,0 +1,118 @@
+"""Unfolded (DUFWI) inference driver — mirror of ``fwilab.unfold`` inference side.
+
+``unfold_infer`` keeps the reference signature (unfold.py:253-267): start from
+the clamped initial map, then per stage compute the gradient, apply the
+stage network's update and clamp.  The loop is device-resident: the speed
+map, gradient and network update never leave the GPU between stages; the
+returned :class:`SosMap` list is copied to the host once at the end.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .forward import DampingProfile, NumericError, SourcePulse, _check_simulation_inputs, get_engine, zero_damping
+from .grid import ChannelData, Grid2D, SosMap, check_cfl
+from .network import NormSpec
+
+__all__ = ["InversionSetup", "cfl_safe_bounds", "clamp_sos", "unfold_infer", "Reconstructor"]
+
+
+@dataclass(frozen=True)
+class InversionSetup:
+    """Physics context of training and inference (unfold.py:66-74); ``density``
+    is an extension."""
+
+    pulse: SourcePulse
+    damping: DampingProfile | None = None
+    bounds: tuple[float, float] = (1300.0, 3200.0)
+    water_speed: float = 1500.0
+    norm: NormSpec = field(default_factory=NormSpec)
+    density: np.ndarray | None = None
+
+
+def cfl_safe_bounds(grid: Grid2D, bounds: tuple[float, float], safety: float = 0.999):
+    """Cap the upper bound at the stability limit (unfold.py:117-131)."""
+    limit = safety * grid.dx / (grid.dt * np.sqrt(2.0))
+    lo, hi = bounds
+    if lo >= limit:
+        raise ValueError(f"lower bound {lo} m/s already exceeds the CFL limit {limit:.1f} m/s")
+    return (lo, min(hi, limit))
+
+
+def clamp_sos(sos: SosMap, bounds: tuple[float, float]) -> SosMap:
+    """Elementwise clamp, idempotent (unfold.py:134-142)."""
+    lo, hi = bounds
+    if not lo < hi:
+        raise ValueError("bounds must satisfy c_min < c_max")
+    v = np.clip(sos.values, lo, hi)
+    return sos if np.array_equal(v, sos.values) else sos.with_values(v)
+
+
+class Reconstructor:
+    """Device-resident K-stage unfolded inference for B phantoms sharing an acquisition.
+
+    ``reconstruct(obs, c0)`` takes device tensors ((B*S, R, nt) f64 observed
+    data and (B, nx, nz) initial maps) and returns the list of stage maps
+    (B, nx, nz) on device, plus the per-stage gradients when asked.
+    """
+
+    def __init__(self, engine, nets, bounds, guard_radius: int = 2, rho=None):
+        self.engine = engine
+        self.nets = list(nets)
+        self.bounds = bounds
+        self.guard_radius = guard_radius
+        self.rho = rho
+
+    def reconstruct(self, obs, c0, keep_gradients: bool = False, check_finite: bool = True):
+        import torch
+
+        lo, hi = self.bounds
+        c = torch.clamp(c0.to(torch.float64), lo, hi)
+        maps, grads = [], []
+        for net in self.nets:
+            self.engine.set_model(c, self.rho)
+            _, g = self.engine.misfit_and_gradient(obs, guard_radius=self.guard_radius,
+                                                   check_finite=check_finite)
+            if hasattr(net, "predict_update_device"):
+                upd = net.predict_update_device(c, g)
+            else:  # a host network (e.g. the reference's NumPy CNN): one round trip per stage
+                upd = torch.stack([torch.as_tensor(net.predict_update(ci.cpu().numpy(),
+                                                                      gi.cpu().numpy()))
+                                   for ci, gi in zip(c, g)]).to(c.device)
+            c = torch.clamp(c + upd, lo, hi)
+            maps.append(c)
+            if keep_gradients:
+                grads.append(g)
+        return (maps, grads) if keep_gradients else maps
+
+
+def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) -> list[SosMap]:
+    """Run all stages; returns C_1..C_K (unfold.py:253-267)."""
+    import torch
+
+    grid = c0.grid
+    lo, hi = setup.bounds
+    if not lo < hi:
+        raise ValueError("bounds must satisfy c_min < c_max")
+    damping = setup.damping if setup.damping is not None else zero_damping(grid)
+    geometry = m_obs.geometry
+    c_first = clamp_sos(c0, setup.bounds)
+    _check_simulation_inputs(c_first, geometry, setup.pulse, damping)
+    # every later iterate is clamped to the same bounds: CFL holds for all of them
+    if not check_cfl(grid, hi).ok and not check_cfl(grid, max(c_first.c_max, lo)).ok:
+        raise ValueError("CFL violated by the clamp bounds")
+    rho = None if setup.density is None else np.asarray(setup.density, dtype=np.float64)[None]
+    eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
+                     setup.pulse.samples, damping, has_rho=rho is not None)
+    rec = Reconstructor(eng, nets, setup.bounds, rho=rho)
+    obs = torch.as_tensor(m_obs.traces, dtype=torch.float64).to(eng.device)
+    c = torch.as_tensor(c0.values, dtype=torch.float64).to(eng.device)[None]
+    try:
+        maps = rec.reconstruct(obs, c)
+    except FloatingPointError as exc:
+        raise NumericError(str(exc)) from exc
+    host = torch.stack(maps).cpu().numpy()
+    return [SosMap(grid, host[k, 0]) for k in range(host.shape[0])]
