@@ -132,6 +132,11 @@ int64_t dufwi_plan_launch_count(const dufwi_plan_t* plan);
 /* Engine actually used for the last forward/adjoint call (DUFWI_ENGINE_*). */
 int32_t dufwi_plan_last_engine(const dufwi_plan_t* plan);
 
+/* Engine diagnostics: out[0..7] = cluster_ok, cluster CTAs, rows per CTA,
+ * rows per thread, threads per CTA, f64 exchange, smem forward, smem adjoint.
+ * Returns the number of values written (<= n). */
+int32_t dufwi_plan_info(const dufwi_plan_t* plan, int64_t* out, int32_t n);
+
 /* Thread-local message for the last non-zero return code on this thread. */
 const char* dufwi_last_error(void);
 

@@ -24,7 +24,7 @@ ENGINE_AUTO, ENGINE_STEPWISE, ENGINE_CLUSTER = 0, 1, 2
 EXPORTED_SYMBOLS = (
     "dufwi_plan_create", "dufwi_plan_destroy", "dufwi_set_model", "dufwi_workspace_bytes",
     "dufwi_forward", "dufwi_history_offset", "dufwi_residual", "dufwi_adjoint",
-    "dufwi_finalize_gradient", "dufwi_plan_launch_count", "dufwi_plan_last_engine", "dufwi_last_error", "dufwi_version",
+    "dufwi_finalize_gradient", "dufwi_plan_launch_count", "dufwi_plan_last_engine", "dufwi_plan_info", "dufwi_last_error", "dufwi_version",
 )
 
 
@@ -77,6 +77,8 @@ def _declare(so: ctypes.CDLL) -> None:
     so.dufwi_plan_launch_count.restype = i64
     so.dufwi_plan_last_engine.argtypes = [vp]
     so.dufwi_plan_last_engine.restype = i32
+    so.dufwi_plan_info.argtypes = [vp, ctypes.POINTER(i64), i32]
+    so.dufwi_plan_info.restype = i32
     so.dufwi_last_error.restype = ctypes.c_char_p
     so.dufwi_version.restype = ctypes.c_char_p
     for name in ("dufwi_plan_create", "dufwi_plan_destroy", "dufwi_set_model",

@@ -547,5 +547,14 @@ extern "C" int dufwi_finalize_gradient(dufwi_plan_t* p, const double* acc_dev, i
 
 extern "C" int64_t dufwi_plan_launch_count(const dufwi_plan_t* p) { return p ? p->launches : -1; }
 extern "C" int32_t dufwi_plan_last_engine(const dufwi_plan_t* p) { return p ? p->last_engine : -1; }
+extern "C" int32_t dufwi_plan_info(const dufwi_plan_t* p, int64_t* out, int32_t n) {
+  if (!p || !out) return 0;
+  const int64_t v[8] = {p->cluster_ok ? 1 : 0, p->ccfg.cs, p->ccfg.rows, p->ccfg.rpt,
+                        p->ccfg.threads, p->ccfg.dbl, (int64_t)p->ccfg.smem_fwd,
+                        (int64_t)p->ccfg.smem_adj};
+  const int k = n < 8 ? n : 8;
+  for (int i = 0; i < k; ++i) out[i] = v[i];
+  return k;
+}
 extern "C" const char* dufwi_last_error(void) { return g_last_error.c_str(); }
 extern "C" const char* dufwi_version(void) { return "dufwi-b200 0.1.0 (sm_100a)"; }

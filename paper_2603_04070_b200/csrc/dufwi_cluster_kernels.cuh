@@ -1,19 +1,26 @@
 // Cluster engine: one kernel launch per sweep, one thread-block cluster per unit.
 //
-// For grids whose per-unit state fits the cluster's shared memory (configs
-// 0/1: 160^2; config 2: 296^2) the whole time loop runs inside one launch.
-// The unit's grid is cut into `cs` slabs of `rows` x-rows, one per CTA of the
-// cluster.  Each CTA keeps its slab of every live field (u[t-1], u[t-2] for the
-// forward; lam[t+1], lam[t+2], u[t], u[t-1] for the adjoint) plus one halo row
-// on each side in shared memory.  After a CTA updates a boundary row it pushes
-// the new values straight into the neighbour CTA's halo row through
-// distributed shared memory (st.shared::cluster); one cluster barrier per time
-// step orders those pushes against the next step's reads.  HBM then only sees
-// the receiver samples, the 1-cell ring strips and the final two states — the
-// "temporal blocking in the extreme" of SURVEY §7.1-5.
+// For grids whose per-unit state fits a cluster (configs 0/1: 160^2) the whole
+// time loop of a sweep runs inside one launch ("temporal blocking in the
+// extreme").  The unit's grid is cut into `cs` slabs of `rows`
+// x-rows, one per CTA.  Inside a CTA thread (seg, z) owns column z of rows
+// [seg*RPT, seg*RPT+RPT): its cells' state (u[t-1], u[t-2] forward; lam[t+1],
+// lam[t+2], u[t], u[t-1] adjoint), E/dx^2 and the imaging accumulators live in
+// f64 REGISTERS for the whole sweep.  Per time step a thread
+//   * reads z-neighbours from a double-buffered shared-memory exchange row,
+//   * takes x-neighbours from its own registers, from the exchange rows of the
+//     adjacent segment, or from the halo rows of the buffer,
+//   * writes its new value into the exchange buffer; threads owning the slab's
+//     first/last row also push it into the neighbouring CTA's halo row with
+//     st.async (DSMEM), completing bytes on that CTA's mbarrier.
+// A step then costs one __syncthreads and one mbarrier phase wait — no
+// cluster-wide barrier, no GPU-scope fence, no L1 invalidation.  HBM only sees
+// receiver samples, the 1-cell ring strips and the final two states.
 //
-// Numerics are the stepwise engine's: f32 storage, f64 per-cell arithmetic in
-// the reference's operation order.
+// Numerics: f64 state and arithmetic in the reference's operation order; the
+// exchange rows are f64 when they fit shared memory (T = double), making the
+// sweep a plain float64 computation; receiver samples, strips and the final
+// states are stored f32 (the ChannelData/workspace format).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -25,313 +32,495 @@ namespace dufwi {
 namespace cg = cooperative_groups;
 
 struct ClusterCfg {
-  int cs = 0;        // CTAs per cluster (slabs per unit)
-  int rows = 0;      // x-rows per slab
-  int threads = 0;   // threads per CTA
+  int cs = 0;       // CTAs per cluster (slabs per unit)
+  int rows = 0;     // x-rows per slab
+  int rpt = 0;      // rows per thread (template instance)
+  int nseg = 0;     // thread segments per column
+  int threads = 0;  // threads per CTA = nz * nseg
+  int dbl = 0;      // exchange rows in f64 (1) or f32 (0)
   size_t smem_fwd = 0, smem_adj = 0;
 };
 
-constexpr int kClusterThreads = 512;
+constexpr int kClusterMaxThreads = 512;  // 128 registers per thread available
 
-__device__ __forceinline__ void cluster_barrier() {
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; "
+      "@!p bra WAIT_%=; }" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void push_async(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void push_async(uint32_t raddr, float v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "r"(__float_as_uint(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-// shared-memory carve-up (all offsets 16-byte aligned)
-struct SmemPlan {
-  size_t fA, fB, fC, fD;   // field buffers, (rows+2) x nz floats each
-  size_t ed;               // (rows+2) x nz doubles (E/dx^2, halo rows included)
-  size_t acc;              // rows x nz doubles (adjoint imaging accumulator)
-  size_t px, pz;           // rows / nz doubles
-  size_t total;
-};
-
-__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
-
-__host__ __device__ inline SmemPlan smem_plan(int rows, int nz, bool adjoint) {
-  SmemPlan p{};
-  const size_t fb = al16((size_t)(rows + 2) * nz * sizeof(float));
-  size_t o = 0;
-  p.fA = o; o += fb;
-  p.fB = o; o += fb;
-  if (adjoint) { p.fC = o; o += fb; p.fD = o; o += fb; } else { p.fC = p.fD = 0; }
-  p.ed = o; o += al16((size_t)(rows + 2) * nz * sizeof(double));
-  if (adjoint) { p.acc = o; o += al16((size_t)rows * nz * sizeof(double)); } else { p.acc = 0; }
-  p.px = o; o += al16((size_t)rows * sizeof(double));
-  p.pz = o; o += al16((size_t)nz * sizeof(double));
-  p.total = o;
-  return p;
+// ------------------------------------------------------------ smem layout
+// [nbufs exchange buffers of (rows+2) x (nz+2) T] [rows x nz double2 (A, B)] [2 mbarriers]
+template <class T>
+__host__ __device__ inline size_t xbuf_elems(int rows, int nz) {
+  return (size_t)(rows + 2) * (nz + 2);
+}
+template <class T>
+__host__ __device__ inline size_t ab_offset(int rows, int nz, int nbufs) {
+  return ((size_t)nbufs * xbuf_elems<T>(rows, nz) * sizeof(T) + 15) & ~(size_t)15;
+}
+template <class T>
+__host__ __device__ inline size_t bar_offset(int rows, int nz, int nbufs) {
+  return ab_offset<T>(rows, nz, nbufs) + (size_t)rows * nz * sizeof(double2);
+}
+template <class T>
+__host__ __device__ inline size_t cluster_smem_bytes(int rows, int nz, int nbufs) {
+  return bar_offset<T>(rows, nz, nbufs) + 2 * sizeof(uint64_t);
 }
 
-// Slab geometry of this CTA.
-struct Slab {
-  int rank, cs, rows, r0, nr;  // rows [r0, r0+nr)
+// Per-thread static description of its cells.
+struct CellCtx {
+  int rank, cs, rows, nr, r0;  // slab of this CTA: global rows [r0, r0+nr)
+  int seg, z, lrow0;           // thread: column z, local rows lrow0 .. lrow0+RPT-1
+  int W;                       // exchange row stride (nz + 2)
+  bool has_up, has_dn;         // CTA rank-1 / rank+1 exist with rows
 };
 
-__device__ __forceinline__ Slab my_slab(int cs, int rows, int nx) {
-  Slab s;
-  s.cs = cs;
-  s.rows = rows;
-  s.rank = (int)cg::this_cluster().block_rank();
-  s.r0 = s.rank * rows;
-  s.nr = max(0, min(nx, s.r0 + rows) - s.r0);
-  return s;
+__device__ __forceinline__ CellCtx make_ctx(int cs, int rows, int nx, int nz, int rpt) {
+  CellCtx c;
+  c.rank = (int)cg::this_cluster().block_rank();
+  c.cs = cs;
+  c.rows = rows;
+  c.r0 = c.rank * rows;
+  c.nr = max(0, min(nx, c.r0 + rows) - c.r0);
+  c.seg = threadIdx.x / nz;
+  c.z = threadIdx.x - c.seg * nz;
+  c.lrow0 = c.seg * rpt;
+  c.W = nz + 2;
+  c.has_up = c.rank > 0 && c.nr > 0;
+  c.has_dn = c.nr > 0 && c.rank + 1 < cs && (c.rank + 1) * rows < nx;
+  return c;
 }
 
-// Push a freshly computed boundary value of local slab row xr (1-based) into
-// the neighbouring CTAs' halo rows of the same buffer.
-__device__ __forceinline__ void push_halo(float* buf, const Slab& sl, int xr, int z, int nz,
-                                          int nx, float v) {
-  if (xr == 1 && sl.rank > 0) {
-    float* dst = cg::this_cluster().map_shared_rank(buf, sl.rank - 1);
-    dst[(size_t)(sl.rows + 1) * nz + z] = v;
+// Ring-strip slot of cell (x, z) (layout of the stepwise engine), or -1.
+__device__ __forceinline__ int ring_index(const Geo& g, int x, int z) {
+  if (z >= g.z_lo && z <= g.z_hi) {
+    if (x == g.x_lo - 1) return z - g.z_lo;
+    if (x == g.x_hi + 1) return g.Lz + z - g.z_lo;
   }
-  if (xr == sl.nr && sl.rank + 1 < sl.cs && (sl.rank + 1) * sl.rows < nx) {
-    float* dst = cg::this_cluster().map_shared_rank(buf, sl.rank + 1);
-    dst[z] = v;
+  if (x >= g.x_lo && x <= g.x_hi) {
+    if (z == g.z_lo - 1) return 2 * g.Lz + x - g.x_lo;
+    if (z == g.z_hi + 1) return 2 * g.Lz + g.Lx + x - g.x_lo;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ bool in_box(const Geo& g, int x, int z) {
+  return x >= g.x_lo && x <= g.x_hi && z >= g.z_lo && z <= g.z_hi;
+}
+
+// Static per-cell data loaded once per sweep.
+template <int RPT>
+struct CellStatic {
+  double ed[RPT];
+  int slot[RPT];
+  int ring[RPT];
+  unsigned active, src, interior;
+  bool pushes_up, pushes_dn;  // owns the slab's first / last row
+  const double2* ab;          // shared (A, B) table, row stride nz
+};
+
+template <int RPT>
+__device__ __forceinline__ void load_static(const Geo& g, const Model& m, const CellCtx& c,
+                                            size_t pb, int txx, int txz, double2* ab_table,
+                                            CellStatic<RPT>& st) {
+  st.active = st.src = st.interior = 0u;
+  st.ab = ab_table;
+  st.pushes_up = c.has_up && c.lrow0 == 0;
+  st.pushes_dn = false;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int lr = c.lrow0 + j;
+    st.ed[j] = 0.0;
+    st.slot[j] = -1;
+    st.ring[j] = -1;
+    if (lr < c.nr) {
+      const int x = c.r0 + lr;
+      st.active |= 1u << j;
+      st.ed[j] = m.Ed[pb + (size_t)x * g.nz + c.z];
+      double A, B;
+      ab_coeffs(damping_at(g, x, c.z), g.dt, A, B);
+      ab_table[(size_t)lr * g.nz + c.z] = make_double2(A, B);
+      if (g.row_flag[x]) st.slot[j] = g.node_slot[(size_t)x * g.nz + c.z];
+      st.ring[j] = ring_index(g, x, c.z);
+      if (x == txx && c.z == txz) st.src |= 1u << j;
+      if (in_box(g, x, c.z)) st.interior |= 1u << j;
+      if (lr == c.nr - 1 && c.has_dn) st.pushes_dn = true;
+    }
+  }
+}
+
+// x-neighbours of cell j of a thread column: register when the neighbour is the
+// thread's own cell, else the exchange buffer row (adjacent segment or halo).
+// Row index in the buffer is lr + 1 (row 0 = top halo).
+template <int RPT, class T>
+__device__ __forceinline__ void x_neighbours(const CellCtx& c, const double (&v)[RPT],
+                                             const T* X, double (&xm)[RPT], double (&xp)[RPT]) {
+  const int W = c.W, z = c.z;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int lr = min(c.lrow0 + j, c.rows - 1);
+    xm[j] = j > 0 ? v[j - 1] : (double)X[(size_t)lr * W + z + 1];
+    const bool own_next = j < RPT - 1 && c.lrow0 + j + 1 < c.nr;
+    xp[j] = own_next ? v[j + 1] : (double)X[(size_t)(lr + 2) * W + z + 1];
   }
 }
 
 // ---------------------------------------------------------------------------
-// forward sweep (MODE 0 none / 1 full history / 2 strips)
-template <bool RHO, int MODE>
-__global__ void __launch_bounds__(kClusterThreads, 1)
+// forward step i (time t = i).  u1 = u[t-1] (read), u2 = u[t-2] -> u[t].
+// Reads exchange buffer Xr (step i-1), writes Xw (step i) and pushes the slab's
+// boundary rows into the neighbours' Xw halo rows (mbarrier `bar_w` remote).
+template <int RPT, class T, int MODE>
+__device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
+                                         double (&u1)[RPT], double (&u2)[RPT], int t, int U,
+                                         int lu, const T* Xr, T* Xw, uint32_t bar_r,
+                                         uint32_t bar_w, uint32_t tx_bytes, double pulse_t,
+                                         float* __restrict__ rec, float* __restrict__ hist,
+                                         float* __restrict__ strips, size_t N2) {
+  const int W = c.W, z = c.z;
+  __syncthreads();  // exchange rows of step i-1 complete; Xw free for reuse
+  if (t >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((t - 1) >> 1) & 1);
+  if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
+  double xm[RPT], xp[RPT], zm[RPT], zp[RPT], v[RPT];
+  x_neighbours<RPT, T>(c, u1, Xr, xm, xp);
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int lr = min(c.lrow0 + j, c.rows - 1);
+    zm[j] = (double)Xr[(size_t)(lr + 1) * W + z];
+    zp[j] = (double)Xr[(size_t)(lr + 1) * W + z + 2];
+  }
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const double lap = (((-4.0 * u1[j] + xm[j]) + xp[j]) + zm[j]) + zp[j];
+    const double2 ab = s.ab[(size_t)min(c.lrow0 + j, c.rows - 1) * g.nz + z];
+    v[j] = ab.x * u1[j] + ab.y * u2[j] + s.ed[j] * lap;
+    if (s.src & (1u << j)) v[j] += pulse_t;
+  }
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    if (!(s.active & (1u << j))) continue;
+    const int lr = c.lrow0 + j;
+    u2[j] = v[j];
+    Xw[(size_t)(lr + 1) * W + z + 1] = (T)v[j];
+    if (lr == 0 && s.pushes_up)  // my first row -> bottom halo of rank-1
+      push_async(mapa_rank(smem_addr(Xw + (size_t)(c.rows + 1) * W + z + 1), c.rank - 1), (T)v[j],
+                 mapa_rank(bar_w, c.rank - 1));
+    if (lr == c.nr - 1 && s.pushes_dn)  // my last row -> top halo of rank+1
+      push_async(mapa_rank(smem_addr(Xw + z + 1), c.rank + 1), (T)v[j],
+                 mapa_rank(bar_w, c.rank + 1));
+    const float vf = (float)v[j];
+    if (s.slot[j] >= 0) rec[((size_t)t * U + lu) * g.M + s.slot[j]] = vf;
+    const int x = c.r0 + lr;
+    if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)x * g.nz + z] = vf;
+    if (MODE == 2 && s.ring[j] >= 0) strips[((size_t)t * U + lu) * g.SL + s.ring[j]] = vf;
+  }
+}
+
+template <int RPT, class T, int MODE>
+__global__ void __launch_bounds__(kClusterMaxThreads, 1)
     cluster_fwd_kernel(Geo g, Model m, int cs, int rows, int unit_begin, int U,
                        float* __restrict__ rec, float* __restrict__ hist,
                        float* __restrict__ strips, float* __restrict__ ubuf) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const Slab sl = my_slab(cs, rows, g.nx);
-  const int nz = g.nz;
-  const SmemPlan sp = smem_plan(rows, nz, false);
-  float* P[2] = {reinterpret_cast<float*>(smem + sp.fA), reinterpret_cast<float*>(smem + sp.fB)};
-  double* eds = reinterpret_cast<double*>(smem + sp.ed);
-  double* pxs = reinterpret_cast<double*>(smem + sp.px);
-  double* pzs = reinterpret_cast<double*>(smem + sp.pz);
-
+  const CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT);
   const int lu = blockIdx.x / cs;
   const int u = unit_begin + lu;
   const int b = u / g.S;
   const int s = u - b * g.S;
-  const size_t N2 = (size_t)g.nx * nz;
+  const size_t N2 = (size_t)g.nx * g.nz;
   const size_t pb = (size_t)b * N2;
-  const int txx = g.tx[2 * s], txz = g.tx[2 * s + 1];
-  const int tid = threadIdx.x, T = blockDim.x;
-  const int halo_n = (rows + 2) * nz;
-  const int ncell = sl.nr * nz;
-
-  for (int i = tid; i < halo_n; i += T) { P[0][i] = 0.f; P[1][i] = 0.f; }
-  for (int i = tid; i < ncell; i += T) eds[nz + i] = m.Ed[pb + (size_t)sl.r0 * nz + i];
-  for (int i = tid; i < sl.nr; i += T) pxs[i] = g.px ? g.px[sl.r0 + i] : 0.0;
-  for (int i = tid; i < nz; i += T) pzs[i] = g.pz ? g.pz[i] : 0.0;
-  cluster_barrier();
-
-  for (int t = 0; t < g.nt; ++t) {
-    const float* u1 = P[(t + 1) & 1];
-    float* u2 = P[t & 1];
-    const double pulse_t = g.pulse[t];
-    float* rec_t = rec + ((size_t)t * U + lu) * g.M;
-    for (int i = tid; i < ncell; i += T) {
-      const int xr = i / nz + 1;
-      const int z = i - (xr - 1) * nz;
-      const int x = sl.r0 + xr - 1;
-      const int k = xr * nz + z;
-      const double uc = u1[k];
-      const double xm = u1[k - nz], xp = u1[k + nz];
-      const double zm = z > 0 ? (double)u1[k - 1] : 0.0;
-      const double zp = z < nz - 1 ? (double)u1[k + 1] : 0.0;
-      double lap;
-      if (RHO) {
-        const RhoW w = rho_weights(m.rho + pb, m.q + pb, g.nx, nz, x, z);
-        lap = (((-w.W * uc + w.xm * xm) + w.xp * xp) + w.zm * zm) + w.zp * zp;
-      } else {
-        lap = (((-4.0 * uc + xm) + xp) + zm) + zp;
-      }
-      double A, Bc;
-      const double D = g.px ? fmax(pxs[xr - 1], pzs[z]) : g.d2d[(size_t)x * nz + z];
-      ab_coeffs(D, g.dt, A, Bc);
-      double v = A * uc + Bc * (double)u2[k] + eds[k] * lap;
-      if (x == txx && z == txz) v += pulse_t;
-      const float vf = (float)v;
-      u2[k] = vf;
-      push_halo(u2, sl, xr, z, nz, g.nx, vf);
-      if (g.row_flag[x]) {
-        const int slot = g.node_slot[(size_t)x * nz + z];
-        if (slot >= 0) rec_t[slot] = vf;
-      }
-      if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)x * nz + z] = vf;
-      if (MODE == 2) {
-        float* st = strips + ((size_t)t * U + lu) * g.SL;
-        if (z >= g.z_lo && z <= g.z_hi) {
-          if (x == g.x_lo - 1) st[z - g.z_lo] = vf;
-          if (x == g.x_hi + 1) st[g.Lz + z - g.z_lo] = vf;
-        }
-        if (x >= g.x_lo && x <= g.x_hi) {
-          if (z == g.z_lo - 1) st[2 * g.Lz + x - g.x_lo] = vf;
-          if (z == g.z_hi + 1) st[2 * g.Lz + g.Lx + x - g.x_lo] = vf;
-        }
-      }
-    }
-    cluster_barrier();
+  const size_t xe = xbuf_elems<T>(rows, g.nz);
+  T* X[2] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem) + xe};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, g.nz, 2));
+  const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
+  for (size_t i = threadIdx.x; i < 2 * xe; i += blockDim.x) X[0][i] = T(0);
+  if (threadIdx.x == 0) {
+    mbar_init(bar[0], 1);
+    mbar_init(bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  CellStatic<RPT> st;
+  load_static<RPT>(g, m, c, pb, g.tx[2 * s], g.tx[2 * s + 1],
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 2)), st);
+  const uint32_t tx_bytes = (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T);
+  double ua[RPT], ub[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) ua[j] = ub[j] = 0.0;
+  const bool owns_src = st.src != 0u;
+  double p_next = owns_src ? g.pulse[0] : 0.0;
+  cluster_sync_all();  // barriers initialised and buffers zeroed cluster-wide
+
+  // step t writes X[t & 1] / bar[t & 1]; ub receives u[t] at even t, ua at odd t
+  int t = 0;
+  for (; t + 1 < g.nt; t += 2) {
+    double p = p_next;
+    if (owns_src) p_next = g.pulse[t + 1];
+    fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, X[1], X[0], bar[1], bar[0], tx_bytes, p,
+                           rec, hist, strips, N2);
+    p = p_next;
+    if (owns_src && t + 2 < g.nt) p_next = g.pulse[t + 2];
+    fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, X[0], X[1], bar[0], bar[1], tx_bytes, p,
+                           rec, hist, strips, N2);
+  }
+  if (t < g.nt)
+    fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, X[1], X[0], bar[1], bar[0], tx_bytes,
+                           p_next, rec, hist, strips, N2);
+  // drain the last step's incoming pushes before any CTA of the cluster exits
+  if (c.has_up || c.has_dn) mbar_wait(bar[(g.nt - 1) & 1], ((g.nt - 1) >> 1) & 1);
+  cluster_sync_all();
+
   if (MODE != 1) {
-    // final two states for the adjoint's reconstruction, in the stepwise
-    // engine's ping-pong layout: ubuf[t & 1][lu] holds u[t].
-    for (int k2 = 0; k2 < 2; ++k2) {
-      float* dst = ubuf + ((size_t)k2 * U + lu) * N2 + (size_t)sl.r0 * nz;
-      const float* src = P[k2] + nz;
-      for (int i = tid; i < ncell; i += T) dst[i] = src[i];
+    // final two states in the stepwise-engine layout: ubuf[t & 1][lu] holds u[t]
+    const bool last_odd = ((g.nt - 1) & 1) != 0;
+    float* d_last = ubuf + ((size_t)((g.nt - 1) & 1) * U + lu) * N2;
+    float* d_prev = ubuf + ((size_t)((g.nt - 2) & 1) * U + lu) * N2;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      if (!(st.active & (1u << j))) continue;
+      const size_t cell = (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z;
+      d_last[cell] = (float)(last_odd ? ua[j] : ub[j]);
+      d_prev[cell] = (float)(last_odd ? ub[j] : ua[j]);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// adjoint sweep (MODE 1 full history / 2 strip reconstruction).  Writes the
-// unit's imaging sum over time into acc_unit[lu][cell] (f64).
-template <bool RHO, int MODE>
-__global__ void __launch_bounds__(kClusterThreads, 1)
+// adjoint step i (time t = nt-1-i).  l1 = lam[t+1], l2 = lam[t+2] -> lam[t];
+// ua = u[t] -> u[t-2] (reconstruction, MODE 2), ub = u[t-1].
+// XL: exchange of E*lam, XU: exchange of u (MODE 2).  Buffers/bars indexed by i.
+template <int RPT, class T, int MODE>
+__device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
+                                         double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
+                                         double (&ub)[RPT], double (&acc)[RPT], int i, int U,
+                                         int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
+                                         uint32_t bar_r, uint32_t bar_w, uint32_t tx_bytes,
+                                         double pulse_t, const double* __restrict__ rres,
+                                         const float* __restrict__ hist,
+                                         const float* __restrict__ strips, size_t N2) {
+  const int W = c.W, z = c.z;
+  const int t = g.nt - 1 - i;
+  // this step's global reads first, so their latency overlaps the syncs
+  double rr[RPT];
+  float ring_v[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    rr[j] = s.slot[j] >= 0 ? rres[((size_t)t * U + lu) * g.M + s.slot[j]] : 0.0;
+    ring_v[j] = (MODE == 2 && s.ring[j] >= 0 && t >= 2)
+                    ? strips[((size_t)(t - 2) * U + lu) * g.SL + s.ring[j]]
+                    : 0.f;
+  }
+  __syncthreads();
+  if (i >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((i - 1) >> 1) & 1);
+  if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
+
+  // lam[t] = A lam1 + L^T(E lam1) + B lam2 (+ residual), reference order
+  double el[RPT], xm[RPT], xp[RPT], lam[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) el[j] = s.ed[j] * l1[j];
+  x_neighbours<RPT, T>(c, el, XLr, xm, xp);
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int lr = min(c.lrow0 + j, c.rows - 1);
+    const size_t o = (size_t)(lr + 1) * W + z + 1;
+    const double adj = (((-4.0 * el[j] + xm[j]) + xp[j]) + (double)XLr[o - 1]) + (double)XLr[o + 1];
+    const double2 ab = s.ab[(size_t)lr * g.nz + z];
+    lam[j] = ab.x * l1[j] + adj + ab.y * l2[j] + rr[j];
+  }
+  // imaging with L(u[t-1]) and reconstruction of u[t-2]
+  double lapu[RPT];
+  if (MODE == 2) {
+    double fxm[RPT], fxp[RPT];
+    x_neighbours<RPT, T>(c, ub, XUr, fxm, fxp);
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int lr = min(c.lrow0 + j, c.rows - 1);
+      const size_t o = (size_t)(lr + 1) * W + z + 1;
+      lapu[j] = (((-4.0 * ub[j] + fxm[j]) + fxp[j]) + (double)XUr[o - 1]) + (double)XUr[o + 1];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      lapu[j] = 0.0;
+      if (t >= 1 && (s.active & (1u << j))) {
+        const float* F = hist + ((size_t)(t - 1) * U + lu) * N2;
+        const int x = c.r0 + c.lrow0 + j;
+        const size_t cell = (size_t)x * g.nz + z;
+        const double fxm = x > 0 ? (double)F[cell - g.nz] : 0.0;
+        const double fxp = x < g.nx - 1 ? (double)F[cell + g.nz] : 0.0;
+        const double fzm = z > 0 ? (double)F[cell - 1] : 0.0;
+        const double fzp = z < g.nz - 1 ? (double)F[cell + 1] : 0.0;
+        lapu[j] = (((-4.0 * (double)F[cell] + fxm) + fxp) + fzm) + fzp;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    if (!(s.active & (1u << j))) continue;
+    const int lr = c.lrow0 + j;
+    const size_t o = (size_t)(lr + 1) * W + z + 1;
+    l2[j] = lam[j];
+    const T elw = (T)(s.ed[j] * lam[j]);
+    XLw[o] = elw;
+    if (t >= 1) {
+      if (MODE == 1) {
+        acc[j] += lapu[j] * lam[j];
+      } else if (s.interior & (1u << j)) {
+        acc[j] += lapu[j] * lam[j];
+        if (t >= 2) {
+          double prev = 2.0 * ub[j] + s.ed[j] * lapu[j] - ua[j];
+          if (s.src & (1u << j)) prev += pulse_t;
+          ua[j] = prev;
+        }
+      } else if (s.ring[j] >= 0 && t >= 2) {
+        ua[j] = (double)ring_v[j];  // ring cell: the saved strip stands in for the reconstruction
+      }
+    }
+    const T uw = (T)ua[j];
+    if (MODE == 2) XUw[o] = uw;
+    if (lr == 0 && s.pushes_up) {
+      const uint32_t rb = mapa_rank(bar_w, c.rank - 1);
+      const size_t ho = (size_t)(c.rows + 1) * W + z + 1;
+      push_async(mapa_rank(smem_addr(XLw + ho), c.rank - 1), elw, rb);
+      if (MODE == 2) push_async(mapa_rank(smem_addr(XUw + ho), c.rank - 1), uw, rb);
+    }
+    if (lr == c.nr - 1 && s.pushes_dn) {
+      const uint32_t rb = mapa_rank(bar_w, c.rank + 1);
+      push_async(mapa_rank(smem_addr(XLw + z + 1), c.rank + 1), elw, rb);
+      if (MODE == 2) push_async(mapa_rank(smem_addr(XUw + z + 1), c.rank + 1), uw, rb);
+    }
+  }
+}
+
+template <int RPT, class T, int MODE>
+__global__ void __launch_bounds__(kClusterMaxThreads, 1)
     cluster_adj_kernel(Geo g, Model m, int cs, int rows, int unit_begin, int U,
                        const double* __restrict__ rres, const float* __restrict__ hist,
                        const float* __restrict__ strips, const float* __restrict__ ubuf,
-                       double* __restrict__ acc_unit, int acc_off) {
+                       double* __restrict__ acc_part, int acc_off) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const Slab sl = my_slab(cs, rows, g.nx);
-  const int nz = g.nz;
-  const SmemPlan sp = smem_plan(rows, nz, true);
-  float* Lb[2] = {reinterpret_cast<float*>(smem + sp.fA), reinterpret_cast<float*>(smem + sp.fB)};
-  float* Ub[2] = {reinterpret_cast<float*>(smem + sp.fC), reinterpret_cast<float*>(smem + sp.fD)};
-  double* eds = reinterpret_cast<double*>(smem + sp.ed);
-  double* acc = reinterpret_cast<double*>(smem + sp.acc);
-  double* pxs = reinterpret_cast<double*>(smem + sp.px);
-  double* pzs = reinterpret_cast<double*>(smem + sp.pz);
-
+  const CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT);
   const int lu = blockIdx.x / cs;
   const int u = unit_begin + lu;
   const int b = u / g.S;
   const int s = u - b * g.S;
-  const size_t N2 = (size_t)g.nx * nz;
+  const size_t N2 = (size_t)g.nx * g.nz;
   const size_t pb = (size_t)b * N2;
-  const int txx = g.tx[2 * s], txz = g.tx[2 * s + 1];
-  const int tid = threadIdx.x, T = blockDim.x;
-  const int halo_n = (rows + 2) * nz;
-  const int ncell = sl.nr * nz;
-
-  for (int i = tid; i < halo_n; i += T) {
-    Lb[0][i] = 0.f;
-    Lb[1][i] = 0.f;
-    const int x = sl.r0 - 1 + i / nz;  // global row of this smem row
-    const bool in = x >= 0 && x < g.nx && (i / nz) <= sl.nr + 1;
-    double e = 0.0;
-    if (in) e = m.Ed[pb + (size_t)x * nz + (i % nz)];
-    eds[i] = e;
-    if (MODE == 2) {
-      Ub[0][i] = in ? ubuf[((size_t)0 * U + lu) * N2 + (size_t)x * nz + (i % nz)] : 0.f;
-      Ub[1][i] = in ? ubuf[((size_t)1 * U + lu) * N2 + (size_t)x * nz + (i % nz)] : 0.f;
+  const int W = c.W;
+  const size_t xe = xbuf_elems<T>(rows, g.nz);
+  T* base = reinterpret_cast<T*>(smem);
+  T* XL[2] = {base, base + xe};
+  T* XU[2] = {base + 2 * xe, base + 3 * xe};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, g.nz, 4));
+  const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
+  for (size_t k = threadIdx.x; k < 4 * xe; k += blockDim.x) base[k] = T(0);
+  if (threadIdx.x == 0) {
+    mbar_init(bar[0], 1);
+    mbar_init(bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  CellStatic<RPT> st;
+  load_static<RPT>(g, m, c, pb, g.tx[2 * s], g.tx[2 * s + 1],
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 4)), st);
+  const int per = MODE == 2 ? 2 : 1;
+  const uint32_t tx_bytes =
+      (uint32_t)(per * ((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T));
+  const int nt = g.nt;
+  const float* u_last = ubuf + ((size_t)((nt - 1) & 1) * U + lu) * N2;
+  const float* u_prev = ubuf + ((size_t)((nt - 2) & 1) * U + lu) * N2;
+  __syncthreads();  // zero fill done before the u[nt-2] exchange rows are written
+  // step i = 0 reads XU[1] = u[nt-2] (own rows and both halo rows from global)
+  if (MODE == 2 && c.nr > 0) {
+    for (int k = threadIdx.x; k < (c.nr + 2) * g.nz; k += blockDim.x) {
+      const int r = k / g.nz, zz = k - r * g.nz;
+      const int x = c.r0 - 1 + r;
+      if (x >= 0 && x < g.nx) XU[1][(size_t)r * W + zz + 1] = (T)u_prev[(size_t)x * g.nz + zz];
     }
   }
-  for (int i = tid; i < ncell; i += T) acc[i] = 0.0;
-  for (int i = tid; i < sl.nr; i += T) pxs[i] = g.px ? g.px[sl.r0 + i] : 0.0;
-  for (int i = tid; i < nz; i += T) pzs[i] = g.pz ? g.pz[i] : 0.0;
-  cluster_barrier();
-
-  for (int t = g.nt - 1; t >= 0; --t) {
-    const float* l1 = Lb[(t + 1) & 1];
-    float* l2 = Lb[t & 1];
-    float* ut = Ub[t & 1];          // u[t]   -> u[t-2] in place
-    const float* um = Ub[(t + 1) & 1];  // u[t-1]
-    const double* rr = rres + ((size_t)t * U + lu) * g.M;
-    const float* st = MODE == 2 && t >= 1 ? strips + ((size_t)(t - 1) * U + lu) * g.SL : nullptr;
-    const float* F = MODE == 1 && t >= 1 ? hist + ((size_t)(t - 1) * U + lu) * N2 : nullptr;
-    const double pulse_t = g.pulse[t];
-    for (int i = tid; i < ncell; i += T) {
-      const int xr = i / nz + 1;
-      const int z = i - (xr - 1) * nz;
-      const int x = sl.r0 + xr - 1;
-      const int k = xr * nz + z;
-      const bool okzm = z > 0, okzp = z < nz - 1;
-      double A, Bc;
-      const double D = g.px ? fmax(pxs[xr - 1], pzs[z]) : g.d2d[(size_t)x * nz + z];
-      ab_coeffs(D, g.dt, A, Bc);
-      // lam[t] = A lam1 + L^T(E lam1) + B lam2  (+ residual)
-      const double lc = l1[k];
-      const double ec = eds[k];
-      double adj;
-      RhoW w{1.0, 1.0, 1.0, 1.0, 4.0};
-      if (RHO) {
-        const double* rho = m.rho + pb;
-        const double* q = m.q + pb;
-        const size_t c = (size_t)x * nz + z;
-        w = rho_weights(rho, q, g.nx, nz, x, z);
-        adj = -w.W * ec * lc;
-        if (x > 0) adj += rho_in_weight(rho, q, c, c - nz) * eds[k - nz] * (double)l1[k - nz];
-        if (x < g.nx - 1) adj += rho_in_weight(rho, q, c, c + nz) * eds[k + nz] * (double)l1[k + nz];
-        if (okzm) adj += rho_in_weight(rho, q, c, c - 1) * eds[k - 1] * (double)l1[k - 1];
-        if (okzp) adj += rho_in_weight(rho, q, c, c + 1) * eds[k + 1] * (double)l1[k + 1];
-      } else {
-        adj = -4.0 * ec * lc;
-        adj += eds[k - nz] * (double)l1[k - nz];
-        adj += eds[k + nz] * (double)l1[k + nz];
-        if (okzm) adj += eds[k - 1] * (double)l1[k - 1];
-        if (okzp) adj += eds[k + 1] * (double)l1[k + 1];
-      }
-      double lam = A * lc + adj + Bc * (double)l2[k];
-      if (g.row_flag[x]) {
-        const int slot = g.node_slot[(size_t)x * nz + z];
-        if (slot >= 0) lam += rr[slot];
-      }
-      const float lf = (float)lam;
-      l2[k] = lf;
-      push_halo(l2, sl, xr, z, nz, g.nx, lf);
-      if (t >= 1) {
-        if (MODE == 1) {
-          const size_t c = (size_t)x * nz + z;
-          const double fc = F[c];
-          const double xm = x > 0 ? (double)F[c - nz] : 0.0;
-          const double xp = x < g.nx - 1 ? (double)F[c + nz] : 0.0;
-          const double zm = okzm ? (double)F[c - 1] : 0.0;
-          const double zp = okzp ? (double)F[c + 1] : 0.0;
-          const double lapu = RHO ? ((((-w.W * fc + w.xm * xm) + w.xp * xp) + w.zm * zm) + w.zp * zp)
-                                  : ((((-4.0 * fc + xm) + xp) + zm) + zp);
-          acc[i] += lapu * lam;
-        } else if (x >= g.x_lo && x <= g.x_hi && z >= g.z_lo && z <= g.z_hi) {
-          const double fc = um[k];
-          const double xm = x > g.x_lo ? (double)um[k - nz] : (x > 0 ? (double)st[z - g.z_lo] : 0.0);
-          const double xp = x < g.x_hi ? (double)um[k + nz]
-                                       : (x < g.nx - 1 ? (double)st[g.Lz + z - g.z_lo] : 0.0);
-          const double zm = z > g.z_lo ? (double)um[k - 1]
-                                       : (z > 0 ? (double)st[2 * g.Lz + x - g.x_lo] : 0.0);
-          const double zp = z < g.z_hi ? (double)um[k + 1]
-                                       : (z < nz - 1 ? (double)st[2 * g.Lz + g.Lx + x - g.x_lo] : 0.0);
-          const double lapu = RHO ? ((((-w.W * fc + w.xm * xm) + w.xp * xp) + w.zm * zm) + w.zp * zp)
-                                  : ((((-4.0 * fc + xm) + xp) + zm) + zp);
-          acc[i] += lapu * lam;
-          if (t >= 2) {
-            double prev = 2.0 * fc + ec * lapu - (double)ut[k];
-            if (x == txx && z == txz) prev += pulse_t;
-            const float pf = (float)prev;
-            ut[k] = pf;
-            push_halo(ut, sl, xr, z, nz, g.nx, pf);
-          }
-        }
-      }
+  double la[RPT], lb[RPT], ua[RPT], ub[RPT], acc[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    la[j] = lb[j] = acc[j] = ua[j] = ub[j] = 0.0;
+    if (MODE == 2 && (st.active & (1u << j))) {
+      const size_t cell = (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z;
+      ua[j] = u_last[cell];
+      ub[j] = u_prev[cell];
     }
-    cluster_barrier();
   }
-  double* dst = acc_unit + (size_t)(lu + acc_off) * N2 + (size_t)sl.r0 * nz;
-  for (int i = tid; i < ncell; i += T) dst[i] = acc[i];
+  const bool owns_src = st.src != 0u;
+  cluster_sync_all();
+
+  // step i writes XL[i&1], XU[i&1], bar[i&1]; reads XL[(i+1)&1], XU[(i+1)&1], bar[(i+1)&1]
+  int i = 0;
+  for (; i + 1 < nt; i += 2) {
+    const double p0 = owns_src ? g.pulse[nt - 1 - i] : 0.0;
+    adj_step<RPT, T, MODE>(g, c, st, la, lb, ua, ub, acc, i, U, lu, XL[1], XL[0], XU[1], XU[0],
+                           bar[1], bar[0], tx_bytes, p0, rres, hist, strips, N2);
+    const double p1 = owns_src ? g.pulse[nt - 2 - i] : 0.0;
+    adj_step<RPT, T, MODE>(g, c, st, lb, la, ub, ua, acc, i + 1, U, lu, XL[0], XL[1], XU[0], XU[1],
+                           bar[0], bar[1], tx_bytes, p1, rres, hist, strips, N2);
+  }
+  if (i < nt)
+    adj_step<RPT, T, MODE>(g, c, st, la, lb, ua, ub, acc, i, U, lu, XL[1], XL[0], XU[1], XU[0],
+                           bar[1], bar[0], tx_bytes, owns_src ? g.pulse[0] : 0.0, rres, hist,
+                           strips, N2);
+  if (c.has_up || c.has_dn) mbar_wait(bar[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
+  cluster_sync_all();
+  double* dst = acc_part + (size_t)(lu + acc_off) * N2;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j)
+    if (st.active & (1u << j)) dst[(size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = acc[j];
 }
 
 // ------------------------------------------------------------------ host side
 template <class K>
-inline bool cluster_fits(K kernel, int cs, size_t smem) {
-  if (smem > 227 * 1024) return false;
-  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return false;
-  if (cs > 8 && cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-    return false;
+inline int max_active_clusters(K kernel, int cs, int threads, size_t smem) {
+  if (smem > 227 * 1024 || threads > kClusterMaxThreads) return 0;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      (cs > 8 && cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) { cudaGetLastError(); return 0; }
+  if ((long)fa.numRegs * threads > 65536) return 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs);
-  cfg.blockDim = dim3(kClusterThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -343,44 +532,52 @@ inline bool cluster_fits(K kernel, int cs, size_t smem) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    return 0;
   }
-  return n > 0;
+  return n;
 }
 
-template <bool RHO>
-inline bool cluster_config_t(const Geo& g, ClusterCfg* out) {
-  // Prefer 16-CTA clusters (more SMs per unit, shortest per-step critical path),
-  // fall back to smaller clusters only if shared memory demands it.
-  for (int cs : {16, 8, 4}) {
-    const int rows = (g.nx + cs - 1) / cs;
-    if (rows < 2) continue;
-    const size_t sf = smem_plan(rows, g.nz, false).total;
-    const size_t sa = smem_plan(rows, g.nz, true).total;
-    if (sa > 220 * 1024) continue;
-    if (!cluster_fits(cluster_fwd_kernel<RHO, 0>, cs, sf)) continue;
-    if (!cluster_fits(cluster_adj_kernel<RHO, 2>, cs, sa)) continue;
-    cluster_fits(cluster_fwd_kernel<RHO, 1>, cs, sf);
-    cluster_fits(cluster_fwd_kernel<RHO, 2>, cs, sf);
-    cluster_fits(cluster_adj_kernel<RHO, 1>, cs, sa);
-    out->cs = cs;
-    out->rows = rows;
-    out->threads = kClusterThreads;
-    out->smem_fwd = sf;
-    out->smem_adj = sa;
-    return true;
-  }
-  return false;
+template <int RPT, class T>
+inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
+  const int rows = (g.nx + cs - 1) / cs;
+  if (rows < 2) return false;
+  const int nseg = (rows + RPT - 1) / RPT;
+  const int threads = g.nz * nseg;
+  if (threads > kClusterMaxThreads) return false;
+  const size_t sf = cluster_smem_bytes<T>(rows, g.nz, 2);
+  const size_t sa = cluster_smem_bytes<T>(rows, g.nz, 4);
+  if (max_active_clusters(cluster_fwd_kernel<RPT, T, 0>, cs, threads, sf) <= 0) return false;
+  if (max_active_clusters(cluster_fwd_kernel<RPT, T, 1>, cs, threads, sf) <= 0) return false;
+  if (max_active_clusters(cluster_fwd_kernel<RPT, T, 2>, cs, threads, sf) <= 0) return false;
+  if (max_active_clusters(cluster_adj_kernel<RPT, T, 1>, cs, threads, sa) <= 0) return false;
+  if (max_active_clusters(cluster_adj_kernel<RPT, T, 2>, cs, threads, sa) <= 0) return false;
+  out->cs = cs;
+  out->rows = rows;
+  out->rpt = RPT;
+  out->nseg = nseg;
+  out->threads = threads;
+  out->dbl = sizeof(T) == 8;
+  out->smem_fwd = sf;
+  out->smem_adj = sa;
+  return true;
 }
 
 inline bool cluster_config(const Geo& g, bool rho, ClusterCfg* out) {
+  if (rho) return false;  // density runs on the stepwise engine
   int dev = 0, major = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return false; }
-  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess || major < 10) {
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      major < 10) {
     cudaGetLastError();
     return false;
   }
-  return rho ? cluster_config_t<true>(g, out) : cluster_config_t<false>(g, out);
+  for (int cs : {16, 8}) {
+    if (try_cluster_cfg<4, double>(g, cs, out)) return true;
+    if (try_cluster_cfg<2, double>(g, cs, out)) return true;
+    if (try_cluster_cfg<4, float>(g, cs, out)) return true;
+    if (try_cluster_cfg<2, float>(g, cs, out)) return true;
+  }
+  return false;
 }
 
 template <class K, class... Args>
@@ -401,36 +598,52 @@ inline cudaError_t launch_cluster(K kernel, const ClusterCfg& c, int U, size_t s
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
-inline int cluster_forward(const Geo& g, const Model& m, const ClusterCfg& c, bool rho, int mode,
-                           int unit_begin, int U, float* rec, float* hist, float* strips,
-                           float* ubuf, cudaStream_t st) {
+template <int RPT, class T>
+inline cudaError_t cluster_forward_t(const Geo& g, const Model& m, const ClusterCfg& c, int mode,
+                                     int unit_begin, int U, float* rec, float* hist, float* strips,
+                                     float* ubuf, cudaStream_t st) {
+  if (mode == 0)
+    return launch_cluster(cluster_fwd_kernel<RPT, T, 0>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
+                          unit_begin, U, rec, hist, strips, ubuf);
+  if (mode == 1)
+    return launch_cluster(cluster_fwd_kernel<RPT, T, 1>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
+                          unit_begin, U, rec, hist, strips, ubuf);
+  return launch_cluster(cluster_fwd_kernel<RPT, T, 2>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
+                        unit_begin, U, rec, hist, strips, ubuf);
+}
+
+template <int RPT, class T>
+inline cudaError_t cluster_adjoint_t(const Geo& g, const Model& m, const ClusterCfg& c, int mode,
+                                     int unit_begin, int U, const double* rres, const float* hist,
+                                     const float* strips, const float* ubuf, double* acc_part,
+                                     int acc_off, cudaStream_t st) {
+  if (mode == 1)
+    return launch_cluster(cluster_adj_kernel<RPT, T, 1>, c, U, c.smem_adj, st, g, m, c.cs, c.rows,
+                          unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off);
+  return launch_cluster(cluster_adj_kernel<RPT, T, 2>, c, U, c.smem_adj, st, g, m, c.cs, c.rows,
+                        unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off);
+}
+
+inline int cluster_forward(const Geo& g, const Model& m, const ClusterCfg& c, bool /*rho*/,
+                           int mode, int unit_begin, int U, float* rec, float* hist,
+                           float* strips, float* ubuf, cudaStream_t st) {
   cudaError_t e;
-#define DUFWI_CF(R, M)                                                                      \
-  e = launch_cluster(cluster_fwd_kernel<R, M>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,    \
-                     unit_begin, U, rec, hist, strips, ubuf)
-  if (rho) {
-    if (mode == 0) DUFWI_CF(true, 0); else if (mode == 1) DUFWI_CF(true, 1); else DUFWI_CF(true, 2);
-  } else {
-    if (mode == 0) DUFWI_CF(false, 0); else if (mode == 1) DUFWI_CF(false, 1); else DUFWI_CF(false, 2);
-  }
-#undef DUFWI_CF
+  if (c.rpt == 4 && c.dbl) e = cluster_forward_t<4, double>(g, m, c, mode, unit_begin, U, rec, hist, strips, ubuf, st);
+  else if (c.rpt == 2 && c.dbl) e = cluster_forward_t<2, double>(g, m, c, mode, unit_begin, U, rec, hist, strips, ubuf, st);
+  else if (c.rpt == 4) e = cluster_forward_t<4, float>(g, m, c, mode, unit_begin, U, rec, hist, strips, ubuf, st);
+  else e = cluster_forward_t<2, float>(g, m, c, mode, unit_begin, U, rec, hist, strips, ubuf, st);
   return (int)e;
 }
 
-inline int cluster_adjoint(const Geo& g, const Model& m, const ClusterCfg& c, bool rho, int mode,
-                           int unit_begin, int U, const double* rres, const float* hist,
+inline int cluster_adjoint(const Geo& g, const Model& m, const ClusterCfg& c, bool /*rho*/,
+                           int mode, int unit_begin, int U, const double* rres, const float* hist,
                            const float* strips, const float* ubuf, double* acc_part, int acc_off,
                            cudaStream_t st) {
   cudaError_t e;
-#define DUFWI_CA(R, M)                                                                      \
-  e = launch_cluster(cluster_adj_kernel<R, M>, c, U, c.smem_adj, st, g, m, c.cs, c.rows,    \
-                     unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off)
-  if (rho) {
-    if (mode == 1) DUFWI_CA(true, 1); else DUFWI_CA(true, 2);
-  } else {
-    if (mode == 1) DUFWI_CA(false, 1); else DUFWI_CA(false, 2);
-  }
-#undef DUFWI_CA
+  if (c.rpt == 4 && c.dbl) e = cluster_adjoint_t<4, double>(g, m, c, mode, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off, st);
+  else if (c.rpt == 2 && c.dbl) e = cluster_adjoint_t<2, double>(g, m, c, mode, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off, st);
+  else if (c.rpt == 4) e = cluster_adjoint_t<4, float>(g, m, c, mode, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off, st);
+  else e = cluster_adjoint_t<2, float>(g, m, c, mode, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off, st);
   return (int)e;
 }
 

@@ -159,6 +159,14 @@ class PhysicsEngine:
         code = int(self._so.dufwi_plan_last_engine(self._plan))
         return {1: "stepwise", 2: "cluster"}.get(code, "none")
 
+    def info(self) -> dict:
+        """Engine configuration chosen by the plan (cluster shape, shared memory)."""
+        buf = (ctypes.c_int64 * 8)()
+        n = self._so.dufwi_plan_info(self._plan, buf, 8)
+        keys = ("cluster_ok", "cluster_ctas", "rows_per_cta", "rows_per_thread",
+                "threads_per_cta", "f64_exchange", "smem_forward", "smem_adjoint")
+        return {k: int(buf[i]) for i, k in enumerate(keys[:n])}
+
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
@@ -326,3 +334,37 @@ class PhysicsEngine:
         if return_traces:
             return misfit, grad, traces
         return misfit, grad
+
+    # ------------------------------------------------------------ timing
+    def time_sweeps(self, obs: torch.Tensor, reps: int = 3, mask: bool = True,
+                    store: str = "auto") -> dict:
+        """Average CUDA-event time of one forward and one adjoint C-ABI call over this
+        rank's units (one chunk), on the launching stream — the roofline denominators."""
+        self._require_model()
+        u0, u1 = self.local_units()
+        mode = self.pick_store(mask, store)
+        U = u1 - u0
+        ws = self._workspace(mode, U)
+        st = self._stream()
+        acc = torch.zeros_like(self._acc)
+        mis = torch.zeros_like(self._misfit)
+        tr = torch.empty((U, self.R, self.nt), dtype=torch.float32, device=self.device)
+        obs = obs.to(self.device, torch.float64).contiguous()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps + 1)]
+        for r in range(reps + 1):
+            ev[r][0].record()
+            check(self._so.dufwi_forward(self._plan, mode, u0, U, _ptr(tr), _ptr(self._flag),
+                                         _ptr(ws.buf), ws.buf.numel(), st))
+            ev[r][1].record()
+            check(self._so.dufwi_residual(self._plan, u0, U, _ptr(tr), _ptr(obs[u0:]), _ptr(mis),
+                                          _ptr(ws.buf), ws.buf.numel(), st))
+            ev[r][2].record()
+            check(self._so.dufwi_adjoint(self._plan, mode, u0, U, _ptr(ws.buf), ws.buf.numel(),
+                                         _ptr(acc), st))
+            ev[r][3].record()
+        torch.cuda.synchronize(self.device)
+        f = [ev[r][0].elapsed_time(ev[r][1]) for r in range(1, reps + 1)]
+        a = [ev[r][2].elapsed_time(ev[r][3]) for r in range(1, reps + 1)]
+        return {"units": U, "forward_ms": sum(f) / reps, "adjoint_ms": sum(a) / reps,
+                "store": {STORE_FULL: "full", STORE_STRIPS: "strips"}.get(mode, "none"),
+                "engine": self.last_engine}

@@ -115,7 +115,7 @@ def test_config0_gradient_own_obs(gpu, golden_dir):
     assert rel_l2(g[0].cpu().numpy(), z["grad"]) <= GRAD_TOL
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ("auto", "stepwise"))
 def test_variable_density_vs_oracle(gpu, engine):
     wl, grid, geom, pulse, damp = small_linear(rho=True, seed=11)
     rho = wl.rho[0]
@@ -142,7 +142,8 @@ def test_density_api_constant_rho_equals_plain(gpu):
     sos = pk.SosMap(grid, wl.c_true[0])
     a = pk.simulate_all(sos, geom, pulse, damp)
     b = pk.simulate_all(sos, geom, pulse, damp, density=np.full(grid.shape, 1000.0))
-    assert np.array_equal(a.traces, b.traces)
+    # different engines (density runs stepwise with f32 state): agree to storage rounding
+    assert rel_l2(b.traces, a.traces) <= 1e-6
 
 
 def test_batch_of_phantoms_equals_individual(gpu):
