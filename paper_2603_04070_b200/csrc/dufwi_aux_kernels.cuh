@@ -99,9 +99,11 @@ __global__ void misfit_sum_kernel(Geo g, int unit_begin, int U, const double* __
   for (int lu = 0; lu < U; ++lu) misfit[(unit_begin + lu) / g.S] += mu[lu];
 }
 
-// acc[b] += acc_part[g] for the non-empty groups of phantom b, in group order.
-__global__ void reduce_groups_kernel(Geo g, int unit_begin, int U, int gs, int b0, int nb,
-                                     int gpp, const double* __restrict__ acc_part,
+// acc[b] += sum of acc_part[g] over phantom b's groups, in group order.  Group
+// numbering follows shot_group(): `first` groups for the chunk's first phantom,
+// then `gpp` per further phantom (empty tail groups hold zeros).
+__global__ void reduce_groups_kernel(Geo g, int b0, int nb, int first, int gpp,
+                                     const double* __restrict__ acc_part,
                                      double* __restrict__ acc) {
   const size_t N2 = (size_t)g.nx * g.nz;
   const size_t total = (size_t)nb * N2;
@@ -109,16 +111,11 @@ __global__ void reduce_groups_kernel(Geo g, int unit_begin, int U, int gs, int b
        i += (size_t)gridDim.x * blockDim.x) {
     const int bl = (int)(i / N2);
     const size_t cell = i % N2;
-    const int b = b0 + bl;
+    const int g0 = bl == 0 ? 0 : first + (bl - 1) * gpp;
+    const int g1 = bl == 0 ? first : g0 + gpp;
     double sum = 0.0;
-    for (int k = 0; k < gpp; ++k) {
-      const int s_first = k * gs;
-      const int u_first = max(b * g.S + s_first, unit_begin);
-      const int u_last = min(b * g.S + min(s_first + gs, g.S), unit_begin + U);
-      if (u_first >= u_last) continue;
-      sum += acc_part[(size_t)(bl * gpp + k) * N2 + cell];
-    }
-    acc[(size_t)b * N2 + cell] += sum;
+    for (int k = g0; k < g1; ++k) sum += acc_part[(size_t)k * N2 + cell];
+    acc[(size_t)(b0 + bl) * N2 + cell] += sum;
   }
 }
 

@@ -58,6 +58,7 @@ struct dufwi_plan {
   double *Ed = nullptr, *dEdc = nullptr, *rho = nullptr, *q = nullptr;
   int* flag = nullptr;
   std::vector<void*> owned;
+  ABTables ab{};  // (A, B) tables of the damped update for the stepwise kernels
   // cluster engine
   ClusterCfg ccfg{};
   bool cluster_ok = false;
@@ -90,29 +91,45 @@ struct Layout {
          total = 0;
 };
 
-// Shot groups of the stepwise adjoint for a concrete unit range.
+// Shot groups of the stepwise kernels for a concrete unit range: groups of up
+// to `gs` shots of one phantom; the adjoint keeps one f64 accumulator per group.
 struct Groups {
-  int gs = 1, gpp = 1, nb = 1, b0 = 0, ngroups = 1;
+  int gs = 1, gpp = 1, nb = 1, b0 = 0, ngroups = 1, first = 1;
 };
 
-int tiles_of(const Geo& g) {
-  return ((g.nz + kTileZ - 1) / kTileZ) * ((g.nx + kTileX - 1) / kTileX);
-}
+int zstrips(const Geo& g) { return (g.nz + kStripZ - 1) / kStripZ; }
+long warps_per_group(const Geo& g) { return (long)zstrips(g) * ((g.nx + kRXA - 1) / kRXA); }
+constexpr long kTargetWarps = 148L * 64;  // resident warps wanted per launch
 
-// Shot-group size: enough CTAs to fill 148 SMs several times, otherwise as many
-// shots per thread as possible (fewer accumulator read-modify-writes).
-Groups groups_for(const Geo& g, int unit_begin, int U, bool per_unit) {
+// Group count as enumerated by shot_group(): the chunk's first phantom (maybe
+// partial), then ceil(S/gs) groups for every further phantom.
+Groups make_groups(const Geo& g, int unit_begin, int U, int gs) {
   Groups G;
-  const int tiles = tiles_of(g);
-  const int target_ctas = 148 * 8;
-  const int wanted = std::max(1, (target_ctas + tiles - 1) / tiles);
-  int gs = per_unit ? 1 : std::max(1, (U + wanted - 1) / wanted);
-  G.gs = std::min(gs, g.S);
+  G.gs = std::max(1, std::min(gs, g.S));
   G.gpp = (g.S + G.gs - 1) / G.gs;
   G.b0 = unit_begin / g.S;
   G.nb = (unit_begin + U - 1) / g.S - G.b0 + 1;
-  G.ngroups = G.nb * G.gpp;
+  const int n_first = std::min(U, (G.b0 + 1) * g.S - unit_begin);
+  G.first = (n_first + G.gs - 1) / G.gs;
+  G.ngroups = G.first + (G.nb - 1) * G.gpp;
   return G;
+}
+
+// Forward: one group per kNSF shots (a thread carries them).
+Groups fwd_groups(const Geo& g, int unit_begin, int U) { return make_groups(g, unit_begin, U, kNSF); }
+
+// Adjoint: as many shots per group as the warp target allows (one f64
+// accumulator read-modify-write per cell, group and step).
+Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit) {
+  if (per_unit) return make_groups(g, unit_begin, U, 1);
+  const long wanted = std::max(1L, (kTargetWarps + warps_per_group(g) - 1) / warps_per_group(g));
+  int gs = (int)std::max(1L, ((long)U + wanted - 1) / wanted);
+  gs = (gs + kNSA - 1) / kNSA * kNSA;
+  return make_groups(g, unit_begin, U, gs);
+}
+
+Groups groups_for(const Geo& g, int unit_begin, int U, bool per_unit) {
+  return adj_groups(g, unit_begin, U, per_unit);
 }
 
 // Upper bound of the group count over every placement of U units.
@@ -265,6 +282,33 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   } else {
     rc = rc ? rc : upload(p, &p->d2d, geo->damping_host, (size_t)nx * nz);
   }
+  {
+    // (A, B) of the damped update (forward.py:226-234) per axis ramp / per cell
+    auto ab_host = [&](double D, double& A, double& B) {
+      if (D == 0.0) { A = 2.0; B = -1.0; return; }
+      const double ddt = D * geo->dt, den = 1.0 + ddt;
+      A = (2.0 - ddt * ddt) / den;
+      B = (ddt - 1.0) / den;
+    };
+    if (geo->px_host) {
+      std::vector<double> Ax(nx), Bx(nx), Az(nz), Bz(nz);
+      for (int x = 0; x < nx; ++x) ab_host(geo->px_host[x], Ax[x], Bx[x]);
+      for (int z = 0; z < nz; ++z) ab_host(geo->pz_host[z], Az[z], Bz[z]);
+      double *dAx, *dBx, *dAz, *dBz;
+      rc = rc ? rc : upload(p, &dAx, Ax.data(), nx);
+      rc = rc ? rc : upload(p, &dBx, Bx.data(), nx);
+      rc = rc ? rc : upload(p, &dAz, Az.data(), nz);
+      rc = rc ? rc : upload(p, &dBz, Bz.data(), nz);
+      if (!rc) { p->ab.Ax = dAx; p->ab.Bx = dBx; p->ab.Az = dAz; p->ab.Bz = dBz; }
+    } else {
+      std::vector<double> A2((size_t)nx * nz), B2((size_t)nx * nz);
+      for (size_t i = 0; i < A2.size(); ++i) ab_host(geo->damping_host[i], A2[i], B2[i]);
+      double *dA2, *dB2;
+      rc = rc ? rc : upload(p, &dA2, A2.data(), A2.size());
+      rc = rc ? rc : upload(p, &dB2, B2.data(), B2.size());
+      if (!rc) { p->ab.A2 = dA2; p->ab.B2 = dB2; }
+    }
+  }
   rc = rc ? rc : upload(p, &p->pulse, geo->pulse_host, geo->nt);
   rc = rc ? rc : upload(p, &p->tx, geo->tx_host, 2 * (size_t)S);
   rc = rc ? rc : upload(p, &p->rx_slot, rx_slot.data(), rx_slot.size());
@@ -289,6 +333,8 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   }
   g.px = p->px;
   g.pz = p->pz;
+  p->ab.px = p->px;
+  p->ab.pz = p->pz;
   g.d2d = p->d2d;
   g.pulse = p->pulse;
   g.tx = p->tx;
@@ -387,35 +433,33 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     ++p->launches;
   } else {
     p->last_engine = DUFWI_ENGINE_STEPWISE;
-    dim3 block(kTileZ, kTileX);
-    dim3 grid((g.nz + kTileZ - 1) / kTileZ, (g.nx + kTileX - 1) / kTileX, U);
+    const Groups G = fwd_groups(g, unit_begin, U);
+    dim3 block(kWarpsX * 32);
+    dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXF - 1) / (kWarpsX * kRXF), G.ngroups);
     for (int t = 0; t < g.nt; ++t) {
       float* rec_t = rec + (size_t)t * U * g.M;
       const int has1 = t >= 1, has2 = t >= 2;
+      const float *u1, *u2;
+      float* uo;
+      float* st_t = mode == DUFWI_STORE_STRIPS ? strips + (size_t)t * U * g.SL : nullptr;
       if (mode == DUFWI_STORE_FULL) {
-        const float* u1 = has1 ? hist + (size_t)(t - 1) * fieldU : nullptr;
-        const float* u2 = has2 ? hist + (size_t)(t - 2) * fieldU : nullptr;
-        float* uo = hist + (size_t)t * fieldU;
-        if (p->has_rho)
-          fwd_step_kernel<true, 1><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, u2, uo, rec_t, nullptr, has1, has2);
-        else
-          fwd_step_kernel<false, 1><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, u2, uo, rec_t, nullptr, has1, has2);
+        u1 = has1 ? hist + (size_t)(t - 1) * fieldU : hist;
+        u2 = has2 ? hist + (size_t)(t - 2) * fieldU : hist;
+        uo = hist + (size_t)t * fieldU;
       } else {
-        const float* u1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
-        float* uo = ubuf + (size_t)(t & 1) * fieldU;
-        float* st_t = mode == DUFWI_STORE_STRIPS ? strips + (size_t)t * U * g.SL : nullptr;
-        if (mode == DUFWI_STORE_STRIPS) {
-          if (p->has_rho)
-            fwd_step_kernel<true, 2><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, uo, uo, rec_t, st_t, has1, has2);
-          else
-            fwd_step_kernel<false, 2><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, uo, uo, rec_t, st_t, has1, has2);
-        } else {
-          if (p->has_rho)
-            fwd_step_kernel<true, 0><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, uo, uo, rec_t, nullptr, has1, has2);
-          else
-            fwd_step_kernel<false, 0><<<grid, block, 0, st>>>(g, m, t, unit_begin, u1, uo, uo, rec_t, nullptr, has1, has2);
-        }
+        u1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
+        uo = ubuf + (size_t)(t & 1) * fieldU;
+        u2 = uo;
       }
+#define DUFWI_FWD(R, M)                                                                         \
+  fwd_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, u1, u2,   \
+                                                  uo, rec_t, st_t, has1, has2)
+      if (p->has_rho) {
+        if (mode == 0) DUFWI_FWD(true, 0); else if (mode == 1) DUFWI_FWD(true, 1); else DUFWI_FWD(true, 2);
+      } else {
+        if (mode == 0) DUFWI_FWD(false, 0); else if (mode == 1) DUFWI_FWD(false, 1); else DUFWI_FWD(false, 2);
+      }
+#undef DUFWI_FWD
       LAUNCH_CHECK(p);
     }
   }
@@ -482,8 +526,8 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   const Groups G = groups_for(g, unit_begin, U, clus);
   if (clus) {
     p->last_engine = DUFWI_ENGINE_CLUSTER;
-    // per-unit accumulators: group (b - b0) * S + s  ==  lu + (unit_begin - b0 * S)
-    const int acc_off = unit_begin - G.b0 * g.S;
+    // per-unit accumulators: with one shot per group, group index == chunk-local unit
+    const int acc_off = 0;
     rc = cluster_adjoint(g, m, p->ccfg, p->has_rho != 0, mode, unit_begin, U, rres,
                          mode == DUFWI_STORE_FULL ? hist : nullptr,
                          mode == DUFWI_STORE_STRIPS ? strips : nullptr, ubuf, acc_part, acc_off,
@@ -493,38 +537,36 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   } else {
   p->last_engine = DUFWI_ENGINE_STEPWISE;
   CUDA_TRY(cudaMemsetAsync(acc_part, 0, (size_t)G.ngroups * N2 * sizeof(double), st));
-  dim3 block(kTileZ, kTileX);
-  dim3 grid((g.nz + kTileZ - 1) / kTileZ, (g.nx + kTileX - 1) / kTileX, G.ngroups);
+  dim3 block(kWarpsX * 32);
+  dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXA - 1) / (kWarpsX * kRXA), G.ngroups);
   for (int t = g.nt - 1; t >= 0; --t) {
     const int has1 = t <= g.nt - 2, has2 = t <= g.nt - 3;
     const float* l1 = lbuf + (size_t)((t + 1) & 1) * fieldU;
     float* l2o = lbuf + (size_t)(t & 1) * fieldU;
     const double* rres_t = rres + (size_t)t * U * g.M;
     const int do_img = t >= 1;
-    if (mode == DUFWI_STORE_FULL) {
-      const float* F = do_img ? hist + (size_t)(t - 1) * fieldU : nullptr;
-      if (p->has_rho)
-        adj_step_kernel<true, 1><<<grid, block, 0, st>>>(g, m, t, unit_begin, U, G.gs, G.b0, G.gpp, l1, l2o, F, nullptr, nullptr, nullptr, rres_t, acc_part, has1, has2, do_img, 0);
-      else
-        adj_step_kernel<false, 1><<<grid, block, 0, st>>>(g, m, t, unit_begin, U, G.gs, G.b0, G.gpp, l1, l2o, F, nullptr, nullptr, nullptr, rres_t, acc_part, has1, has2, do_img, 0);
+    const float* F = (mode == DUFWI_STORE_FULL && do_img) ? hist + (size_t)(t - 1) * fieldU : nullptr;
+    float* ut = ubuf + (size_t)(t & 1) * fieldU;
+    const float* utm1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
+    const float* st_tm1 = (mode == DUFWI_STORE_STRIPS && do_img) ? strips + (size_t)(t - 1) * U * g.SL : nullptr;
+    const int do_recon = t >= 2;
+#define DUFWI_ADJ(R, M)                                                                          \
+  adj_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o,  \
+                                                  F, ut, utm1, st_tm1,                            \
+                                                  rres_t, acc_part, has1, has2, do_img, do_recon)
+    if (p->has_rho) {
+      if (mode == DUFWI_STORE_FULL) DUFWI_ADJ(true, 1); else DUFWI_ADJ(true, 2);
     } else {
-      float* ut = ubuf + (size_t)(t & 1) * fieldU;
-      const float* utm1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
-      const float* st_tm1 = do_img ? strips + (size_t)(t - 1) * U * g.SL : nullptr;
-      const int do_recon = t >= 2;
-      if (p->has_rho)
-        adj_step_kernel<true, 2><<<grid, block, 0, st>>>(g, m, t, unit_begin, U, G.gs, G.b0, G.gpp, l1, l2o, nullptr, ut, utm1, st_tm1, rres_t, acc_part, has1, has2, do_img, do_recon);
-      else
-        adj_step_kernel<false, 2><<<grid, block, 0, st>>>(g, m, t, unit_begin, U, G.gs, G.b0, G.gpp, l1, l2o, nullptr, ut, utm1, st_tm1, rres_t, acc_part, has1, has2, do_img, do_recon);
+      if (mode == DUFWI_STORE_FULL) DUFWI_ADJ(false, 1); else DUFWI_ADJ(false, 2);
     }
+#undef DUFWI_ADJ
     LAUNCH_CHECK(p);
   }
   }
   {
     const size_t total = (size_t)G.nb * N2;
     const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
-    reduce_groups_kernel<<<blocks, 256, 0, st>>>(g, unit_begin, U, G.gs, G.b0, G.nb, G.gpp,
-                                                 acc_part, acc_dev);
+    reduce_groups_kernel<<<blocks, 256, 0, st>>>(g, G.b0, G.nb, G.first, G.gpp, acc_part, acc_dev);
     LAUNCH_CHECK(p);
   }
   return DUFWI_OK;

@@ -337,11 +337,11 @@ class PhysicsEngine:
 
     # ------------------------------------------------------------ timing
     def time_sweeps(self, obs: torch.Tensor, reps: int = 3, mask: bool = True,
-                    store: str = "auto") -> dict:
+                    store: str = "auto", units: tuple[int, int] | None = None) -> dict:
         """Average CUDA-event time of one forward and one adjoint C-ABI call over this
         rank's units (one chunk), on the launching stream — the roofline denominators."""
         self._require_model()
-        u0, u1 = self.local_units()
+        u0, u1 = units if units is not None else self.local_units()
         mode = self.pick_store(mask, store)
         U = u1 - u0
         ws = self._workspace(mode, U)
