@@ -44,6 +44,20 @@ def shard_range(n_units: int, rank: int, world: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
+def combine_partials(packed: torch.Tensor) -> None:
+    """Sum the per-rank partials — imaging accumulators (B, nx, nz), misfits (B,) and
+    the non-finite flag, packed in one f64 buffer — in place: the one collective
+    of a gradient evaluation.
+
+    NCCL over NVLink on GPUs; the same call runs on gloo for the CPU tests.
+    """
+    if not (torch.distributed.is_available() and torch.distributed.is_initialized()):
+        return
+    if torch.distributed.get_world_size() == 1:
+        return
+    torch.distributed.all_reduce(packed)
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -138,8 +152,12 @@ class PhysicsEngine:
         self._c = None
         self._rho = None
         self.box = self._undamped_box()
-        self._acc = torch.zeros((self.B, self.nx, self.nz), dtype=torch.float64, device=self.device)
-        self._misfit = torch.zeros(self.B, dtype=torch.float64, device=self.device)
+        # one packed f64 buffer [acc (B*nx*nz) | misfit (B) | flags (1)] so the
+        # per-gradient combine across ranks is a single all_reduce
+        n_acc = self.B * self.nx * self.nz
+        self._red = torch.zeros(n_acc + self.B + 1, dtype=torch.float64, device=self.device)
+        self._acc = self._red[:n_acc].view(self.B, self.nx, self.nz)
+        self._misfit = self._red[n_acc:n_acc + self.B]
         del N2, keep
 
     # ------------------------------------------------------------------ misc
@@ -300,10 +318,9 @@ class PhysicsEngine:
         chunk = self.chunk_units(mode, max(n, 1))
         ws = self._workspace(mode, chunk) if n > 0 else None
         st = self._stream()
-        self._acc.zero_()
-        self._misfit.zero_()
+        self._red.zero_()
         self._flag.zero_()
-        traces = torch.empty((max(n, 0), self.R, self.nt), dtype=torch.float32, device=self.device)
+        traces =torch.empty((max(n, 0), self.R, self.nt), dtype=torch.float32, device=self.device)
         if obs.dtype != torch.float64 or obs.device != self.device:
             obs = obs.to(self.device, torch.float64)
         obs = obs.contiguous()
@@ -316,10 +333,10 @@ class PhysicsEngine:
                                           _ptr(self._misfit), _ptr(ws.buf), ws.buf.numel(), st))
             check(self._so.dufwi_adjoint(self._plan, mode, a, U, _ptr(ws.buf), ws.buf.numel(),
                                          _ptr(self._acc), st))
-        if dist and reduce and torch.distributed.get_world_size() > 1:
-            torch.distributed.all_reduce(self._acc)
-            torch.distributed.all_reduce(self._misfit)
-            torch.distributed.all_reduce(self._flag)
+        if dist and reduce:
+            self._red[-1] = self._flag[0].double()
+            combine_partials(self._red)
+            self._flag[0] = (self._red[-1] > 0).int()
         grad = torch.empty_like(self._acc)
         check(self._so.dufwi_finalize_gradient(self._plan, _ptr(self._acc), int(bool(mask)),
                                                int(guard_radius), _ptr(grad),
