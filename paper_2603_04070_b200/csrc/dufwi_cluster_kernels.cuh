@@ -79,6 +79,21 @@ __device__ __forceinline__ void push_async(uint32_t raddr, float v, uint32_t rba
                "r"(__float_as_uint(v)), "r"(rbar)
                : "memory");
 }
+// Predicated push: keeps the value in a register (no run-time register indexing).
+__device__ __forceinline__ void push_if(uint32_t on, uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.u32 q, %3, 0; "
+      "@q st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2]; }" ::"r"(raddr),
+      "l"(__double_as_longlong(v)), "r"(rbar), "r"(on)
+      : "memory");
+}
+__device__ __forceinline__ void push_if(uint32_t on, uint32_t raddr, float v, uint32_t rbar) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.u32 q, %3, 0; "
+      "@q st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2]; }" ::"r"(raddr),
+      "r"(__float_as_uint(v)), "r"(rbar), "r"(on)
+      : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -152,6 +167,8 @@ struct CellStatic {
   int ring[RPT];
   unsigned active, src, interior;
   bool pushes_up, pushes_dn;  // owns the slab's first / last row
+  unsigned dn_mask;           // bit j set: register j holds the slab's last row (pushes_dn)
+  bool special;               // any receiver / ring / source / push / history cell
   const double2* ab;          // shared (A, B) table, row stride nz
 };
 
@@ -163,6 +180,7 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
   st.ab = ab_table;
   st.pushes_up = c.has_up && c.lrow0 == 0;
   st.pushes_dn = false;
+  st.dn_mask = 0u;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const int lr = c.lrow0 + j;
@@ -180,9 +198,16 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
       st.ring[j] = ring_index(g, x, c.z);
       if (x == txx && c.z == txz) st.src |= 1u << j;
       if (in_box(g, x, c.z)) st.interior |= 1u << j;
-      if (lr == c.nr - 1 && c.has_dn) st.pushes_dn = true;
+      if (lr == c.nr - 1 && c.has_dn) {
+        st.pushes_dn = true;
+        st.dn_mask = 1u << j;
+      }
     }
   }
+  bool any = st.pushes_up || st.pushes_dn || st.src != 0u;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) any = any || st.slot[j] >= 0 || st.ring[j] >= 0;
+  st.special = any;
 }
 
 // x-neighbours of cell j of a thread column: register when the neighbour is the
@@ -231,21 +256,31 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
     v[j] = ab.x * u1[j] + ab.y * u2[j] + s.ed[j] * lap;
     if (s.src & (1u << j)) v[j] += pulse_t;
   }
+  // common path: state and exchange row (inactive rows only exist in the last segment)
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     if (!(s.active & (1u << j))) continue;
-    const int lr = c.lrow0 + j;
     u2[j] = v[j];
-    Xw[(size_t)(lr + 1) * W + z + 1] = (T)v[j];
-    if (lr == 0 && s.pushes_up)  // my first row -> bottom halo of rank-1
-      push_async(mapa_rank(smem_addr(Xw + (size_t)(c.rows + 1) * W + z + 1), c.rank - 1), (T)v[j],
-                 mapa_rank(bar_w, c.rank - 1));
-    if (lr == c.nr - 1 && s.pushes_dn)  // my last row -> top halo of rank+1
-      push_async(mapa_rank(smem_addr(Xw + z + 1), c.rank + 1), (T)v[j],
-                 mapa_rank(bar_w, c.rank + 1));
+    Xw[(size_t)(c.lrow0 + j + 1) * W + z + 1] = (T)v[j];
+  }
+  if (!s.special) return;
+  // rare path: halo pushes, receivers, history / ring strips
+  if (s.pushes_up)  // my first row -> bottom halo of rank-1
+    push_async(mapa_rank(smem_addr(Xw + (size_t)(c.rows + 1) * W + z + 1), c.rank - 1), (T)v[0],
+               mapa_rank(bar_w, c.rank - 1));
+  if (s.pushes_dn) {  // my last row -> top halo of rank+1
+    const uint32_t ra = mapa_rank(smem_addr(Xw + z + 1), c.rank + 1);
+    const uint32_t rb = mapa_rank(bar_w, c.rank + 1);
+    // explicit predicate per register so v[] is never indexed at run time
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) push_if((s.dn_mask >> j) & 1u, ra, (T)v[j], rb);
+  }
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    if (!(s.active & (1u << j))) continue;
     const float vf = (float)v[j];
     if (s.slot[j] >= 0) rec[((size_t)t * U + lu) * g.M + s.slot[j]] = vf;
-    const int x = c.r0 + lr;
+    const int x = c.r0 + c.lrow0 + j;
     if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)x * g.nz + z] = vf;
     if (MODE == 2 && s.ring[j] >= 0) strips[((size_t)t * U + lu) * g.SL + s.ring[j]] = vf;
   }
@@ -277,6 +312,7 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
   CellStatic<RPT> st;
   load_static<RPT>(g, m, c, pb, g.tx[2 * s], g.tx[2 * s + 1],
                    reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 2)), st);
+  if (MODE == 1) st.special = true;  // every cell goes to the history
   const uint32_t tx_bytes = (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T);
   double ua[RPT], ub[RPT];
 #pragma unroll
@@ -410,18 +446,24 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
         ua[j] = (double)ring_v[j];  // ring cell: the saved strip stands in for the reconstruction
       }
     }
-    const T uw = (T)ua[j];
-    if (MODE == 2) XUw[o] = uw;
-    if (lr == 0 && s.pushes_up) {
-      const uint32_t rb = mapa_rank(bar_w, c.rank - 1);
-      const size_t ho = (size_t)(c.rows + 1) * W + z + 1;
-      push_async(mapa_rank(smem_addr(XLw + ho), c.rank - 1), elw, rb);
-      if (MODE == 2) push_async(mapa_rank(smem_addr(XUw + ho), c.rank - 1), uw, rb);
-    }
-    if (lr == c.nr - 1 && s.pushes_dn) {
-      const uint32_t rb = mapa_rank(bar_w, c.rank + 1);
-      push_async(mapa_rank(smem_addr(XLw + z + 1), c.rank + 1), elw, rb);
-      if (MODE == 2) push_async(mapa_rank(smem_addr(XUw + z + 1), c.rank + 1), uw, rb);
+    if (MODE == 2) XUw[o] = (T)ua[j];
+  }
+  // halo pushes of the slab's first / last row (rare path)
+  if (s.pushes_up) {
+    const uint32_t rb = mapa_rank(bar_w, c.rank - 1);
+    const size_t ho = (size_t)(c.rows + 1) * W + z + 1;
+    push_async(mapa_rank(smem_addr(XLw + ho), c.rank - 1), (T)(s.ed[0] * l2[0]), rb);
+    if (MODE == 2) push_async(mapa_rank(smem_addr(XUw + ho), c.rank - 1), (T)ua[0], rb);
+  }
+  if (s.pushes_dn) {
+    const uint32_t rb = mapa_rank(bar_w, c.rank + 1);
+    const uint32_t ral = mapa_rank(smem_addr(XLw + z + 1), c.rank + 1);
+    const uint32_t rau = mapa_rank(smem_addr(XUw + z + 1), c.rank + 1);
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const uint32_t on = (s.dn_mask >> j) & 1u;
+      push_if(on, ral, (T)(s.ed[j] * l2[j]), rb);
+      if (MODE == 2) push_if(on, rau, (T)ua[j], rb);
     }
   }
 }
