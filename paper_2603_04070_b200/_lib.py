@@ -16,7 +16,7 @@ __all__ = ["LIB_PATH", "ExtensionUnavailable", "DufwiError", "Geometry", "lib", 
            "EXPORTED_SYMBOLS", "STORE_NONE", "STORE_FULL", "STORE_STRIPS",
            "ENGINE_AUTO", "ENGINE_STEPWISE", "ENGINE_CLUSTER"]
 
-LIB_PATH = Path(__file__).resolve().parent / "libdufwi.so"
+LIB_PATH = Path(os.environ.get("DUFWI_LIB", Path(__file__).resolve().parent / "libdufwi.so"))
 
 STORE_NONE, STORE_FULL, STORE_STRIPS = 0, 1, 2
 ENGINE_AUTO, ENGINE_STEPWISE, ENGINE_CLUSTER = 0, 1, 2

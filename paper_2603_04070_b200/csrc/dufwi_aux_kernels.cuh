@@ -51,10 +51,13 @@ __global__ void gather_traces_kernel(Geo g, int unit_begin, int U, const float* 
   }
 }
 
-// One block per unit: resid merged per receiver node into rres[t][lu][slot]
-// (duplicates summed in receiver order, like np.add.at in adjoint.py:127) and
-// the unit's misfit sum((tr - obs)^2) (adjoint.py:113-114) with a fixed-shape
-// block reduction, so results do not depend on scheduling.
+// kResidualSplit blocks per unit (blockIdx.x = part, blockIdx.y = unit): resid
+// merged per receiver node into rres[t][lu][slot] (duplicates summed in
+// receiver order, like np.add.at in adjoint.py:127) and per-part partial
+// misfits sum((tr - obs)^2) (adjoint.py:113-114) from fixed-shape block
+// reductions, summed in part order later — results do not depend on scheduling.
+constexpr int kResidualSplit = 16;
+
 template <int NT>
 __global__ void __launch_bounds__(NT) residual_kernel(Geo g, int unit_begin, int U,
                                                       const float* __restrict__ traces,
@@ -64,12 +67,14 @@ __global__ void __launch_bounds__(NT) residual_kernel(Geo g, int unit_begin, int
                                                       const unsigned char* __restrict__ rx_head,
                                                       double* __restrict__ rres,
                                                       double* __restrict__ misfit_unit) {
-  const int lu = blockIdx.x;
+  const int lu = blockIdx.y;
   const int s = (unit_begin + lu) % g.S;
   const size_t base = (size_t)lu * g.R * g.nt;
   const size_t n = (size_t)g.R * g.nt;
+  const size_t per = (n + kResidualSplit - 1) / kResidualSplit;
+  const size_t i0 = blockIdx.x * per, i1 = min(n, i0 + per);
   double sq = 0.0;
-  for (size_t i = threadIdx.x; i < n; i += NT) {
+  for (size_t i = i0 + threadIdx.x; i < i1; i += NT) {
     const int r = (int)(i / g.nt), t = (int)(i % g.nt);
     const double d = (double)traces[base + i] - obs[base + i];
     sq += d * d;
@@ -89,14 +94,18 @@ __global__ void __launch_bounds__(NT) residual_kernel(Geo g, int unit_begin, int
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) misfit_unit[lu] = red[0];
+  if (threadIdx.x == 0) misfit_unit[(size_t)lu * kResidualSplit + blockIdx.x] = red[0];
 }
 
 // misfit[b] += sum over the chunk's units of phantom b, in unit order.
 __global__ void misfit_sum_kernel(Geo g, int unit_begin, int U, const double* __restrict__ mu,
                                   double* __restrict__ misfit) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int lu = 0; lu < U; ++lu) misfit[(unit_begin + lu) / g.S] += mu[lu];
+  for (int lu = 0; lu < U; ++lu) {
+    double m = 0.0;
+    for (int k = 0; k < kResidualSplit; ++k) m += mu[(size_t)lu * kResidualSplit + k];
+    misfit[(unit_begin + lu) / g.S] += m;
+  }
 }
 
 // acc[b] += sum of acc_part[g] over phantom b's groups, in group order.  Group

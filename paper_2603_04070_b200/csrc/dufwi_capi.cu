@@ -146,7 +146,7 @@ Layout layout(const dufwi_plan_t* p, int mode, int U) {
     return o;
   };
   L.rres = take((size_t)g.nt * U * g.M * sizeof(double));
-  L.mis = take((size_t)U * sizeof(double));
+  L.mis = take((size_t)U * kResidualSplit * sizeof(double));
   L.rec = take((size_t)g.nt * U * g.M * sizeof(float));
   L.ubuf = take(2 * (size_t)U * N2 * sizeof(float));
   if (mode == DUFWI_STORE_FULL) L.hist = take((size_t)g.nt * U * N2 * sizeof(float));
@@ -490,7 +490,7 @@ extern "C" int dufwi_residual(dufwi_plan_t* p, int32_t unit_begin, int32_t U,
   double* mu = reinterpret_cast<double*>(base + L.mis);
   const size_t rres_bytes = (size_t)g.nt * U * g.M * sizeof(double);
   CUDA_TRY(cudaMemsetAsync(rres, 0, rres_bytes, st));
-  residual_kernel<256><<<U, 256, 0, st>>>(g, unit_begin, U, traces_dev, obs_dev, p->rx_slot,
+  residual_kernel<256><<<dim3(kResidualSplit, U), 256, 0, st>>>(g, unit_begin, U, traces_dev, obs_dev, p->rx_slot,
                                           p->rx_next, p->rx_head, rres, mu);
   LAUNCH_CHECK(p);
   misfit_sum_kernel<<<1, 32, 0, st>>>(g, unit_begin, U, mu, misfit_dev);
@@ -598,5 +598,14 @@ extern "C" int32_t dufwi_plan_info(const dufwi_plan_t* p, int64_t* out, int32_t 
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }
+#ifdef DUFWI_EXP_TIMING
+extern "C" int dufwi_debug_counters(unsigned long long* out, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * (n < 256 ? n : 256));
+  unsigned long long z[256] = {0};
+  cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
+  return 0;
+}
+#endif
 extern "C" const char* dufwi_last_error(void) { return g_last_error.c_str(); }
 extern "C" const char* dufwi_version(void) { return "dufwi-b200 0.1.0 (sm_100a)"; }

@@ -30,6 +30,9 @@
 namespace dufwi {
 
 namespace cg = cooperative_groups;
+#ifdef DUFWI_EXP_TIMING
+__device__ unsigned long long g_dbg[256];
+#endif
 
 struct ClusterCfg {
   int cs = 0;       // CTAs per cluster (slabs per unit)
@@ -38,8 +41,16 @@ struct ClusterCfg {
   int nseg = 0;     // thread segments per column
   int threads = 0;  // threads per CTA = nz * nseg
   int dbl = 0;      // exchange rows in f64 (1) or f32 (0)
+  int maxrec = 0;   // receiver cells per CTA (upper bound) staged in shared memory
+  int maxring = 0;  // ring-strip cells per CTA (upper bound) staged in shared memory
   size_t smem_fwd = 0, smem_adj = 0;
 };
+
+// Receiver samples / ring strips / residuals move between HBM and the step loop
+// through shared-memory stages of kStage steps: written (forward) or read
+// (adjoint) with one coalesced pass per kStage steps instead of scattered
+// global accesses inside every step.
+constexpr int kStage = 16;
 
 constexpr int kClusterMaxThreads = 512;  // 128 registers per thread available
 
@@ -94,6 +105,20 @@ __device__ __forceinline__ void push_if(uint32_t on, uint32_t raddr, float v, ui
       "r"(__float_as_uint(v)), "r"(rbar), "r"(on)
       : "memory");
 }
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+// One thread moves a whole exchange row into a neighbour CTA's halo row and
+// completes the bytes on that CTA's mbarrier (async proxy).
+__device__ __forceinline__ void push_row(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                         uint32_t bar_cluster) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(smem_addr(src)), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -101,9 +126,16 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 // ------------------------------------------------------------ smem layout
 // [nbufs exchange buffers of (rows+2) x (nz+2) T] [rows x nz double2 (A, B)] [2 mbarriers]
+// Exchange row stride: nz + 2 pad columns, rounded so every row starts on a
+// 16-byte boundary (bulk DSMEM copies move whole rows).
+template <class T>
+__host__ __device__ inline int xstride(int nz) {
+  const int q = 16 / (int)sizeof(T);
+  return (nz + 2 + q - 1) / q * q;
+}
 template <class T>
 __host__ __device__ inline size_t xbuf_elems(int rows, int nz) {
-  return (size_t)(rows + 2) * (nz + 2);
+  return (size_t)(rows + 2) * xstride<T>(nz);
 }
 template <class T>
 __host__ __device__ inline size_t ab_offset(int rows, int nz, int nbufs) {
@@ -113,20 +145,61 @@ template <class T>
 __host__ __device__ inline size_t bar_offset(int rows, int nz, int nbufs) {
   return ab_offset<T>(rows, nz, nbufs) + (size_t)rows * nz * sizeof(double2);
 }
+// IO stage after the mbarriers: [n_rec, n_ring, pad] [rec_g[maxrec]] [ring_g[maxring]]
+// [double stage_rec[kStage][maxrec]] [float stage_ring[kStage][maxring]]
+struct IoStage {
+  int* counts;
+  int* rec_g;
+  int* ring_g;
+  double* srec;
+  float* sring;
+  int maxrec, maxring;
+};
+
+__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
+
 template <class T>
-__host__ __device__ inline size_t cluster_smem_bytes(int rows, int nz, int nbufs) {
-  return bar_offset<T>(rows, nz, nbufs) + 2 * sizeof(uint64_t);
+__host__ __device__ inline size_t io_offset(int rows, int nz, int nbufs) {
+  return al16(bar_offset<T>(rows, nz, nbufs) + 2 * sizeof(uint64_t));
+}
+
+__host__ __device__ inline size_t io_bytes(int maxrec, int maxring) {
+  return 16 + al16((size_t)maxrec * 4) + al16((size_t)maxring * 4) +
+         al16((size_t)kStage * maxrec * 8) + al16((size_t)kStage * maxring * 4);
+}
+
+template <class T>
+__host__ __device__ inline size_t cluster_smem_bytes(int rows, int nz, int nbufs, int maxrec,
+                                                     int maxring) {
+  return io_offset<T>(rows, nz, nbufs) + io_bytes(maxrec, maxring);
+}
+
+__device__ __forceinline__ IoStage io_stage(unsigned char* base, int maxrec, int maxring) {
+  IoStage io;
+  io.counts = reinterpret_cast<int*>(base);
+  size_t o = 16;
+  io.rec_g = reinterpret_cast<int*>(base + o);
+  o += al16((size_t)maxrec * 4);
+  io.ring_g = reinterpret_cast<int*>(base + o);
+  o += al16((size_t)maxring * 4);
+  io.srec = reinterpret_cast<double*>(base + o);
+  o += al16((size_t)kStage * maxrec * 8);
+  io.sring = reinterpret_cast<float*>(base + o);
+  io.maxrec = maxrec;
+  io.maxring = maxring;
+  return io;
 }
 
 // Per-thread static description of its cells.
 struct CellCtx {
   int rank, cs, rows, nr, r0;  // slab of this CTA: global rows [r0, r0+nr)
   int seg, z, lrow0;           // thread: column z, local rows lrow0 .. lrow0+RPT-1
-  int W;                       // exchange row stride (nz + 2)
+  int W;                       // exchange row stride (>= nz + 2, 16-byte rows)
+  int seg_last;                // segment owning the slab's last row
   bool has_up, has_dn;         // CTA rank-1 / rank+1 exist with rows
 };
 
-__device__ __forceinline__ CellCtx make_ctx(int cs, int rows, int nx, int nz, int rpt) {
+__device__ __forceinline__ CellCtx make_ctx(int cs, int rows, int nx, int nz, int rpt, int W) {
   CellCtx c;
   c.rank = (int)cg::this_cluster().block_rank();
   c.cs = cs;
@@ -136,7 +209,8 @@ __device__ __forceinline__ CellCtx make_ctx(int cs, int rows, int nx, int nz, in
   c.seg = threadIdx.x / nz;
   c.z = threadIdx.x - c.seg * nz;
   c.lrow0 = c.seg * rpt;
-  c.W = nz + 2;
+  c.W = W;
+  c.seg_last = c.nr > 0 ? (c.nr - 1) / rpt : 0;
   c.has_up = c.rank > 0 && c.nr > 0;
   c.has_dn = c.nr > 0 && c.rank + 1 < cs && (c.rank + 1) * rows < nx;
   return c;
@@ -163,19 +237,20 @@ __device__ __forceinline__ bool in_box(const Geo& g, int x, int z) {
 template <int RPT>
 struct CellStatic {
   double ed[RPT];
-  int slot[RPT];
-  int ring[RPT];
+  int rl[RPT];  // receiver cell: local index into the IO stage, else -1
+  int gl[RPT];  // ring cell: local index into the IO stage, else -1
   unsigned active, src, interior;
   bool pushes_up, pushes_dn;  // owns the slab's first / last row
   unsigned dn_mask;           // bit j set: register j holds the slab's last row (pushes_dn)
   bool special;               // any receiver / ring / source / push / history cell
+  bool undamped;              // every cell has D == 0: (A, B) = (2, -1), no table reads
   const double2* ab;          // shared (A, B) table, row stride nz
 };
 
 template <int RPT>
 __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const CellCtx& c,
                                             size_t pb, int txx, int txz, double2* ab_table,
-                                            CellStatic<RPT>& st) {
+                                            const IoStage& io, CellStatic<RPT>& st) {
   st.active = st.src = st.interior = 0u;
   st.ab = ab_table;
   st.pushes_up = c.has_up && c.lrow0 == 0;
@@ -185,8 +260,8 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
   for (int j = 0; j < RPT; ++j) {
     const int lr = c.lrow0 + j;
     st.ed[j] = 0.0;
-    st.slot[j] = -1;
-    st.ring[j] = -1;
+    st.rl[j] = -1;
+    st.gl[j] = -1;
     if (lr < c.nr) {
       const int x = c.r0 + lr;
       st.active |= 1u << j;
@@ -194,8 +269,16 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
       double A, B;
       ab_coeffs(damping_at(g, x, c.z), g.dt, A, B);
       ab_table[(size_t)lr * g.nz + c.z] = make_double2(A, B);
-      if (g.row_flag[x]) st.slot[j] = g.node_slot[(size_t)x * g.nz + c.z];
-      st.ring[j] = ring_index(g, x, c.z);
+      const int slot = g.row_flag[x] ? g.node_slot[(size_t)x * g.nz + c.z] : -1;
+      if (slot >= 0) {
+        st.rl[j] = atomicAdd(&io.counts[0], 1);  // storage slot only: order does not matter
+        io.rec_g[st.rl[j]] = slot;
+      }
+      const int ring = ring_index(g, x, c.z);
+      if (ring >= 0 && io.maxring > 0) {
+        st.gl[j] = atomicAdd(&io.counts[1], 1);
+        io.ring_g[st.gl[j]] = ring;
+      }
       if (x == txx && c.z == txz) st.src |= 1u << j;
       if (in_box(g, x, c.z)) st.interior |= 1u << j;
       if (lr == c.nr - 1 && c.has_dn) {
@@ -204,9 +287,13 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
       }
     }
   }
-  bool any = st.pushes_up || st.pushes_dn || st.src != 0u;
+  st.undamped = true;
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) any = any || st.slot[j] >= 0 || st.ring[j] >= 0;
+  for (int j = 0; j < RPT; ++j)
+    if (c.lrow0 + j < c.nr && damping_at(g, c.r0 + c.lrow0 + j, c.z) != 0.0) st.undamped = false;
+  bool any = st.src != 0u;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) any = any || st.rl[j] >= 0 || st.gl[j] >= 0;
   st.special = any;
 }
 
@@ -226,6 +313,26 @@ __device__ __forceinline__ void x_neighbours(const CellCtx& c, const double (&v)
   }
 }
 
+// Bulk halo exchange: the threads owning the slab's first (last) row sync on a
+// named barrier, then one of them copies the whole row into the halo row of
+// CTA rank-1 (rank+1).  Needs nz % 32 == 0 so a row's threads are whole warps.
+template <class T>
+__device__ __forceinline__ void push_rows(const CellCtx& c, int nz, T* Xw, uint32_t bar_w) {
+  const uint32_t bytes = (uint32_t)(c.W * sizeof(T));
+  if (c.has_up && c.seg == 0) {
+    named_sync(1, nz);
+    if (threadIdx.x == 0)
+      push_row(mapa_rank(smem_addr(Xw + (size_t)(c.rows + 1) * c.W), c.rank - 1), Xw + (size_t)c.W,
+               bytes, mapa_rank(bar_w, c.rank - 1));
+  }
+  if (c.has_dn && c.seg == c.seg_last) {
+    named_sync(2, nz);
+    if (threadIdx.x == c.seg_last * nz)
+      push_row(mapa_rank(smem_addr(Xw), c.rank + 1), Xw + (size_t)c.nr * c.W, bytes,
+               mapa_rank(bar_w, c.rank + 1));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // forward step i (time t = i).  u1 = u[t-1] (read), u2 = u[t-2] -> u[t].
 // Reads exchange buffer Xr (step i-1), writes Xw (step i) and pushes the slab's
@@ -235,13 +342,31 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
                                          double (&u1)[RPT], double (&u2)[RPT], int t, int U,
                                          int lu, const T* Xr, T* Xw, uint32_t bar_r,
                                          uint32_t bar_w, uint32_t tx_bytes, double pulse_t,
-                                         float* __restrict__ rec, float* __restrict__ hist,
-                                         float* __restrict__ strips, size_t N2) {
+                                         const IoStage& io, float* __restrict__ hist, size_t N2,
+                                         bool bulk) {
   const int W = c.W, z = c.z;
+#ifdef DUFWI_EXP_TIMING
+  const bool tm = blockIdx.x == 5 && (threadIdx.x & 31) == 0;
+  long long T0 = clock64();
+#endif
+#ifndef DUFWI_EXP_NOSYNC
   __syncthreads();  // exchange rows of step i-1 complete; Xw free for reuse
+#endif
+#ifdef DUFWI_EXP_TIMING
+  long long T1 = clock64();
+#endif
+#ifndef DUFWI_EXP_NOWAIT
   if (t >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((t - 1) >> 1) & 1);
+#endif
+#ifdef DUFWI_EXP_TIMING
+  long long T2 = clock64();
+#endif
   if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
   double xm[RPT], xp[RPT], zm[RPT], zp[RPT], v[RPT];
+#ifdef DUFWI_EXP_NOLDS
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) { xm[j] = xp[j] = zm[j] = zp[j] = u1[j] * 0.25; }
+#else
   x_neighbours<RPT, T>(c, u1, Xr, xm, xp);
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
@@ -249,11 +374,16 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
     zm[j] = (double)Xr[(size_t)(lr + 1) * W + z];
     zp[j] = (double)Xr[(size_t)(lr + 1) * W + z + 2];
   }
+#endif
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const double lap = (((-4.0 * u1[j] + xm[j]) + xp[j]) + zm[j]) + zp[j];
-    const double2 ab = s.ab[(size_t)min(c.lrow0 + j, c.rows - 1) * g.nz + z];
+    const double2 ab = s.undamped ? make_double2(2.0, -1.0) : s.ab[(size_t)min(c.lrow0 + j, c.rows - 1) * g.nz + z];
+#ifdef DUFWI_EXP_NOCOMPUTE
+    v[j] = u1[j] + zm[j];
+#else
     v[j] = ab.x * u1[j] + ab.y * u2[j] + s.ed[j] * lap;
+#endif
     if (s.src & (1u << j)) v[j] += pulse_t;
   }
   // common path: state and exchange row (inactive rows only exist in the last segment)
@@ -263,36 +393,72 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
     u2[j] = v[j];
     Xw[(size_t)(c.lrow0 + j + 1) * W + z + 1] = (T)v[j];
   }
-  if (!s.special) return;
-  // rare path: halo pushes, receivers, history / ring strips
-  if (s.pushes_up)  // my first row -> bottom halo of rank-1
-    push_async(mapa_rank(smem_addr(Xw + (size_t)(c.rows + 1) * W + z + 1), c.rank - 1), (T)v[0],
-               mapa_rank(bar_w, c.rank - 1));
-  if (s.pushes_dn) {  // my last row -> top halo of rank+1
-    const uint32_t ra = mapa_rank(smem_addr(Xw + z + 1), c.rank + 1);
-    const uint32_t rb = mapa_rank(bar_w, c.rank + 1);
-    // explicit predicate per register so v[] is never indexed at run time
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) push_if((s.dn_mask >> j) & 1u, ra, (T)v[j], rb);
+#ifdef DUFWI_EXP_TIMING
+  long long T3 = clock64();
+  if (tm) {
+    const int w = threadIdx.x >> 5;
+    atomicAdd(&g_dbg[w * 4 + 0], (unsigned long long)(T1 - T0));
+    atomicAdd(&g_dbg[w * 4 + 1], (unsigned long long)(T2 - T1));
+    atomicAdd(&g_dbg[w * 4 + 2], (unsigned long long)(T3 - T2));
   }
+#endif
+  // halo rows to the neighbouring CTAs
+  if (bulk) {
+    push_rows<T>(c, g.nz, Xw, bar_w);
+  } else {
+    if (s.pushes_up)  // my first row -> bottom halo of rank-1
+      push_async(mapa_rank(smem_addr(Xw + (size_t)(c.rows + 1) * W + z + 1), c.rank - 1), (T)v[0],
+                 mapa_rank(bar_w, c.rank - 1));
+    if (s.pushes_dn) {  // my last row -> top halo of rank+1
+      const uint32_t ra = mapa_rank(smem_addr(Xw + z + 1), c.rank + 1);
+      const uint32_t rb = mapa_rank(bar_w, c.rank + 1);
+      // explicit predicate per register so v[] is never indexed at run time
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) push_if((s.dn_mask >> j) & 1u, ra, (T)v[j], rb);
+    }
+  }
+  if (!s.special) return;
+  // rare path: receivers, history / ring strips
+  const int k = t % kStage;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     if (!(s.active & (1u << j))) continue;
     const float vf = (float)v[j];
-    if (s.slot[j] >= 0) rec[((size_t)t * U + lu) * g.M + s.slot[j]] = vf;
-    const int x = c.r0 + c.lrow0 + j;
-    if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)x * g.nz + z] = vf;
-    if (MODE == 2 && s.ring[j] >= 0) strips[((size_t)t * U + lu) * g.SL + s.ring[j]] = vf;
+    if (s.rl[j] >= 0) io.srec[k * io.maxrec + s.rl[j]] = (double)vf;
+    if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + z] = vf;
+    if (MODE == 2 && s.gl[j] >= 0) io.sring[k * io.maxring + s.gl[j]] = vf;
+  }
+#ifdef DUFWI_EXP_TIMING
+  if (tm) atomicAdd(&g_dbg[(threadIdx.x >> 5) * 4 + 3], (unsigned long long)(clock64() - T3));
+#endif
+}
+
+// Write the staged receiver samples / ring strips of steps [t0, t0+nk) to HBM.
+template <int MODE>
+__device__ __forceinline__ void flush_stage(const Geo& g, const IoStage& io, int t0, int nk, int U,
+                                            int lu, float* __restrict__ rec,
+                                            float* __restrict__ strips) {
+  __syncthreads();
+  const int nrec = io.counts[0], nring = io.counts[1];
+  for (int idx = threadIdx.x; idx < nk * nrec; idx += blockDim.x) {
+    const int k = idx / nrec, i = idx - k * nrec;
+    rec[((size_t)(t0 + k) * U + lu) * g.M + io.rec_g[i]] = (float)io.srec[k * io.maxrec + i];
+  }
+  if (MODE == 2) {
+    for (int idx = threadIdx.x; idx < nk * nring; idx += blockDim.x) {
+      const int k = idx / nring, i = idx - k * nring;
+      strips[((size_t)(t0 + k) * U + lu) * g.SL + io.ring_g[i]] = io.sring[k * io.maxring + i];
+    }
   }
 }
 
 template <int RPT, class T, int MODE>
 __global__ void __launch_bounds__(kClusterMaxThreads, 1)
-    cluster_fwd_kernel(Geo g, Model m, int cs, int rows, int unit_begin, int U,
-                       float* __restrict__ rec, float* __restrict__ hist,
+    cluster_fwd_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
+                       int unit_begin, int U, float* __restrict__ rec, float* __restrict__ hist,
                        float* __restrict__ strips, float* __restrict__ ubuf) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT);
+  const CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT, xstride<T>(g.nz));
   const int lu = blockIdx.x / cs;
   const int u = unit_begin + lu;
   const int b = u / g.S;
@@ -304,16 +470,21 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, g.nz, 2));
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
   for (size_t i = threadIdx.x; i < 2 * xe; i += blockDim.x) X[0][i] = T(0);
+  const IoStage io = io_stage(smem + io_offset<T>(rows, g.nz, 2), maxrec, maxring);
   if (threadIdx.x == 0) {
     mbar_init(bar[0], 1);
     mbar_init(bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    io.counts[0] = io.counts[1] = 0;
   }
+  __syncthreads();
   CellStatic<RPT> st;
   load_static<RPT>(g, m, c, pb, g.tx[2 * s], g.tx[2 * s + 1],
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 2)), st);
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 2)), io, st);
   if (MODE == 1) st.special = true;  // every cell goes to the history
-  const uint32_t tx_bytes = (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T);
+  const bool bulk = false;  // measured slower than per-thread st.async (named-barrier + bulk-copy latency)
+  const uint32_t tx_bytes =
+      (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * (bulk ? c.W : g.nz) * sizeof(T);
   double ua[RPT], ub[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) ua[j] = ub[j] = 0.0;
@@ -327,15 +498,20 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
     double p = p_next;
     if (owns_src) p_next = g.pulse[t + 1];
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, X[1], X[0], bar[1], bar[0], tx_bytes, p,
-                           rec, hist, strips, N2);
+                           io, hist, N2, bulk);
     p = p_next;
     if (owns_src && t + 2 < g.nt) p_next = g.pulse[t + 2];
     fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, X[0], X[1], bar[0], bar[1], tx_bytes, p,
-                           rec, hist, strips, N2);
+                           io, hist, N2, bulk);
+    if ((t + 2) % kStage == 0) flush_stage<MODE>(g, io, t + 2 - kStage, kStage, U, lu, rec, strips);
   }
   if (t < g.nt)
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, X[1], X[0], bar[1], bar[0], tx_bytes,
-                           p_next, rec, hist, strips, N2);
+                           p_next, io, hist, N2, bulk);
+  if (g.nt % kStage) {
+    const int t0 = g.nt - g.nt % kStage;
+    flush_stage<MODE>(g, io, t0, g.nt - t0, U, lu, rec, strips);
+  }
   // drain the last step's incoming pushes before any CTA of the cluster exits
   if (c.has_up || c.has_dn) mbar_wait(bar[(g.nt - 1) & 1], ((g.nt - 1) >> 1) & 1);
   cluster_sync_all();
@@ -365,22 +541,20 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
                                          double (&ub)[RPT], double (&acc)[RPT], int i, int U,
                                          int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
                                          uint32_t bar_r, uint32_t bar_w, uint32_t tx_bytes,
-                                         double pulse_t, const double* __restrict__ rres,
-                                         const float* __restrict__ hist,
-                                         const float* __restrict__ strips, size_t N2) {
+                                         double pulse_t, const IoStage& io,
+                                         const float* __restrict__ hist, size_t N2, bool bulk) {
   const int W = c.W, z = c.z;
   const int t = g.nt - 1 - i;
-  // this step's global reads first, so their latency overlaps the syncs
+  __syncthreads();
+  // residuals / ring values of this step from the shared-memory stage
   double rr[RPT];
   float ring_v[RPT];
+  const int k = i % kStage;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    rr[j] = s.slot[j] >= 0 ? rres[((size_t)t * U + lu) * g.M + s.slot[j]] : 0.0;
-    ring_v[j] = (MODE == 2 && s.ring[j] >= 0 && t >= 2)
-                    ? strips[((size_t)(t - 2) * U + lu) * g.SL + s.ring[j]]
-                    : 0.f;
+    rr[j] = s.rl[j] >= 0 ? io.srec[k * io.maxrec + s.rl[j]] : 0.0;
+    ring_v[j] = (MODE == 2 && s.gl[j] >= 0) ? io.sring[k * io.maxring + s.gl[j]] : 0.f;
   }
-  __syncthreads();
   if (i >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((i - 1) >> 1) & 1);
   if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
 
@@ -394,7 +568,7 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
     const int lr = min(c.lrow0 + j, c.rows - 1);
     const size_t o = (size_t)(lr + 1) * W + z + 1;
     const double adj = (((-4.0 * el[j] + xm[j]) + xp[j]) + (double)XLr[o - 1]) + (double)XLr[o + 1];
-    const double2 ab = s.ab[(size_t)lr * g.nz + z];
+    const double2 ab = s.undamped ? make_double2(2.0, -1.0) : s.ab[(size_t)lr * g.nz + z];
     lam[j] = ab.x * l1[j] + adj + ab.y * l2[j] + rr[j];
   }
   // imaging with L(u[t-1]) and reconstruction of u[t-2]
@@ -442,13 +616,18 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
           if (s.src & (1u << j)) prev += pulse_t;
           ua[j] = prev;
         }
-      } else if (s.ring[j] >= 0 && t >= 2) {
+      } else if (s.gl[j] >= 0 && t >= 2) {
         ua[j] = (double)ring_v[j];  // ring cell: the saved strip stands in for the reconstruction
       }
     }
     if (MODE == 2) XUw[o] = (T)ua[j];
   }
-  // halo pushes of the slab's first / last row (rare path)
+  // halo rows to the neighbouring CTAs
+  if (bulk) {
+    push_rows<T>(c, g.nz, XLw, bar_w);
+    if (MODE == 2) push_rows<T>(c, g.nz, XUw, bar_w);
+    return;
+  }
   if (s.pushes_up) {
     const uint32_t rb = mapa_rank(bar_w, c.rank - 1);
     const size_t ho = (size_t)(c.rows + 1) * W + z + 1;
@@ -468,14 +647,38 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
   }
 }
 
+// Load residuals of steps [i0, i0+kStage) (t = nt-1-i) and the ring strips they
+// reconstruct from (t-2) into the shared-memory stage, one coalesced pass.
+template <int MODE>
+__device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, int i0, int U,
+                                               int lu, const double* __restrict__ rres,
+                                               const float* __restrict__ strips) {
+  __syncthreads();  // the previous block's readers are done with the stage
+  const int nk = min(kStage, g.nt - i0);
+  const int nrec = io.counts[0], nring = io.counts[1];
+  for (int idx = threadIdx.x; idx < nk * nrec; idx += blockDim.x) {
+    const int k = idx / nrec, r = idx - k * nrec;
+    const int t = g.nt - 1 - (i0 + k);
+    io.srec[k * io.maxrec + r] = rres[((size_t)t * U + lu) * g.M + io.rec_g[r]];
+  }
+  if (MODE == 2) {
+    for (int idx = threadIdx.x; idx < nk * nring; idx += blockDim.x) {
+      const int k = idx / nring, r = idx - k * nring;
+      const int t = g.nt - 1 - (i0 + k);
+      io.sring[k * io.maxring + r] = t >= 2 ? strips[((size_t)(t - 2) * U + lu) * g.SL + io.ring_g[r]] : 0.f;
+    }
+  }
+}
+
 template <int RPT, class T, int MODE>
 __global__ void __launch_bounds__(kClusterMaxThreads, 1)
-    cluster_adj_kernel(Geo g, Model m, int cs, int rows, int unit_begin, int U,
+    cluster_adj_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
+                       int unit_begin, int U,
                        const double* __restrict__ rres, const float* __restrict__ hist,
                        const float* __restrict__ strips, const float* __restrict__ ubuf,
                        double* __restrict__ acc_part, int acc_off) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT);
+  const CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT, xstride<T>(g.nz));
   const int lu = blockIdx.x / cs;
   const int u = unit_begin + lu;
   const int b = u / g.S;
@@ -490,17 +693,21 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, g.nz, 4));
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
   for (size_t k = threadIdx.x; k < 4 * xe; k += blockDim.x) base[k] = T(0);
+  const IoStage io = io_stage(smem + io_offset<T>(rows, g.nz, 4), maxrec, maxring);
   if (threadIdx.x == 0) {
     mbar_init(bar[0], 1);
     mbar_init(bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    io.counts[0] = io.counts[1] = 0;
   }
+  __syncthreads();
   CellStatic<RPT> st;
   load_static<RPT>(g, m, c, pb, g.tx[2 * s], g.tx[2 * s + 1],
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 4)), st);
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 4)), io, st);
   const int per = MODE == 2 ? 2 : 1;
+  const bool bulk = false;  // measured slower than per-thread st.async (named-barrier + bulk-copy latency)
   const uint32_t tx_bytes =
-      (uint32_t)(per * ((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T));
+      (uint32_t)(per * ((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * (bulk ? c.W : g.nz) * sizeof(T));
   const int nt = g.nt;
   const float* u_last = ubuf + ((size_t)((nt - 1) & 1) * U + lu) * N2;
   const float* u_prev = ubuf + ((size_t)((nt - 2) & 1) * U + lu) * N2;
@@ -529,17 +736,19 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
   // step i writes XL[i&1], XU[i&1], bar[i&1]; reads XL[(i+1)&1], XU[(i+1)&1], bar[(i+1)&1]
   int i = 0;
   for (; i + 1 < nt; i += 2) {
+    if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
     const double p0 = owns_src ? g.pulse[nt - 1 - i] : 0.0;
     adj_step<RPT, T, MODE>(g, c, st, la, lb, ua, ub, acc, i, U, lu, XL[1], XL[0], XU[1], XU[0],
-                           bar[1], bar[0], tx_bytes, p0, rres, hist, strips, N2);
+                           bar[1], bar[0], tx_bytes, p0, io, hist, N2, bulk);
     const double p1 = owns_src ? g.pulse[nt - 2 - i] : 0.0;
     adj_step<RPT, T, MODE>(g, c, st, lb, la, ub, ua, acc, i + 1, U, lu, XL[0], XL[1], XU[0], XU[1],
-                           bar[0], bar[1], tx_bytes, p1, rres, hist, strips, N2);
+                           bar[0], bar[1], tx_bytes, p1, io, hist, N2, bulk);
   }
-  if (i < nt)
+  if (i < nt) {
+    if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
     adj_step<RPT, T, MODE>(g, c, st, la, lb, ua, ub, acc, i, U, lu, XL[1], XL[0], XU[1], XU[0],
-                           bar[1], bar[0], tx_bytes, owns_src ? g.pulse[0] : 0.0, rres, hist,
-                           strips, N2);
+                           bar[1], bar[0], tx_bytes, owns_src ? g.pulse[0] : 0.0, io, hist, N2, bulk);
+  }
   if (c.has_up || c.has_dn) mbar_wait(bar[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
   cluster_sync_all();
   double* dst = acc_part + (size_t)(lu + acc_off) * N2;
@@ -586,8 +795,10 @@ inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
   const int nseg = (rows + RPT - 1) / RPT;
   const int threads = g.nz * nseg;
   if (threads > kClusterMaxThreads) return false;
-  const size_t sf = cluster_smem_bytes<T>(rows, g.nz, 2);
-  const size_t sa = cluster_smem_bytes<T>(rows, g.nz, 4);
+  const int maxrec = std::min(g.M, rows * g.nz);
+  const int maxring = g.SL > 0 ? std::min(g.SL, 2 * rows + 2 * g.nz) : 0;
+  const size_t sf = cluster_smem_bytes<T>(rows, g.nz, 2, maxrec, maxring);
+  const size_t sa = cluster_smem_bytes<T>(rows, g.nz, 4, maxrec, maxring);
   if (max_active_clusters(cluster_fwd_kernel<RPT, T, 0>, cs, threads, sf) <= 0) return false;
   if (max_active_clusters(cluster_fwd_kernel<RPT, T, 1>, cs, threads, sf) <= 0) return false;
   if (max_active_clusters(cluster_fwd_kernel<RPT, T, 2>, cs, threads, sf) <= 0) return false;
@@ -601,6 +812,8 @@ inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
   out->dbl = sizeof(T) == 8;
   out->smem_fwd = sf;
   out->smem_adj = sa;
+  out->maxrec = maxrec;
+  out->maxring = maxring;
   return true;
 }
 
@@ -614,8 +827,10 @@ inline bool cluster_config(const Geo& g, bool rho, ClusterCfg* out) {
     return false;
   }
   for (int cs : {16, 8}) {
+#ifndef DUFWI_EXCHANGE_F32
     if (try_cluster_cfg<4, double>(g, cs, out)) return true;
     if (try_cluster_cfg<2, double>(g, cs, out)) return true;
+#endif
     if (try_cluster_cfg<4, float>(g, cs, out)) return true;
     if (try_cluster_cfg<2, float>(g, cs, out)) return true;
   }
@@ -625,6 +840,10 @@ inline bool cluster_config(const Geo& g, bool rho, ClusterCfg* out) {
 template <class K, class... Args>
 inline cudaError_t launch_cluster(K kernel, const ClusterCfg& c, int U, size_t smem,
                                   cudaStream_t st, Args... args) {
+  // the dynamic shared-memory limit is per kernel, not per plan: plans with
+  // different receiver / ring counts need their own size set before launching
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(U * c.cs);
   cfg.blockDim = dim3(c.threads);
@@ -646,12 +865,12 @@ inline cudaError_t cluster_forward_t(const Geo& g, const Model& m, const Cluster
                                      float* ubuf, cudaStream_t st) {
   if (mode == 0)
     return launch_cluster(cluster_fwd_kernel<RPT, T, 0>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
-                          unit_begin, U, rec, hist, strips, ubuf);
+                          c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
   if (mode == 1)
     return launch_cluster(cluster_fwd_kernel<RPT, T, 1>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
-                          unit_begin, U, rec, hist, strips, ubuf);
+                          c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
   return launch_cluster(cluster_fwd_kernel<RPT, T, 2>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
-                        unit_begin, U, rec, hist, strips, ubuf);
+                        c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
 }
 
 template <int RPT, class T>
@@ -661,9 +880,9 @@ inline cudaError_t cluster_adjoint_t(const Geo& g, const Model& m, const Cluster
                                      int acc_off, cudaStream_t st) {
   if (mode == 1)
     return launch_cluster(cluster_adj_kernel<RPT, T, 1>, c, U, c.smem_adj, st, g, m, c.cs, c.rows,
-                          unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off);
+                          c.maxrec, c.maxring, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off);
   return launch_cluster(cluster_adj_kernel<RPT, T, 2>, c, U, c.smem_adj, st, g, m, c.cs, c.rows,
-                        unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off);
+                        c.maxrec, c.maxring, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off);
 }
 
 inline int cluster_forward(const Geo& g, const Model& m, const ClusterCfg& c, bool /*rho*/,
