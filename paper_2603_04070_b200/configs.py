@@ -72,8 +72,9 @@ CONFIGS: dict[int, WorkloadSpec] = {
                     8, 5, (1, 6), "ellipse", (10.0, 40.0), 60.0, True, 0.01),
     3: WorkloadSpec("config3-strips", 512, 24, 5e-5, 1e-8, 4000, 2.5e6, 256, 128, 2, 256,
                     1, 3, (1, 6), "ellipse", (10.0, 40.0), 60.0, True, 0.01, strips=True),
+    # config 4 names "random multi-inclusion SoS phantoms": speed of sound only
     4: WorkloadSpec("config4-scaling", 1024, 32, 5e-5, 1e-8, 6000, 2.5e6, 256, 256, 1, 256,
-                    4, 0, (1, 6), "ellipse", (10.0, 40.0), 60.0, True, 0.01, strips=True),
+                    4, 0, (1, 6), "ellipse", (10.0, 40.0), 60.0, False, 0.01, strips=True),
 }
 
 

@@ -11,6 +11,7 @@
 #include "dufwi_aux_kernels.cuh"
 #include "dufwi_cluster_kernels.cuh"
 #include "dufwi_step_kernels.cuh"
+#include "dufwi_vec_kernels.cuh"
 
 using namespace dufwi;
 
@@ -120,16 +121,22 @@ Groups fwd_groups(const Geo& g, int unit_begin, int U) { return make_groups(g, u
 
 // Adjoint: as many shots per group as the warp target allows (one f64
 // accumulator read-modify-write per cell, group and step).
-Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit) {
+Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec) {
   if (per_unit) return make_groups(g, unit_begin, U, 1);
-  const long wanted = std::max(1L, (kTargetWarps + warps_per_group(g) - 1) / warps_per_group(g));
+  const long wpg = vec ? (long)((g.nz + 127) / 128) * ((g.nx + kVecAdjTX - 1) / kVecAdjTX)
+                       : warps_per_group(g);
+  const long target = vec ? 148L * 32 : kTargetWarps;
+  const long wanted = std::max(1L, (target + wpg - 1) / wpg);
   int gs = (int)std::max(1L, ((long)U + wanted - 1) / wanted);
-  gs = (gs + kNSA - 1) / kNSA * kNSA;
+  if (!vec) gs = (gs + kNSA - 1) / kNSA * kNSA;
   return make_groups(g, unit_begin, U, gs);
 }
 
-Groups groups_for(const Geo& g, int unit_begin, int U, bool per_unit) {
-  return adj_groups(g, unit_begin, U, per_unit);
+// Vectorised stepwise kernels: constant density, rows made of whole float4s.
+bool use_vec(const dufwi_plan_t* p) { return !p->has_rho && p->geo.nz % 4 == 0; }
+
+Groups groups_for(const dufwi_plan_t* p, int unit_begin, int U, bool per_unit) {
+  return adj_groups(p->geo, unit_begin, U, per_unit, use_vec(p));
 }
 
 // Upper bound of the group count over every placement of U units.
@@ -166,7 +173,7 @@ int max_groups(const dufwi_plan_t* p, int U, bool per_unit) {
   int best = 0;
   // the count only depends on the start modulo S (and on clipping at the end)
   for (int start = 0; start < std::min(g.S, std::max(1, total - U + 1)); ++start)
-    best = std::max(best, groups_for(g, start, U, per_unit).ngroups);
+    best = std::max(best, groups_for(p, start, U, per_unit).ngroups);
   return std::max(best, 1);
 }
 
@@ -434,6 +441,14 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   } else {
     p->last_engine = DUFWI_ENGINE_STEPWISE;
     const Groups G = fwd_groups(g, unit_begin, U);
+    // vectorised kernel: constant density, rows of whole float4s
+    const bool vec = use_vec(p);
+    int vtx = 4;
+    for (int c : {32, 16, 8, 4}) {
+      const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
+      if (warps >= 148L * 32) { vtx = c; break; }
+    }
+    const dim3 vgrid((g.nz + 127) / 128, (g.nx + kVecWarps * vtx - 1) / (kVecWarps * vtx), U);
     dim3 block(kWarpsX * 32);
     dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXF - 1) / (kWarpsX * kRXF), G.ngroups);
     for (int t = 0; t < g.nt; ++t) {
@@ -454,12 +469,18 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
 #define DUFWI_FWD(R, M)                                                                         \
   fwd_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, u1, u2,   \
                                                   uo, rec_t, st_t, has1, has2)
-      if (p->has_rho) {
+#define DUFWI_VEC(M)                                                                            \
+  fwd_vec_kernel<M><<<vgrid, kVecWarps * 32, 0, st>>>(g, m, p->ab, t, unit_begin, vtx, u1, u2,   \
+                                                      uo, rec_t, st_t, has1, has2)
+      if (vec) {
+        if (mode == 0) DUFWI_VEC(0); else if (mode == 1) DUFWI_VEC(1); else DUFWI_VEC(2);
+      } else if (p->has_rho) {
         if (mode == 0) DUFWI_FWD(true, 0); else if (mode == 1) DUFWI_FWD(true, 1); else DUFWI_FWD(true, 2);
       } else {
         if (mode == 0) DUFWI_FWD(false, 0); else if (mode == 1) DUFWI_FWD(false, 1); else DUFWI_FWD(false, 2);
       }
 #undef DUFWI_FWD
+#undef DUFWI_VEC
       LAUNCH_CHECK(p);
     }
   }
@@ -523,7 +544,7 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   const size_t fieldU = (size_t)U * N2;
 
   const bool clus = use_cluster(p);
-  const Groups G = groups_for(g, unit_begin, U, clus);
+  const Groups G = groups_for(p, unit_begin, U, clus);
   if (clus) {
     p->last_engine = DUFWI_ENGINE_CLUSTER;
     // per-unit accumulators: with one shot per group, group index == chunk-local unit
@@ -550,6 +571,28 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     const float* utm1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
     const float* st_tm1 = (mode == DUFWI_STORE_STRIPS && do_img) ? strips + (size_t)(t - 1) * U * g.SL : nullptr;
     const int do_recon = t >= 2;
+    if (use_vec(p)) {
+      // split adjoint: lam update (12 B/update) then imaging + reconstruction
+      int vtx = 4;
+      for (int c : {32, 16, 8, 4}) {
+        const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
+        if (warps >= 148L * 32) { vtx = c; break; }
+      }
+      const dim3 lgrid((g.nz + 127) / 128, (g.nx + kVecWarps * vtx - 1) / (kVecWarps * vtx), U);
+      adjlam_vec_kernel<<<lgrid, kVecWarps * 32, 0, st>>>(g, m, p->ab, t, unit_begin, vtx, l1, l2o,
+                                                          rres_t, has1, has2);
+      LAUNCH_CHECK(p);
+      if (do_img) {
+        const dim3 igrid((g.nz + 127) / 128,
+                         (g.nx + kVecAdjWarps * kVecAdjTX - 1) / (kVecAdjWarps * kVecAdjTX), G.ngroups);
+        if (mode == DUFWI_STORE_FULL)
+          img_vec_kernel<1><<<igrid, kVecAdjWarps * 32, 0, st>>>(g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm1, acc_part, do_recon);
+        else
+          img_vec_kernel<2><<<igrid, kVecAdjWarps * 32, 0, st>>>(g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm1, acc_part, do_recon);
+        LAUNCH_CHECK(p);
+      }
+      continue;
+    }
 #define DUFWI_ADJ(R, M)                                                                          \
   adj_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o,  \
                                                   F, ut, utm1, st_tm1,                            \

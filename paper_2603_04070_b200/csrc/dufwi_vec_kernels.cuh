@@ -1,0 +1,681 @@
+// Stepwise engine, vectorised forward step (nz % 4 == 0, constant density).
+//
+// A warp owns a 128-wide z strip — each lane 4 consecutive cells, loaded and
+// stored as one float4 — and walks TX x-rows of ONE shot, keeping rows x-1,
+// x, x+1 in f64 registers (every f32 value converted once).  The next row's
+// loads (u[t-1] row x+2, u[t-2] row x+1, E row x+1) are issued before the
+// current row is computed, so each warp keeps a row of loads in flight while
+// it computes.  z-neighbours come from f64 warp shuffles; the strip's outer
+// neighbours (z0-1, z0+128) are two scalar loads per row (L1/L2 hits).
+// DRAM per cell update: read u[t-1], u[t-2]; write u[t] = 12 B.
+#pragma once
+
+#include "dufwi_step_kernels.cuh"
+
+namespace dufwi {
+
+constexpr int kVecWarps = 8;  // warps per CTA, stacked along x
+
+struct Row4 {
+  double v[4];
+};
+
+__device__ __forceinline__ Row4 to_d(float4 f) {
+  Row4 r;
+  r.v[0] = f.x;
+  r.v[1] = f.y;
+  r.v[2] = f.z;
+  r.v[3] = f.w;
+  return r;
+}
+
+// (A, B) for the 4 cells of a lane: fast path (2, -1) when the row and the
+// lane's cells are undamped, else the 1-D tables (or the 2-D map).
+__device__ __forceinline__ void ab4(const ABTables& T, int x, int z4, int nz, bool lane_damped,
+                                    double (&A)[4], double (&B)[4]) {
+  const double px = T.px ? __ldg(T.px + x) : 0.0;
+  if (T.px && px == 0.0 && !lane_damped) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { A[k] = 2.0; B[k] = -1.0; }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int z = min(z4 + k, nz - 1);
+    if (T.px) {
+      const double pz = __ldg(T.pz + z);
+      const bool xs = px >= pz;
+      A[k] = xs ? __ldg(T.Ax + x) : __ldg(T.Az + z);
+      B[k] = xs ? __ldg(T.Bx + x) : __ldg(T.Bz + z);
+    } else {
+      A[k] = __ldg(T.A2 + (size_t)x * nz + z);
+      B[k] = __ldg(T.B2 + (size_t)x * nz + z);
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kVecWarps * 32)
+    fwd_vec_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
+                   const float* __restrict__ u1, const float* u2, float* uo,
+                   float* __restrict__ rec_t, float* __restrict__ strip_t, int has1, int has2) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nz = g.nz, nx = g.nx;
+  const int z0 = blockIdx.x * 128;
+  const int z4 = z0 + 4 * lane;
+  const bool act = z4 < nz;
+  const int x0 = (blockIdx.y * kVecWarps + warp) * TX;
+  if (x0 >= nx) return;  // warp-uniform
+  const int x1 = min(nx, x0 + TX);
+  const int lu = blockIdx.z;
+  const int u = unit_begin + lu;
+  const int b = u / g.S;
+  const int s = u - b * g.S;
+  const size_t N2 = (size_t)nx * nz;
+  const float* f1 = u1 + (size_t)lu * N2;
+  const float* f2 = u2 + (size_t)lu * N2;
+  float* fo = uo + (size_t)lu * N2;
+  const double* Ed = m.Ed + (size_t)b * N2;
+  const int txx = __ldg(g.tx + 2 * s), txz = __ldg(g.tx + 2 * s + 1);
+  const int tk = (txz >= z4 && txz < z4 + 4) ? txz - z4 : -1;  // my cell index of the source
+  const double pulse_t = __ldg(g.pulse + t);
+  bool lane_damped = false;
+  if (T.px && act) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lane_damped |= __ldg(T.pz + min(z4 + k, nz - 1)) != 0.0;
+  }
+  const bool ld1 = has1 != 0 && act;
+  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
+
+  auto ld_row = [&](int x, float& el, float& er) -> float4 {
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    el = er = 0.f;
+    if (has1 && x >= 0 && x < nx) {
+      const float* p = f1 + (size_t)x * nz;
+      if (act) r = __ldg(reinterpret_cast<const float4*>(p + z4));
+      if (edge_l) el = __ldg(p + z0 - 1);
+      if (edge_r) er = __ldg(p + z0 + 128);
+    }
+    return r;
+  };
+  (void)ld1;
+
+  float elm, erm, elc, erc, eln, ern;
+  Row4 um = to_d(ld_row(x0 - 1, elm, erm));
+  Row4 uc = to_d(ld_row(x0, elc, erc));
+  // prefetch for row x0
+  float4 p_up = ld_row(x0 + 1, eln, ern);
+  float4 p_u2 = (has2 && act) ? *reinterpret_cast<const float4*>(f2 + (size_t)x0 * nz + z4)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+  double2 p_e0 = act ? __ldg(reinterpret_cast<const double2*>(Ed + (size_t)x0 * nz + z4)) : make_double2(0, 0);
+  double2 p_e1 = act ? __ldg(reinterpret_cast<const double2*>(Ed + (size_t)x0 * nz + z4 + 2)) : make_double2(0, 0);
+  (void)elm;
+  (void)erm;
+
+  for (int x = x0; x < x1; ++x) {
+    const float4 c_up = p_up;
+    const float4 c_u2 = p_u2;
+    const double ed[4] = {p_e0.x, p_e0.y, p_e1.x, p_e1.y};
+    const float el_up = eln, er_up = ern;
+    // prefetch the next row's operands
+    if (x + 1 < x1) {
+      p_up = ld_row(x + 2, eln, ern);
+      const size_t rn = (size_t)(x + 1) * nz + z4;
+      p_u2 = (has2 && act) ? *reinterpret_cast<const float4*>(f2 + rn) : make_float4(0.f, 0.f, 0.f, 0.f);
+      p_e0 = act ? __ldg(reinterpret_cast<const double2*>(Ed + rn)) : make_double2(0, 0);
+      p_e1 = act ? __ldg(reinterpret_cast<const double2*>(Ed + rn + 2)) : make_double2(0, 0);
+    }
+    const Row4 up = to_d(c_up);
+    const Row4 w2 = to_d(c_u2);
+    // z-neighbours of row x: lanes exchange their outer cells
+    double zl = __shfl_up_sync(0xffffffffu, uc.v[3], 1);
+    double zr = __shfl_down_sync(0xffffffffu, uc.v[0], 1);
+    if (lane == 0) zl = (double)elc;
+    if (lane == 31) zr = (double)erc;
+    double A[4], B[4];
+    ab4(T, x, z4, nz, lane_damped, A, B);
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double zm = k == 0 ? zl : uc.v[k - 1];
+      const double zp = k == 3 ? zr : uc.v[k + 1];
+      const double lap = (((-4.0 * uc.v[k] + um.v[k]) + up.v[k]) + zm) + zp;
+      v[k] = A[k] * uc.v[k] + B[k] * w2.v[k] + ed[k] * lap;
+    }
+    if (x == txx && tk >= 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k == tk) v[k] += pulse_t;
+    }
+    if (act) {
+      const size_t row = (size_t)x * nz;
+      *reinterpret_cast<float4*>(fo + row + z4) =
+          make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
+      if (__ldg(g.row_flag + x)) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int slot = __ldg(g.node_slot + row + z4 + k);
+          if (slot >= 0) rec_t[(size_t)lu * g.M + slot] = (float)v[k];
+        }
+      }
+      if (MODE == 2) {
+        float* st = strip_t + (size_t)lu * g.SL;
+        const bool xr = x == g.x_lo - 1 || x == g.x_hi + 1;
+        const bool xin = x >= g.x_lo && x <= g.x_hi;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int z = z4 + k;
+          if (xr && z >= g.z_lo && z <= g.z_hi)
+            st[(x == g.x_lo - 1 ? 0 : g.Lz) + z - g.z_lo] = (float)v[k];
+          if (xin && (z == g.z_lo - 1 || z == g.z_hi + 1))
+            st[2 * g.Lz + (z == g.z_lo - 1 ? 0 : g.Lx) + x - g.x_lo] = (float)v[k];
+        }
+      }
+    }
+    um = uc;
+    uc = up;
+    elc = el_up;
+    erc = er_up;
+  }
+}
+
+}  // namespace dufwi
+
+namespace dufwi {
+
+// ---------------------------------------------------------------------------
+// Vectorised adjoint step (constant density, nz % 4 == 0).  A warp owns a
+// 128-wide z strip × TX rows of one phantom and walks the shots of its group
+// one after another; per shot it streams the rows of lam[t+1] (with E/dx^2
+// for the transposed operator) and of u[t-1] (buffer; ring cells from the
+// strips, MODE 2 — or the full history, MODE 1), writes lam[t] in place over
+// lam[t+2] and reconstructs u[t-2] in place over u[t] on the undamped box.
+// The imaging sum of all the group's shots is kept in a per-warp shared tile
+// and added to acc_part[group] once per step (deterministic shot order).
+constexpr int kVecAdjWarps = 4;
+constexpr int kVecAdjTX = 8;
+
+template <int MODE>
+__global__ void __launch_bounds__(kVecAdjWarps * 32)
+    adj_vec_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int U, int gs,
+                   const float* __restrict__ l1, float* l2o, const float* __restrict__ F,
+                   float* ut, const float* __restrict__ utm1,
+                   const float* __restrict__ strip_tm1, const double* __restrict__ rres_t,
+                   double* __restrict__ acc_part, int has1, int has2, int do_img, int do_recon) {
+  __shared__ double acc_s[kVecAdjWarps][kVecAdjTX][128];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nz = g.nz, nx = g.nx;
+  const int z0 = blockIdx.x * 128;
+  const int z4 = z0 + 4 * lane;
+  const bool act = z4 < nz;
+  const int x0 = (blockIdx.y * kVecAdjWarps + warp) * kVecAdjTX;
+  if (x0 >= nx) return;
+  const int x1 = min(nx, x0 + kVecAdjTX);
+  const ShotGroup sg = shot_group(g, blockIdx.z, unit_begin, U, gs);
+  if (sg.n == 0) return;
+  const size_t N2 = (size_t)nx * nz;
+  const double* Ed = m.Ed + (size_t)sg.b * N2;
+  const double pulse_t = __ldg(g.pulse + t);
+  bool lane_damped = false;
+  if (T.px && act) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lane_damped |= __ldg(T.pz + min(z4 + k, nz - 1)) != 0.0;
+  }
+  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
+  double(&acc)[kVecAdjTX][128] = acc_s[warp];
+#pragma unroll
+  for (int r = 0; r < kVecAdjTX; ++r)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[r][4 * lane + k] = 0.0;
+
+  // per-lane ring-column flags (MODE 2): the strip replaces the buffer there
+  int ringk[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int z = z4 + k;
+    ringk[k] = (z == g.z_lo - 1) ? 2 * g.Lz : (z == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;
+  }
+
+  auto ld4 = [&](const float* p, int x) -> Row4 {
+    Row4 r;
+    const float4 f = (act && x >= 0 && x < nx) ? __ldg(reinterpret_cast<const float4*>(p + (size_t)x * nz + z4))
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+    r = to_d(f);
+    return r;
+  };
+  auto ld_ed = [&](int x) -> Row4 {
+    Row4 r;
+    if (act && x >= 0 && x < nx) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(Ed + (size_t)x * nz + z4));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(Ed + (size_t)x * nz + z4 + 2));
+      r.v[0] = a.x; r.v[1] = a.y; r.v[2] = b.x; r.v[3] = b.y;
+    } else {
+      r.v[0] = r.v[1] = r.v[2] = r.v[3] = 0.0;
+    }
+    return r;
+  };
+  auto edge = [&](const float* p, int x, bool right) -> double {
+    if (x < 0 || x >= nx) return 0.0;
+    if (right) return edge_r ? (double)__ldg(p + (size_t)x * nz + z0 + 128) : 0.0;
+    return edge_l ? (double)__ldg(p + (size_t)x * nz + z0 - 1) : 0.0;
+  };
+  auto edge_ed = [&](int x, bool right) -> double {
+    if (x < 0 || x >= nx) return 0.0;
+    if (right) return edge_r ? __ldg(Ed + (size_t)x * nz + z0 + 128) : 0.0;
+    return edge_l ? __ldg(Ed + (size_t)x * nz + z0 - 1) : 0.0;
+  };
+  // u[t-1] as the reconstruction sees it (MODE 2): buffer on the box, strips on the ring
+  auto ld_u = [&](const float* ub, const float* st, int x, double& el, double& er) -> Row4 {
+    Row4 r;
+    r.v[0] = r.v[1] = r.v[2] = r.v[3] = 0.0;
+    el = er = 0.0;
+    if (x < 0 || x >= nx) return r;
+    if (MODE == 1) {
+      r = ld4(ub, x);
+      el = edge(ub, x, false);
+      er = edge(ub, x, true);
+      return r;
+    }
+    const bool xbox = x >= g.x_lo && x <= g.x_hi;
+    const bool xring = x == g.x_lo - 1 || x == g.x_hi + 1;
+    if (xbox) {
+      r = ld4(ub, x);
+      el = edge(ub, x, false);
+      er = edge(ub, x, true);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int z = z4 + k;
+        if (ringk[k] >= 0) r.v[k] = (double)__ldg(st + ringk[k] + x - g.x_lo);
+        else if (z < g.z_lo || z > g.z_hi) r.v[k] = 0.0;
+      }
+      // strip edges: the neighbouring strip's outer cell may be a ring column
+      if (edge_l) {
+        const int z = z0 - 1;
+        el = (z == g.z_lo - 1) ? (double)__ldg(st + 2 * g.Lz + x - g.x_lo)
+                               : (z >= g.z_lo && z <= g.z_hi ? el : 0.0);
+      }
+      if (edge_r) {
+        const int z = z0 + 128;
+        er = (z == g.z_hi + 1) ? (double)__ldg(st + 2 * g.Lz + g.Lx + x - g.x_lo)
+                               : (z >= g.z_lo && z <= g.z_hi ? er : 0.0);
+      }
+    } else if (xring) {
+      const float* sr = st + (x == g.x_lo - 1 ? 0 : g.Lz);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int z = z4 + k;
+        r.v[k] = (act && z >= g.z_lo && z <= g.z_hi) ? (double)__ldg(sr + z - g.z_lo) : 0.0;
+      }
+      if (edge_l && z0 - 1 >= g.z_lo && z0 - 1 <= g.z_hi) el = (double)__ldg(sr + z0 - 1 - g.z_lo);
+      if (edge_r && z0 + 128 >= g.z_lo && z0 + 128 <= g.z_hi) er = (double)__ldg(sr + z0 + 128 - g.z_lo);
+    }
+    return r;
+  };
+
+  for (int k0 = 0; k0 < sg.n; ++k0) {
+    const int lu = sg.lu0 + k0;
+    const size_t fo = (size_t)lu * N2;
+    const int s = (unit_begin + lu) % g.S;
+    const int txx = __ldg(g.tx + 2 * s), txz = __ldg(g.tx + 2 * s + 1);
+    const int tk = (txz >= z4 && txz < z4 + 4) ? txz - z4 : -1;
+    const float* L1 = l1 + fo;
+    const float* st = MODE == 2 ? strip_tm1 + (size_t)lu * g.SL : nullptr;
+    const float* UB = MODE == 1 ? F + fo : utm1 + fo;
+    // rolling rows: E*lam1 (em, ec, ep) + raw lam1 centre, u[t-1] (fm, fc, fp)
+    Row4 edm = ld_ed(x0 - 1), edc = ld_ed(x0);
+    Row4 lm = has1 ? ld4(L1, x0 - 1) : Row4{}, lc = has1 ? ld4(L1, x0) : Row4{};
+    double elc_l = has1 ? edge(L1, x0, false) * edge_ed(x0, false) : 0.0;
+    double elc_r = has1 ? edge(L1, x0, true) * edge_ed(x0, true) : 0.0;
+    Row4 em, ec;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { em.v[k] = edm.v[k] * lm.v[k]; ec.v[k] = edc.v[k] * lc.v[k]; }
+    double fcl = 0.0, fcr = 0.0, tmp_l, tmp_r;
+    Row4 fm{}, fc{};
+    if (do_img) {
+      fm = ld_u(UB, st, x0 - 1, tmp_l, tmp_r);
+      fc = ld_u(UB, st, x0, fcl, fcr);
+    }
+    for (int x = x0; x < x1; ++x) {
+      const size_t row = (size_t)x * nz;
+      // next rows
+      const Row4 edp = ld_ed(x + 1);
+      const Row4 lp = has1 ? ld4(L1, x + 1) : Row4{};
+      const double elp_l = has1 ? edge(L1, x + 1, false) * edge_ed(x + 1, false) : 0.0;
+      const double elp_r = has1 ? edge(L1, x + 1, true) * edge_ed(x + 1, true) : 0.0;
+      Row4 ep;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ep.v[k] = edp.v[k] * lp.v[k];
+      double fpl = 0.0, fpr = 0.0;
+      Row4 fp{};
+      if (do_img) fp = ld_u(UB, st, x + 1, fpl, fpr);
+      const float4 l2f = (has2 && act) ? *reinterpret_cast<const float4*>(l2o + fo + row + z4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      const Row4 l2v = to_d(l2f);
+      double A[4], B[4];
+      ab4(T, x, z4, nz, lane_damped, A, B);
+      // z-neighbours
+      double ezl = __shfl_up_sync(0xffffffffu, ec.v[3], 1);
+      double ezr = __shfl_down_sync(0xffffffffu, ec.v[0], 1);
+      if (lane == 0) ezl = elc_l;
+      if (lane == 31) ezr = elc_r;
+      double fzl = __shfl_up_sync(0xffffffffu, fc.v[3], 1);
+      double fzr = __shfl_down_sync(0xffffffffu, fc.v[0], 1);
+      if (lane == 0) fzl = fcl;
+      if (lane == 31) fzr = fcr;
+      double lam[4], lapu[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double zm = k == 0 ? ezl : ec.v[k - 1];
+        const double zp = k == 3 ? ezr : ec.v[k + 1];
+        const double adj = (((-4.0 * ec.v[k] + em.v[k]) + ep.v[k]) + zm) + zp;
+        lam[k] = (A[k] * lc.v[k] + adj) + B[k] * l2v.v[k];
+        const double fzm = k == 0 ? fzl : fc.v[k - 1];
+        const double fzp = k == 3 ? fzr : fc.v[k + 1];
+        lapu[k] = (((-4.0 * fc.v[k] + fm.v[k]) + fp.v[k]) + fzm) + fzp;
+      }
+      if (act) {
+        if (__ldg(g.row_flag + x)) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int slot = __ldg(g.node_slot + row + z4 + k);
+            if (slot >= 0) lam[k] += __ldg(rres_t + (size_t)lu * g.M + slot);
+          }
+        }
+        *reinterpret_cast<float4*>(l2o + fo + row + z4) =
+            make_float4((float)lam[0], (float)lam[1], (float)lam[2], (float)lam[3]);
+        if (do_img) {
+          const bool xbox = MODE == 1 || (x >= g.x_lo && x <= g.x_hi);
+          double* ar = acc[x - x0];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int z = z4 + k;
+            const bool in = MODE == 1 || (xbox && z >= g.z_lo && z <= g.z_hi);
+            if (in) ar[4 * lane + k] += lapu[k] * lam[k];
+          }
+          if (MODE == 2 && do_recon && xbox) {
+            const float4 uf = *reinterpret_cast<const float4*>(ut + fo + row + z4);
+            const Row4 uv = to_d(uf);
+            float o[4] = {uf.x, uf.y, uf.z, uf.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int z = z4 + k;
+              if (z >= g.z_lo && z <= g.z_hi) {
+                double prev = 2.0 * fc.v[k] + edc.v[k] * lapu[k] - uv.v[k];
+                if (x == txx && k == tk) prev += pulse_t;
+                o[k] = (float)prev;
+              }
+            }
+            *reinterpret_cast<float4*>(ut + fo + row + z4) = make_float4(o[0], o[1], o[2], o[3]);
+          }
+        }
+      }
+      // roll
+      edm = edc; edc = edp;
+      lm = lc; lc = lp;
+      em = ec; ec = ep;
+      elc_l = elp_l; elc_r = elp_r;
+      fm = fc; fc = fp;
+      fcl = fpl; fcr = fpr;
+    }
+  }
+  if (do_img && act) {
+    double* dst = acc_part + (size_t)blockIdx.z * N2;
+    for (int x = x0; x < x1; ++x)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[(size_t)x * nz + z4 + k] += acc[x - x0][4 * lane + k];
+  }
+}
+
+}  // namespace dufwi
+
+namespace dufwi {
+
+// ---------------------------------------------------------------------------
+// Split vectorised adjoint (constant density, nz % 4 == 0), kernel 1 of 2:
+// lam[t] = A lam[t+1] + L^T(E lam[t+1]) + B lam[t+2] (+ merged residual at the
+// receiver nodes), in place over lam[t+2].  Same streaming/prefetch structure
+// as fwd_vec_kernel, one shot per warp.  DRAM: 12 B per cell update.
+__global__ void __launch_bounds__(kVecWarps * 32)
+    adjlam_vec_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
+                      const float* __restrict__ l1, float* l2o, const double* __restrict__ rres_t,
+                      int has1, int has2) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nz = g.nz, nx = g.nx;
+  const int z0 = blockIdx.x * 128;
+  const int z4 = z0 + 4 * lane;
+  const bool act = z4 < nz;
+  const int x0 = (blockIdx.y * kVecWarps + warp) * TX;
+  if (x0 >= nx) return;
+  const int x1 = min(nx, x0 + TX);
+  const int lu = blockIdx.z;
+  const int b = (unit_begin + lu) / g.S;
+  const size_t N2 = (size_t)nx * nz;
+  const float* L1 = l1 + (size_t)lu * N2;
+  float* L2 = l2o + (size_t)lu * N2;
+  const double* Ed = m.Ed + (size_t)b * N2;
+  bool lane_damped = false;
+  if (T.px && act) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lane_damped |= __ldg(T.pz + min(z4 + k, nz - 1)) != 0.0;
+  }
+  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
+  // E*lam1 of row x: 4 own cells + the strip's two outer cells
+  struct ERow {
+    double e[4], l[4], el, er;
+  };
+  auto ld = [&](int x) -> ERow {
+    ERow r;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r.e[k] = r.l[k] = 0.0;
+    r.el = r.er = 0.0;
+    if (has1 && x >= 0 && x < nx) {
+      const size_t row = (size_t)x * nz;
+      if (act) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(L1 + row + z4));
+        const double2 a = __ldg(reinterpret_cast<const double2*>(Ed + row + z4));
+        const double2 c = __ldg(reinterpret_cast<const double2*>(Ed + row + z4 + 2));
+        r.l[0] = f.x; r.l[1] = f.y; r.l[2] = f.z; r.l[3] = f.w;
+        r.e[0] = a.x * r.l[0]; r.e[1] = a.y * r.l[1]; r.e[2] = c.x * r.l[2]; r.e[3] = c.y * r.l[3];
+      }
+      if (edge_l) r.el = __ldg(Ed + row + z0 - 1) * (double)__ldg(L1 + row + z0 - 1);
+      if (edge_r) r.er = __ldg(Ed + row + z0 + 128) * (double)__ldg(L1 + row + z0 + 128);
+    }
+    return r;
+  };
+  ERow rm = ld(x0 - 1), rc = ld(x0);
+  ERow rn = ld(x0 + 1);
+  float4 p_l2 = (has2 && act) ? *reinterpret_cast<const float4*>(L2 + (size_t)x0 * nz + z4)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int x = x0; x < x1; ++x) {
+    const ERow rp = rn;
+    const float4 c_l2 = p_l2;
+    if (x + 1 < x1) {
+      rn = ld(x + 2);
+      p_l2 = (has2 && act) ? *reinterpret_cast<const float4*>(L2 + (size_t)(x + 1) * nz + z4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const Row4 w2 = to_d(c_l2);
+    double zl = __shfl_up_sync(0xffffffffu, rc.e[3], 1);
+    double zr = __shfl_down_sync(0xffffffffu, rc.e[0], 1);
+    if (lane == 0) zl = rc.el;
+    if (lane == 31) zr = rc.er;
+    double A[4], B[4];
+    ab4(T, x, z4, nz, lane_damped, A, B);
+    double lam[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double zm = k == 0 ? zl : rc.e[k - 1];
+      const double zp = k == 3 ? zr : rc.e[k + 1];
+      const double adj = (((-4.0 * rc.e[k] + rm.e[k]) + rp.e[k]) + zm) + zp;
+      lam[k] = (A[k] * rc.l[k] + adj) + B[k] * w2.v[k];
+    }
+    if (act) {
+      const size_t row = (size_t)x * nz;
+      if (__ldg(g.row_flag + x)) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int slot = __ldg(g.node_slot + row + z4 + k);
+          if (slot >= 0) lam[k] += __ldg(rres_t + (size_t)lu * g.M + slot);
+        }
+      }
+      *reinterpret_cast<float4*>(L2 + row + z4) =
+          make_float4((float)lam[0], (float)lam[1], (float)lam[2], (float)lam[3]);
+    }
+    rm = rc;
+    rc = rp;
+  }
+}
+
+// Split vectorised adjoint, kernel 2 of 2: imaging sum_t L(u[t-1]) lam[t] over
+// the group's shots (per-warp shared tile, one read-modify-write of
+// acc_part[group] per step) and, MODE 2, the reconstruction
+// u[t-2] = 2 u[t-1] + E L u[t-1] + s[t] d_tx - u[t] in place over u[t] on the
+// undamped box, with the ring neighbours taken from strips[t-1].
+// DRAM per cell update: MODE 2 read u[t-1], u[t], lam[t], write u[t-2] = 16 B;
+// MODE 1 read u[t-1] (history), lam[t] = 8 B.
+template <int MODE>
+__global__ void __launch_bounds__(kVecAdjWarps * 32)
+    img_vec_kernel(Geo g, Model m, int t, int unit_begin, int U, int gs,
+                   const float* __restrict__ lam_t, const float* __restrict__ F, float* ut,
+                   const float* __restrict__ utm1, const float* __restrict__ strip_tm1,
+                   double* __restrict__ acc_part, int do_recon) {
+  __shared__ double acc_s[kVecAdjWarps][kVecAdjTX][128];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nz = g.nz, nx = g.nx;
+  const int z0 = blockIdx.x * 128;
+  const int z4 = z0 + 4 * lane;
+  const bool act = z4 < nz;
+  int x0 = (blockIdx.y * kVecAdjWarps + warp) * kVecAdjTX;
+  int x1 = min(nx, x0 + kVecAdjTX);
+  if (MODE == 2) {  // imaging and reconstruction live on the undamped box only
+    x0 = max(x0, g.x_lo);
+    x1 = min(x1, g.x_hi + 1);
+  }
+  if (x0 >= x1) return;
+  const ShotGroup sg = shot_group(g, blockIdx.z, unit_begin, U, gs);
+  if (sg.n == 0) return;
+  const size_t N2 = (size_t)nx * nz;
+  const double* Ed = m.Ed + (size_t)sg.b * N2;
+  const double pulse_t = __ldg(g.pulse + t);
+  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
+  double(&acc)[kVecAdjTX][128] = acc_s[warp];
+  const int xb = (blockIdx.y * kVecAdjWarps + warp) * kVecAdjTX;
+#pragma unroll
+  for (int r = 0; r < kVecAdjTX; ++r)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[r][4 * lane + k] = 0.0;
+  // which of my cells are in the box (MODE 2) / on a ring column
+  unsigned inbox = 0u;
+  int ringk[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int z = z4 + k;
+    if (MODE == 1 || (act && z >= g.z_lo && z <= g.z_hi)) inbox |= 1u << k;
+    ringk[k] = (MODE == 2 && z == g.z_lo - 1) ? 2 * g.Lz : (MODE == 2 && z == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;
+  }
+  const int ring_l = (MODE == 2 && z0 - 1 == g.z_lo - 1) ? 2 * g.Lz : -1;
+  const int ring_r = (MODE == 2 && z0 + 128 == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;
+  const bool in_l = MODE == 1 || (z0 - 1 >= g.z_lo && z0 - 1 <= g.z_hi);
+  const bool in_r = MODE == 1 || (z0 + 128 >= g.z_lo && z0 + 128 <= g.z_hi);
+
+  struct URow {
+    double v[4], el, er;
+  };
+  for (int k0 = 0; k0 < sg.n; ++k0) {
+    const int lu = sg.lu0 + k0;
+    const size_t fo = (size_t)lu * N2;
+    const int s = (unit_begin + lu) % g.S;
+    const int txx = __ldg(g.tx + 2 * s), txz = __ldg(g.tx + 2 * s + 1);
+    const int tk = (txz >= z4 && txz < z4 + 4) ? txz - z4 : -1;
+    const float* UB = MODE == 1 ? F + fo : utm1 + fo;
+    const float* st = MODE == 2 ? strip_tm1 + (size_t)lu * g.SL : nullptr;
+    // u[t-1] of row x as the reconstruction sees it
+    auto ld = [&](int x) -> URow {
+      URow r;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r.v[k] = 0.0;
+      r.el = r.er = 0.0;
+      if (x < 0 || x >= nx) return r;
+      const size_t row = (size_t)x * nz;
+      const bool xbox = MODE == 1 || (x >= g.x_lo && x <= g.x_hi);
+      if (xbox) {
+        if (act) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(UB + row + z4));
+          r.v[0] = f.x; r.v[1] = f.y; r.v[2] = f.z; r.v[3] = f.w;
+        }
+        if (edge_l) r.el = in_l ? (double)__ldg(UB + row + z0 - 1)
+                                : (ring_l >= 0 ? (double)__ldg(st + ring_l + x - g.x_lo) : 0.0);
+        if (edge_r) r.er = in_r ? (double)__ldg(UB + row + z0 + 128)
+                                : (ring_r >= 0 ? (double)__ldg(st + ring_r + x - g.x_lo) : 0.0);
+        if (MODE == 2) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (ringk[k] >= 0) r.v[k] = (double)__ldg(st + ringk[k] + x - g.x_lo);
+            else if (!(inbox & (1u << k))) r.v[k] = 0.0;
+          }
+        }
+      } else if (MODE == 2) {  // ring row above/below the box
+        const float* sr = st + (x == g.x_lo - 1 ? 0 : g.Lz);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (inbox & (1u << k)) r.v[k] = (double)__ldg(sr + z4 + k - g.z_lo);
+        if (edge_l && in_l) r.el = (double)__ldg(sr + z0 - 1 - g.z_lo);
+        if (edge_r && in_r) r.er = (double)__ldg(sr + z0 + 128 - g.z_lo);
+      }
+      return r;
+    };
+    URow rm = ld(x0 - 1), rc = ld(x0), rn = ld(x0 + 1);
+    for (int x = x0; x < x1; ++x) {
+      const URow rp = rn;
+      const size_t row = (size_t)x * nz;
+      const float4 lf = act ? __ldg(reinterpret_cast<const float4*>(lam_t + fo + row + z4))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 uf = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (MODE == 2 && do_recon && act) uf = *reinterpret_cast<const float4*>(ut + fo + row + z4);
+      double2 e0 = make_double2(0, 0), e1 = make_double2(0, 0);
+      if (MODE == 2 && do_recon && act) {
+        e0 = __ldg(reinterpret_cast<const double2*>(Ed + row + z4));
+        e1 = __ldg(reinterpret_cast<const double2*>(Ed + row + z4 + 2));
+      }
+      if (x + 1 < x1) rn = ld(x + 2);
+      double zl = __shfl_up_sync(0xffffffffu, rc.v[3], 1);
+      double zr = __shfl_down_sync(0xffffffffu, rc.v[0], 1);
+      if (lane == 0) zl = rc.el;
+      if (lane == 31) zr = rc.er;
+      const Row4 lam = to_d(lf);
+      const double ed[4] = {e0.x, e0.y, e1.x, e1.y};
+      const Row4 uv = to_d(uf);
+      float o[4] = {uf.x, uf.y, uf.z, uf.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double zm = k == 0 ? zl : rc.v[k - 1];
+        const double zp = k == 3 ? zr : rc.v[k + 1];
+        const double lapu = (((-4.0 * rc.v[k] + rm.v[k]) + rp.v[k]) + zm) + zp;
+        if (inbox & (1u << k)) {
+          acc[x - xb][4 * lane + k] += lapu * lam.v[k];
+          if (MODE == 2 && do_recon) {
+            double prev = 2.0 * rc.v[k] + ed[k] * lapu - uv.v[k];
+            if (x == txx && k == tk) prev += pulse_t;
+            o[k] = (float)prev;
+          }
+        }
+      }
+      if (MODE == 2 && do_recon && act)
+        *reinterpret_cast<float4*>(ut + fo + row + z4) = make_float4(o[0], o[1], o[2], o[3]);
+      rm = rc;
+      rc = rp;
+    }
+  }
+  if (act) {
+    double* dst = acc_part + (size_t)blockIdx.z * N2;
+    for (int x = x0; x < x1; ++x)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[(size_t)x * nz + z4 + k] += acc[x - xb][4 * lane + k];
+  }
+}
+
+}  // namespace dufwi
