@@ -448,7 +448,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
       const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
       if (warps >= 148L * 32) { vtx = c; break; }
     }
-    const dim3 vgrid((g.nz + 127) / 128, (g.nx + kVecWarps * vtx - 1) / (kVecWarps * vtx), U);
+    const dim3 vgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
     dim3 block(kWarpsX * 32);
     dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXF - 1) / (kWarpsX * kRXF), G.ngroups);
     for (int t = 0; t < g.nt; ++t) {
@@ -470,8 +470,8 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   fwd_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, u1, u2,   \
                                                   uo, rec_t, st_t, has1, has2)
 #define DUFWI_VEC(M)                                                                            \
-  fwd_vec_kernel<M><<<vgrid, kVecWarps * 32, 0, st>>>(g, m, p->ab, t, unit_begin, vtx, u1, u2,   \
-                                                      uo, rec_t, st_t, has1, has2)
+  fwd_vec_kernel<M><<<vgrid, kPipeWarps * 32, sizeof(FwdRing), st>>>(g, m, p->ab, t, unit_begin, \
+                                                      vtx, u1, u2, uo, rec_t, st_t, has1, has2)
       if (vec) {
         if (mode == 0) DUFWI_VEC(0); else if (mode == 1) DUFWI_VEC(1); else DUFWI_VEC(2);
       } else if (p->has_rho) {

@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(kWarpsX * 32)
   const int zc = L.zin ? L.z : 0;
   const int z = L.z;
   const bool zbox = z >= g.z_lo && z <= g.z_hi;
-  const int ringz = (z == g.z_lo - 1) ? 2 * g.Lz : (z == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;
+  // ring columns inside the grid only (no PML: the ring lies outside, = 0)
+  const int ringz = !L.zin ? -1 : (z == g.z_lo - 1) ? 2 * g.Lz : (z == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;
 
   // per-phantom coefficients (shared by every shot of the group)
   double edv[kRXA + 2];

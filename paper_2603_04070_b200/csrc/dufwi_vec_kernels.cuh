@@ -29,43 +29,82 @@ __device__ __forceinline__ Row4 to_d(float4 f) {
   return r;
 }
 
-// (A, B) for the 4 cells of a lane: fast path (2, -1) when the row and the
-// lane's cells are undamped, else the 1-D tables (or the 2-D map).
+// (A, B) of one cell in the damping band: the 1-D tables (or the 2-D map).
+// Kept out of line (returned in registers) so the undamped fast path carries
+// none of its address arithmetic.
+__device__ __noinline__ double2 ab_damped(ABTables T, int x, int z, int nz) {
+  if (T.px) {
+    const bool xs = __ldg(T.px + x) >= __ldg(T.pz + z);
+    return make_double2(xs ? __ldg(T.Ax + x) : __ldg(T.Az + z),
+                        xs ? __ldg(T.Bx + x) : __ldg(T.Bz + z));
+  }
+  const size_t i = (size_t)x * nz + z;
+  return make_double2(__ldg(T.A2 + i), __ldg(T.B2 + i));
+}
+
+// (A, B) for the 4 cells of a lane: (2, -1) when the row and the lane's cells
+// are undamped, else per cell from the tables.
 __device__ __forceinline__ void ab4(const ABTables& T, int x, int z4, int nz, bool lane_damped,
                                     double (&A)[4], double (&B)[4]) {
-  const double px = T.px ? __ldg(T.px + x) : 0.0;
-  if (T.px && px == 0.0 && !lane_damped) {
+  if (T.px && !lane_damped && __ldg(T.px + x) == 0.0) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) { A[k] = 2.0; B[k] = -1.0; }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int z = min(z4 + k, nz - 1);
-    if (T.px) {
-      const double pz = __ldg(T.pz + z);
-      const bool xs = px >= pz;
-      A[k] = xs ? __ldg(T.Ax + x) : __ldg(T.Az + z);
-      B[k] = xs ? __ldg(T.Bx + x) : __ldg(T.Bz + z);
-    } else {
-      A[k] = __ldg(T.A2 + (size_t)x * nz + z);
-      B[k] = __ldg(T.B2 + (size_t)x * nz + z);
+    for (int k = 0; k < 4; ++k) {
+      const double2 ab = ab_damped(T, x, min(z4 + k, nz - 1), nz);
+      A[k] = ab.x;
+      B[k] = ab.y;
     }
   }
 }
 
+// cp.async helpers: per-lane asynchronous global->shared copies; src_size 0
+// zero-fills (rows outside the grid).  Each lane reads back only what it
+// copied, so the pipeline needs no inter-lane synchronisation.
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp4(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(ok ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kPipe = 4;       // rows of loads in flight per lane (power of two)
+constexpr int kPipeWarps = 4;  // warps per CTA (shared-memory ring per lane)
+
+// Per-lane ring of kPipe row slots, structure-of-arrays so every access is
+// bank-conflict free: u[t-1] row x+1 (+ strip edges), u[t-2] row x, E row x.
+struct FwdRing {
+  float4 u1[kPipe][kPipeWarps * 32];
+  float4 u2[kPipe][kPipeWarps * 32];
+  double2 e[kPipe][2][kPipeWarps * 32];
+  float2 edge[kPipe][kPipeWarps * 32];
+};
+
 template <int MODE>
-__global__ void __launch_bounds__(kVecWarps * 32)
+__global__ void __launch_bounds__(kPipeWarps * 32)
     fwd_vec_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
                    const float* __restrict__ u1, const float* u2, float* uo,
                    float* __restrict__ rec_t, float* __restrict__ strip_t, int has1, int has2) {
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FwdRing& ring = *reinterpret_cast<FwdRing*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
   const int nz = g.nz, nx = g.nx;
   const int z0 = blockIdx.x * 128;
   const int z4 = z0 + 4 * lane;
   const bool act = z4 < nz;
-  const int x0 = (blockIdx.y * kVecWarps + warp) * TX;
+  const int x0 = (blockIdx.y * kPipeWarps + warp) * TX;
   if (x0 >= nx) return;  // warp-uniform
   const int x1 = min(nx, x0 + TX);
   const int lu = blockIdx.z;
@@ -78,15 +117,38 @@ __global__ void __launch_bounds__(kVecWarps * 32)
   float* fo = uo + (size_t)lu * N2;
   const double* Ed = m.Ed + (size_t)b * N2;
   const int txx = __ldg(g.tx + 2 * s), txz = __ldg(g.tx + 2 * s + 1);
-  const int tk = (txz >= z4 && txz < z4 + 4) ? txz - z4 : -1;  // my cell index of the source
+  const int tk = (txz >= z4 && txz < z4 + 4) ? txz - z4 : -1;
   const double pulse_t = __ldg(g.pulse + t);
   bool lane_damped = false;
   if (T.px && act) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) lane_damped |= __ldg(T.pz + min(z4 + k, nz - 1)) != 0.0;
   }
-  const bool ld1 = has1 != 0 && act;
   const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
+  const int zc = act ? z4 : 0;
+
+  // issue the copies of "row r": u[t-1] row r+1 (+ edges), u[t-2] row r, E row r.
+  // 32-bit row offsets from per-lane base pointers keep the address math short.
+  const float* b1 = f1 + zc;
+  const float* b2 = f2 + zc;
+  const double* be = Ed + zc;
+  const float* bl = f1 + (edge_l ? z0 - 1 : 0);
+  const float* br = f1 + (edge_r ? z0 + 128 : 0);
+  const bool has2a = has2 && act;
+  auto issue = [&](int r) {
+    const int sl = r & (kPipe - 1);
+    const bool okn = r + 1 < nx;
+    const int ou = okn ? (r + 1) * nz : 0;
+    const int orr = r * nz;  // r < x1 <= nx
+    const bool ok1 = has1 && okn;
+    cp16(&ring.u1[sl][tid], b1 + ou, ok1 && act);
+    cp16(&ring.u2[sl][tid], b2 + orr, has2a);
+    cp16(&ring.e[sl][0][tid], be + orr, act);
+    cp16(&ring.e[sl][1][tid], be + orr + 2, act);
+    float* ed = reinterpret_cast<float*>(&ring.edge[sl][tid]);
+    cp4(ed, bl + ou, ok1 && edge_l);
+    cp4(ed + 1, br + ou, ok1 && edge_r);
+  };
 
   auto ld_row = [&](int x, float& el, float& er) -> float4 {
     float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -99,36 +161,27 @@ __global__ void __launch_bounds__(kVecWarps * 32)
     }
     return r;
   };
-  (void)ld1;
-
-  float elm, erm, elc, erc, eln, ern;
+  float elm, erm, elc, erc;
   Row4 um = to_d(ld_row(x0 - 1, elm, erm));
   Row4 uc = to_d(ld_row(x0, elc, erc));
-  // prefetch for row x0
-  float4 p_up = ld_row(x0 + 1, eln, ern);
-  float4 p_u2 = (has2 && act) ? *reinterpret_cast<const float4*>(f2 + (size_t)x0 * nz + z4)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-  double2 p_e0 = act ? __ldg(reinterpret_cast<const double2*>(Ed + (size_t)x0 * nz + z4)) : make_double2(0, 0);
-  double2 p_e1 = act ? __ldg(reinterpret_cast<const double2*>(Ed + (size_t)x0 * nz + z4 + 2)) : make_double2(0, 0);
   (void)elm;
   (void)erm;
+#pragma unroll
+  for (int k = 0; k < kPipe - 1; ++k) {
+    if (x0 + k < x1) issue(x0 + k);
+    cp_commit();
+  }
 
   for (int x = x0; x < x1; ++x) {
-    const float4 c_up = p_up;
-    const float4 c_u2 = p_u2;
-    const double ed[4] = {p_e0.x, p_e0.y, p_e1.x, p_e1.y};
-    const float el_up = eln, er_up = ern;
-    // prefetch the next row's operands
-    if (x + 1 < x1) {
-      p_up = ld_row(x + 2, eln, ern);
-      const size_t rn = (size_t)(x + 1) * nz + z4;
-      p_u2 = (has2 && act) ? *reinterpret_cast<const float4*>(f2 + rn) : make_float4(0.f, 0.f, 0.f, 0.f);
-      p_e0 = act ? __ldg(reinterpret_cast<const double2*>(Ed + rn)) : make_double2(0, 0);
-      p_e1 = act ? __ldg(reinterpret_cast<const double2*>(Ed + rn + 2)) : make_double2(0, 0);
-    }
-    const Row4 up = to_d(c_up);
-    const Row4 w2 = to_d(c_u2);
-    // z-neighbours of row x: lanes exchange their outer cells
+    if (x + kPipe - 1 < x1) issue(x + kPipe - 1);
+    cp_commit();
+    cp_wait<kPipe - 1>();  // the group of row x has landed
+    const int sl = x & (kPipe - 1);
+    const Row4 up = to_d(ring.u1[sl][tid]);
+    const Row4 w2 = to_d(ring.u2[sl][tid]);
+    const double2 e0 = ring.e[sl][0][tid], e1 = ring.e[sl][1][tid];
+    const float2 edn = ring.edge[sl][tid];
+    const double ed[4] = {e0.x, e0.y, e1.x, e1.y};
     double zl = __shfl_up_sync(0xffffffffu, uc.v[3], 1);
     double zr = __shfl_down_sync(0xffffffffu, uc.v[0], 1);
     if (lane == 0) zl = (double)elc;
@@ -163,21 +216,24 @@ __global__ void __launch_bounds__(kVecWarps * 32)
         float* st = strip_t + (size_t)lu * g.SL;
         const bool xr = x == g.x_lo - 1 || x == g.x_hi + 1;
         const bool xin = x >= g.x_lo && x <= g.x_hi;
+        if (xr || xin) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int z = z4 + k;
-          if (xr && z >= g.z_lo && z <= g.z_hi)
-            st[(x == g.x_lo - 1 ? 0 : g.Lz) + z - g.z_lo] = (float)v[k];
-          if (xin && (z == g.z_lo - 1 || z == g.z_hi + 1))
-            st[2 * g.Lz + (z == g.z_lo - 1 ? 0 : g.Lx) + x - g.x_lo] = (float)v[k];
+          for (int k = 0; k < 4; ++k) {
+            const int z = z4 + k;
+            if (xr && z >= g.z_lo && z <= g.z_hi)
+              st[(x == g.x_lo - 1 ? 0 : g.Lz) + z - g.z_lo] = (float)v[k];
+            if (xin && (z == g.z_lo - 1 || z == g.z_hi + 1))
+              st[2 * g.Lz + (z == g.z_lo - 1 ? 0 : g.Lx) + x - g.x_lo] = (float)v[k];
+          }
         }
       }
     }
     um = uc;
     uc = up;
-    elc = el_up;
-    erc = er_up;
+    elc = edn.x;
+    erc = edn.y;
   }
+  cp_wait<0>();
 }
 
 }  // namespace dufwi
@@ -185,252 +241,12 @@ __global__ void __launch_bounds__(kVecWarps * 32)
 namespace dufwi {
 
 // ---------------------------------------------------------------------------
-// Vectorised adjoint step (constant density, nz % 4 == 0).  A warp owns a
-// 128-wide z strip × TX rows of one phantom and walks the shots of its group
-// one after another; per shot it streams the rows of lam[t+1] (with E/dx^2
-// for the transposed operator) and of u[t-1] (buffer; ring cells from the
-// strips, MODE 2 — or the full history, MODE 1), writes lam[t] in place over
-// lam[t+2] and reconstructs u[t-2] in place over u[t] on the undamped box.
-// The imaging sum of all the group's shots is kept in a per-warp shared tile
-// and added to acc_part[group] once per step (deterministic shot order).
+// Vectorised adjoint (constant density, nz % 4 == 0), split in two kernels per
+// step: adjlam_vec (lam[t]) then img_vec (imaging + u[t-2] reconstruction).
+// A warp owns a 128-wide z strip x kVecAdjTX rows.
 constexpr int kVecAdjWarps = 4;
 constexpr int kVecAdjTX = 8;
 
-template <int MODE>
-__global__ void __launch_bounds__(kVecAdjWarps * 32)
-    adj_vec_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int U, int gs,
-                   const float* __restrict__ l1, float* l2o, const float* __restrict__ F,
-                   float* ut, const float* __restrict__ utm1,
-                   const float* __restrict__ strip_tm1, const double* __restrict__ rres_t,
-                   double* __restrict__ acc_part, int has1, int has2, int do_img, int do_recon) {
-  __shared__ double acc_s[kVecAdjWarps][kVecAdjTX][128];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nz = g.nz, nx = g.nx;
-  const int z0 = blockIdx.x * 128;
-  const int z4 = z0 + 4 * lane;
-  const bool act = z4 < nz;
-  const int x0 = (blockIdx.y * kVecAdjWarps + warp) * kVecAdjTX;
-  if (x0 >= nx) return;
-  const int x1 = min(nx, x0 + kVecAdjTX);
-  const ShotGroup sg = shot_group(g, blockIdx.z, unit_begin, U, gs);
-  if (sg.n == 0) return;
-  const size_t N2 = (size_t)nx * nz;
-  const double* Ed = m.Ed + (size_t)sg.b * N2;
-  const double pulse_t = __ldg(g.pulse + t);
-  bool lane_damped = false;
-  if (T.px && act) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) lane_damped |= __ldg(T.pz + min(z4 + k, nz - 1)) != 0.0;
-  }
-  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
-  double(&acc)[kVecAdjTX][128] = acc_s[warp];
-#pragma unroll
-  for (int r = 0; r < kVecAdjTX; ++r)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc[r][4 * lane + k] = 0.0;
-
-  // per-lane ring-column flags (MODE 2): the strip replaces the buffer there
-  int ringk[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int z = z4 + k;
-    ringk[k] = (z == g.z_lo - 1) ? 2 * g.Lz : (z == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;
-  }
-
-  auto ld4 = [&](const float* p, int x) -> Row4 {
-    Row4 r;
-    const float4 f = (act && x >= 0 && x < nx) ? __ldg(reinterpret_cast<const float4*>(p + (size_t)x * nz + z4))
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-    r = to_d(f);
-    return r;
-  };
-  auto ld_ed = [&](int x) -> Row4 {
-    Row4 r;
-    if (act && x >= 0 && x < nx) {
-      const double2 a = __ldg(reinterpret_cast<const double2*>(Ed + (size_t)x * nz + z4));
-      const double2 b = __ldg(reinterpret_cast<const double2*>(Ed + (size_t)x * nz + z4 + 2));
-      r.v[0] = a.x; r.v[1] = a.y; r.v[2] = b.x; r.v[3] = b.y;
-    } else {
-      r.v[0] = r.v[1] = r.v[2] = r.v[3] = 0.0;
-    }
-    return r;
-  };
-  auto edge = [&](const float* p, int x, bool right) -> double {
-    if (x < 0 || x >= nx) return 0.0;
-    if (right) return edge_r ? (double)__ldg(p + (size_t)x * nz + z0 + 128) : 0.0;
-    return edge_l ? (double)__ldg(p + (size_t)x * nz + z0 - 1) : 0.0;
-  };
-  auto edge_ed = [&](int x, bool right) -> double {
-    if (x < 0 || x >= nx) return 0.0;
-    if (right) return edge_r ? __ldg(Ed + (size_t)x * nz + z0 + 128) : 0.0;
-    return edge_l ? __ldg(Ed + (size_t)x * nz + z0 - 1) : 0.0;
-  };
-  // u[t-1] as the reconstruction sees it (MODE 2): buffer on the box, strips on the ring
-  auto ld_u = [&](const float* ub, const float* st, int x, double& el, double& er) -> Row4 {
-    Row4 r;
-    r.v[0] = r.v[1] = r.v[2] = r.v[3] = 0.0;
-    el = er = 0.0;
-    if (x < 0 || x >= nx) return r;
-    if (MODE == 1) {
-      r = ld4(ub, x);
-      el = edge(ub, x, false);
-      er = edge(ub, x, true);
-      return r;
-    }
-    const bool xbox = x >= g.x_lo && x <= g.x_hi;
-    const bool xring = x == g.x_lo - 1 || x == g.x_hi + 1;
-    if (xbox) {
-      r = ld4(ub, x);
-      el = edge(ub, x, false);
-      er = edge(ub, x, true);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int z = z4 + k;
-        if (ringk[k] >= 0) r.v[k] = (double)__ldg(st + ringk[k] + x - g.x_lo);
-        else if (z < g.z_lo || z > g.z_hi) r.v[k] = 0.0;
-      }
-      // strip edges: the neighbouring strip's outer cell may be a ring column
-      if (edge_l) {
-        const int z = z0 - 1;
-        el = (z == g.z_lo - 1) ? (double)__ldg(st + 2 * g.Lz + x - g.x_lo)
-                               : (z >= g.z_lo && z <= g.z_hi ? el : 0.0);
-      }
-      if (edge_r) {
-        const int z = z0 + 128;
-        er = (z == g.z_hi + 1) ? (double)__ldg(st + 2 * g.Lz + g.Lx + x - g.x_lo)
-                               : (z >= g.z_lo && z <= g.z_hi ? er : 0.0);
-      }
-    } else if (xring) {
-      const float* sr = st + (x == g.x_lo - 1 ? 0 : g.Lz);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int z = z4 + k;
-        r.v[k] = (act && z >= g.z_lo && z <= g.z_hi) ? (double)__ldg(sr + z - g.z_lo) : 0.0;
-      }
-      if (edge_l && z0 - 1 >= g.z_lo && z0 - 1 <= g.z_hi) el = (double)__ldg(sr + z0 - 1 - g.z_lo);
-      if (edge_r && z0 + 128 >= g.z_lo && z0 + 128 <= g.z_hi) er = (double)__ldg(sr + z0 + 128 - g.z_lo);
-    }
-    return r;
-  };
-
-  for (int k0 = 0; k0 < sg.n; ++k0) {
-    const int lu = sg.lu0 + k0;
-    const size_t fo = (size_t)lu * N2;
-    const int s = (unit_begin + lu) % g.S;
-    const int txx = __ldg(g.tx + 2 * s), txz = __ldg(g.tx + 2 * s + 1);
-    const int tk = (txz >= z4 && txz < z4 + 4) ? txz - z4 : -1;
-    const float* L1 = l1 + fo;
-    const float* st = MODE == 2 ? strip_tm1 + (size_t)lu * g.SL : nullptr;
-    const float* UB = MODE == 1 ? F + fo : utm1 + fo;
-    // rolling rows: E*lam1 (em, ec, ep) + raw lam1 centre, u[t-1] (fm, fc, fp)
-    Row4 edm = ld_ed(x0 - 1), edc = ld_ed(x0);
-    Row4 lm = has1 ? ld4(L1, x0 - 1) : Row4{}, lc = has1 ? ld4(L1, x0) : Row4{};
-    double elc_l = has1 ? edge(L1, x0, false) * edge_ed(x0, false) : 0.0;
-    double elc_r = has1 ? edge(L1, x0, true) * edge_ed(x0, true) : 0.0;
-    Row4 em, ec;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) { em.v[k] = edm.v[k] * lm.v[k]; ec.v[k] = edc.v[k] * lc.v[k]; }
-    double fcl = 0.0, fcr = 0.0, tmp_l, tmp_r;
-    Row4 fm{}, fc{};
-    if (do_img) {
-      fm = ld_u(UB, st, x0 - 1, tmp_l, tmp_r);
-      fc = ld_u(UB, st, x0, fcl, fcr);
-    }
-    for (int x = x0; x < x1; ++x) {
-      const size_t row = (size_t)x * nz;
-      // next rows
-      const Row4 edp = ld_ed(x + 1);
-      const Row4 lp = has1 ? ld4(L1, x + 1) : Row4{};
-      const double elp_l = has1 ? edge(L1, x + 1, false) * edge_ed(x + 1, false) : 0.0;
-      const double elp_r = has1 ? edge(L1, x + 1, true) * edge_ed(x + 1, true) : 0.0;
-      Row4 ep;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) ep.v[k] = edp.v[k] * lp.v[k];
-      double fpl = 0.0, fpr = 0.0;
-      Row4 fp{};
-      if (do_img) fp = ld_u(UB, st, x + 1, fpl, fpr);
-      const float4 l2f = (has2 && act) ? *reinterpret_cast<const float4*>(l2o + fo + row + z4)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-      const Row4 l2v = to_d(l2f);
-      double A[4], B[4];
-      ab4(T, x, z4, nz, lane_damped, A, B);
-      // z-neighbours
-      double ezl = __shfl_up_sync(0xffffffffu, ec.v[3], 1);
-      double ezr = __shfl_down_sync(0xffffffffu, ec.v[0], 1);
-      if (lane == 0) ezl = elc_l;
-      if (lane == 31) ezr = elc_r;
-      double fzl = __shfl_up_sync(0xffffffffu, fc.v[3], 1);
-      double fzr = __shfl_down_sync(0xffffffffu, fc.v[0], 1);
-      if (lane == 0) fzl = fcl;
-      if (lane == 31) fzr = fcr;
-      double lam[4], lapu[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double zm = k == 0 ? ezl : ec.v[k - 1];
-        const double zp = k == 3 ? ezr : ec.v[k + 1];
-        const double adj = (((-4.0 * ec.v[k] + em.v[k]) + ep.v[k]) + zm) + zp;
-        lam[k] = (A[k] * lc.v[k] + adj) + B[k] * l2v.v[k];
-        const double fzm = k == 0 ? fzl : fc.v[k - 1];
-        const double fzp = k == 3 ? fzr : fc.v[k + 1];
-        lapu[k] = (((-4.0 * fc.v[k] + fm.v[k]) + fp.v[k]) + fzm) + fzp;
-      }
-      if (act) {
-        if (__ldg(g.row_flag + x)) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int slot = __ldg(g.node_slot + row + z4 + k);
-            if (slot >= 0) lam[k] += __ldg(rres_t + (size_t)lu * g.M + slot);
-          }
-        }
-        *reinterpret_cast<float4*>(l2o + fo + row + z4) =
-            make_float4((float)lam[0], (float)lam[1], (float)lam[2], (float)lam[3]);
-        if (do_img) {
-          const bool xbox = MODE == 1 || (x >= g.x_lo && x <= g.x_hi);
-          double* ar = acc[x - x0];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int z = z4 + k;
-            const bool in = MODE == 1 || (xbox && z >= g.z_lo && z <= g.z_hi);
-            if (in) ar[4 * lane + k] += lapu[k] * lam[k];
-          }
-          if (MODE == 2 && do_recon && xbox) {
-            const float4 uf = *reinterpret_cast<const float4*>(ut + fo + row + z4);
-            const Row4 uv = to_d(uf);
-            float o[4] = {uf.x, uf.y, uf.z, uf.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int z = z4 + k;
-              if (z >= g.z_lo && z <= g.z_hi) {
-                double prev = 2.0 * fc.v[k] + edc.v[k] * lapu[k] - uv.v[k];
-                if (x == txx && k == tk) prev += pulse_t;
-                o[k] = (float)prev;
-              }
-            }
-            *reinterpret_cast<float4*>(ut + fo + row + z4) = make_float4(o[0], o[1], o[2], o[3]);
-          }
-        }
-      }
-      // roll
-      edm = edc; edc = edp;
-      lm = lc; lc = lp;
-      em = ec; ec = ep;
-      elc_l = elp_l; elc_r = elp_r;
-      fm = fc; fc = fp;
-      fcl = fpl; fcr = fpr;
-    }
-  }
-  if (do_img && act) {
-    double* dst = acc_part + (size_t)blockIdx.z * N2;
-    for (int x = x0; x < x1; ++x)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) dst[(size_t)x * nz + z4 + k] += acc[x - x0][4 * lane + k];
-  }
-}
-
-}  // namespace dufwi
-
-namespace dufwi {
 
 // ---------------------------------------------------------------------------
 // Split vectorised adjoint (constant density, nz % 4 == 0), kernel 1 of 2:
@@ -575,7 +391,9 @@ __global__ void __launch_bounds__(kVecAdjWarps * 32)
   for (int k = 0; k < 4; ++k) {
     const int z = z4 + k;
     if (MODE == 1 || (act && z >= g.z_lo && z <= g.z_hi)) inbox |= 1u << k;
-    ringk[k] = (MODE == 2 && z == g.z_lo - 1) ? 2 * g.Lz : (MODE == 2 && z == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;
+    // ring columns inside the grid only (no PML: the ring lies outside, = 0)
+    ringk[k] = (MODE == 2 && act && z == g.z_lo - 1) ? 2 * g.Lz
+             : (MODE == 2 && act && z == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;
   }
   const int ring_l = (MODE == 2 && z0 - 1 == g.z_lo - 1) ? 2 * g.Lz : -1;
   const int ring_r = (MODE == 2 && z0 + 128 == g.z_hi + 1) ? 2 * g.Lz + g.Lx : -1;

@@ -62,6 +62,22 @@ def test_gradcheck16_no_pml_matches_reference_and_fd(gpu):
         assert rel.max() < 1e-3
 
 
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("store", STORES)
+def test_gradcheck16_poisoned_workspace(gpu, engine, store):
+    """No PML puts the strip ring outside the grid; no kernel may read the
+    (never written) ring slots — NaN-filled recycled memory must not leak in."""
+    z, grid, geom, pulse = gradcheck16()
+    fwd._ENGINE_CACHE.clear()
+    torch.cuda.synchronize()
+    junk = torch.full((1 << 26,), float("nan"), device=gpu)
+    del junk
+    eng = _engine(grid, geom, pulse, pk.zero_damping(grid), engine)
+    eng.set_model(z["c0"][None])
+    _, g = eng.misfit_and_gradient(torch.as_tensor(z["obs"]).to(gpu), store=store)
+    assert rel_l2(g[0].cpu().numpy(), z["grad"]) <= GRAD_TOL
+
+
 def test_public_api_ring48(gpu):
     z, grid, geom, pulse, damp = ring48()
     obs = pk.simulate_all(pk.SosMap(grid, z["c_true"]), geom, pulse, damp)
