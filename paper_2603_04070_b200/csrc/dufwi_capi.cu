@@ -61,7 +61,8 @@ struct dufwi_plan {
   std::vector<void*> owned;
   ABTables ab{};  // (A, B) tables of the damped update for the stepwise kernels
   // cluster engine
-  ClusterCfg ccfg{};
+  std::vector<ClusterCfg> ccands;  // launch shapes that fit, one per cluster size
+  ClusterCfg ccfg{};                // the shape for all units at once (plan_info)
   bool cluster_ok = false;
 };
 
@@ -347,7 +348,8 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.tx = p->tx;
   g.node_slot = p->node_slot;
   g.row_flag = p->row_flag;
-  p->cluster_ok = cluster_config(g, p->has_rho != 0, &p->ccfg);
+  p->cluster_ok = cluster_candidates(g, p->has_rho != 0, p->ccands);
+  if (p->cluster_ok) p->ccfg = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots);
   *plan_out = p;
   return DUFWI_OK;
 }
@@ -433,7 +435,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
 
   if (use_cluster(p)) {
     p->last_engine = DUFWI_ENGINE_CLUSTER;
-    rc = cluster_forward(g, m, p->ccfg, p->has_rho != 0, mode, unit_begin, U, rec,
+    rc = cluster_forward(g, m, pick_cluster(p->ccands, U), mode, unit_begin, U, rec,
                          mode == DUFWI_STORE_FULL ? hist : nullptr,
                          mode == DUFWI_STORE_STRIPS ? strips : nullptr, ubuf, st);
     if (rc) return fail(DUFWI_ECUDA, std::string("cluster forward: ") + cudaGetErrorString((cudaError_t)rc));
@@ -549,7 +551,7 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     p->last_engine = DUFWI_ENGINE_CLUSTER;
     // per-unit accumulators: with one shot per group, group index == chunk-local unit
     const int acc_off = 0;
-    rc = cluster_adjoint(g, m, p->ccfg, p->has_rho != 0, mode, unit_begin, U, rres,
+    rc = cluster_adjoint(g, m, pick_cluster(p->ccands, U), mode, unit_begin, U, rres,
                          mode == DUFWI_STORE_FULL ? hist : nullptr,
                          mode == DUFWI_STORE_STRIPS ? strips : nullptr, ubuf, acc_part, acc_off,
                          st);
@@ -634,10 +636,10 @@ extern "C" int64_t dufwi_plan_launch_count(const dufwi_plan_t* p) { return p ? p
 extern "C" int32_t dufwi_plan_last_engine(const dufwi_plan_t* p) { return p ? p->last_engine : -1; }
 extern "C" int32_t dufwi_plan_info(const dufwi_plan_t* p, int64_t* out, int32_t n) {
   if (!p || !out) return 0;
-  const int64_t v[8] = {p->cluster_ok ? 1 : 0, p->ccfg.cs, p->ccfg.rows, p->ccfg.rpt,
+  const int64_t v[9] = {p->cluster_ok ? 1 : 0, p->ccfg.cs, p->ccfg.rows, p->ccfg.rpt,
                         p->ccfg.threads, p->ccfg.dbl, (int64_t)p->ccfg.smem_fwd,
-                        (int64_t)p->ccfg.smem_adj};
-  const int k = n < 8 ? n : 8;
+                        (int64_t)p->ccfg.smem_adj, p->ccfg.maxc};
+  const int k = n < 9 ? n : 9;
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }

@@ -7,12 +7,15 @@
 // [seg*RPT, seg*RPT+RPT): its cells' state (u[t-1], u[t-2] forward; lam[t+1],
 // lam[t+2], u[t], u[t-1] adjoint), E/dx^2 and the imaging accumulators live in
 // f64 REGISTERS for the whole sweep.  Per time step a thread
-//   * reads z-neighbours from a double-buffered shared-memory exchange row,
-//   * takes x-neighbours from its own registers, from the exchange rows of the
+//   * reads z-neighbours from a double-buffered shared-memory exchange buffer,
+//   * takes x-neighbours from its own registers, from the exchange cells of the
 //     adjacent segment, or from the halo rows of the buffer,
-//   * writes its new value into the exchange buffer; threads owning the slab's
+//   * writes its new values into the exchange buffer; threads owning the slab's
 //     first/last row also push it into the neighbouring CTA's halo row with
 //     st.async (DSMEM), completing bytes on that CTA's mbarrier.
+// Columns are permuted so that the few holding damped, receiver, ring or
+// source cells share warps; every other warp runs a branch-free fast step
+// (A = 2, B = -1, no IO), chosen once per sweep and uniform per warp.
 // A step then costs one __syncthreads and one mbarrier phase wait — no
 // cluster-wide barrier, no GPU-scope fence, no L1 invalidation.  HBM only sees
 // receiver samples, the 1-cell ring strips and the final two states.
@@ -24,6 +27,10 @@
 #pragma once
 
 #include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
 
 #include "dufwi_common.cuh"
 
@@ -43,6 +50,7 @@ struct ClusterCfg {
   int dbl = 0;      // exchange rows in f64 (1) or f32 (0)
   int maxrec = 0;   // receiver cells per CTA (upper bound) staged in shared memory
   int maxring = 0;  // ring-strip cells per CTA (upper bound) staged in shared memory
+  int maxc = 0;     // clusters co-resident on the device (one wave)
   size_t smem_fwd = 0, smem_adj = 0;
 };
 
@@ -105,45 +113,32 @@ __device__ __forceinline__ void push_if(uint32_t on, uint32_t raddr, float v, ui
       "r"(__float_as_uint(v)), "r"(rbar), "r"(on)
       : "memory");
 }
-__device__ __forceinline__ void named_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-// One thread moves a whole exchange row into a neighbour CTA's halo row and
-// completes the bytes on that CTA's mbarrier (async proxy).
-__device__ __forceinline__ void push_row(uint32_t dst_cluster, const void* src, uint32_t bytes,
-                                         uint32_t bar_cluster) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          dst_cluster),
-      "r"(smem_addr(src)), "r"(bytes), "r"(bar_cluster)
-      : "memory");
-}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 // ------------------------------------------------------------ smem layout
-// [nbufs exchange buffers of (rows+2) x (nz+2) T] [rows x nz double2 (A, B)] [2 mbarriers]
-// Exchange row stride: nz + 2 pad columns, rounded so every row starts on a
-// 16-byte boundary (bulk DSMEM copies move whole rows).
-template <class T>
-__host__ __device__ inline int xstride(int nz) {
-  const int q = 16 / (int)sizeof(T);
-  return (nz + 2 + q - 1) / q * q;
+// [nbufs exchange buffers] [rows x nz double2 (A, B)] [2 mbarriers] [IO stage]
+// An exchange buffer is column-major: cell (buffer row r, column z) at
+// (z + 1) * RS + r, r = local row + 1 (r = 0 / rows + 1: halo rows from the
+// neighbouring CTAs), z = -1 / nz: zero pad columns.  RS >= nseg * RPT + 2 is
+// odd, so 32 lanes on consecutive columns hit 32 distinct 8-byte bank pairs,
+// and a thread's own rows sit at compile-time offsets from one base address.
+__host__ __device__ inline int xcol_stride(int rows, int rpt) {
+  const int nseg = (rows + rpt - 1) / rpt;
+  return (nseg * rpt + 2) | 1;
+}
+__host__ __device__ inline size_t xbuf_elems(int rows, int rpt, int nz) {
+  return (size_t)(nz + 2) * xcol_stride(rows, rpt);
 }
 template <class T>
-__host__ __device__ inline size_t xbuf_elems(int rows, int nz) {
-  return (size_t)(rows + 2) * xstride<T>(nz);
+__host__ __device__ inline size_t ab_offset(int rows, int rpt, int nz, int nbufs) {
+  return ((size_t)nbufs * xbuf_elems(rows, rpt, nz) * sizeof(T) + 15) & ~(size_t)15;
 }
 template <class T>
-__host__ __device__ inline size_t ab_offset(int rows, int nz, int nbufs) {
-  return ((size_t)nbufs * xbuf_elems<T>(rows, nz) * sizeof(T) + 15) & ~(size_t)15;
-}
-template <class T>
-__host__ __device__ inline size_t bar_offset(int rows, int nz, int nbufs) {
-  return ab_offset<T>(rows, nz, nbufs) + (size_t)rows * nz * sizeof(double2);
+__host__ __device__ inline size_t bar_offset(int rows, int rpt, int nz, int nbufs) {
+  return ab_offset<T>(rows, rpt, nz, nbufs) + (size_t)rows * nz * sizeof(double2);
 }
 // IO stage after the mbarriers: [n_rec, n_ring, pad] [rec_g[maxrec]] [ring_g[maxring]]
 // [double stage_rec[kStage][maxrec]] [float stage_ring[kStage][maxring]]
@@ -159,8 +154,8 @@ struct IoStage {
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
 
 template <class T>
-__host__ __device__ inline size_t io_offset(int rows, int nz, int nbufs) {
-  return al16(bar_offset<T>(rows, nz, nbufs) + 2 * sizeof(uint64_t));
+__host__ __device__ inline size_t io_offset(int rows, int rpt, int nz, int nbufs) {
+  return al16(bar_offset<T>(rows, rpt, nz, nbufs) + 2 * sizeof(uint64_t));
 }
 
 __host__ __device__ inline size_t io_bytes(int maxrec, int maxring) {
@@ -169,9 +164,9 @@ __host__ __device__ inline size_t io_bytes(int maxrec, int maxring) {
 }
 
 template <class T>
-__host__ __device__ inline size_t cluster_smem_bytes(int rows, int nz, int nbufs, int maxrec,
-                                                     int maxring) {
-  return io_offset<T>(rows, nz, nbufs) + io_bytes(maxrec, maxring);
+__host__ __device__ inline size_t cluster_smem_bytes(int rows, int rpt, int nz, int nbufs,
+                                                     int maxrec, int maxring) {
+  return io_offset<T>(rows, rpt, nz, nbufs) + io_bytes(maxrec, maxring);
 }
 
 __device__ __forceinline__ IoStage io_stage(unsigned char* base, int maxrec, int maxring) {
@@ -190,16 +185,46 @@ __device__ __forceinline__ IoStage io_stage(unsigned char* base, int maxrec, int
   return io;
 }
 
-// Per-thread static description of its cells.
+// ------------------------------------------------------------ f64 arithmetic
+// Explicit roundings, shared by the fast and the generic step so both produce
+// the same bits: the reference's 5-point sum (((-4c + xm) + xp) + zm) + zp and
+// the update A u1 + B u2 + E lap (forward.py:301-308).
+__device__ __forceinline__ double lap5(double c, double xm, double xp, double zm, double zp) {
+  return __dadd_rn(__dadd_rn(__dadd_rn(__fma_rn(-4.0, c, xm), xp), zm), zp);
+}
+__device__ __forceinline__ double fwd_update(double A, double B, double u1, double u2, double e,
+                                             double lap) {
+  return __fma_rn(e, lap, __fma_rn(A, u1, __dmul_rn(B, u2)));
+}
+// (A, B) = (2, -1): B u2 = -u2 exactly, so this equals fwd_update bit for bit.
+__device__ __forceinline__ double fwd_update_free(double u1, double u2, double e, double lap) {
+  return __fma_rn(e, lap, __fma_rn(2.0, u1, -u2));
+}
+// lam = (A lam1 + L^T(E lam1)) + B lam2 (adjoint.py:119-131)
+__device__ __forceinline__ double adj_update(double A, double B, double l1, double l2,
+                                             double adj) {
+  return __fma_rn(B, l2, __fma_rn(A, l1, adj));
+}
+__device__ __forceinline__ double adj_update_free(double l1, double l2, double adj) {
+  return __dadd_rn(__fma_rn(2.0, l1, adj), -l2);
+}
+// u[t-2] = 2 u[t-1] + E L u[t-1] - u[t] (+ source), the forward step solved backwards
+__device__ __forceinline__ double recon(double ub, double ua, double e, double lapu) {
+  return __dadd_rn(__fma_rn(e, lapu, 2.0 * ub), -ua);
+}
+
+// ------------------------------------------------------------ per-thread state
 struct CellCtx {
   int rank, cs, rows, nr, r0;  // slab of this CTA: global rows [r0, r0+nr)
-  int seg, z, lrow0;           // thread: column z, local rows lrow0 .. lrow0+RPT-1
-  int W;                       // exchange row stride (>= nz + 2, 16-byte rows)
-  int seg_last;                // segment owning the slab's last row
+  int seg, zi, z, lrow0;       // thread: column z (= order[zi]), local rows lrow0 ..
+  int RS;                      // exchange column stride
+  int xo;                      // buffer offset of the thread's first cell
   bool has_up, has_dn;         // CTA rank-1 / rank+1 exist with rows
+  uint32_t lbase, rup, rdn;    // shared-window base: own, rank-1, rank+1
 };
 
-__device__ __forceinline__ CellCtx make_ctx(int cs, int rows, int nx, int nz, int rpt, int W) {
+__device__ __forceinline__ CellCtx make_ctx(int cs, int rows, int nx, int nz, int rpt,
+                                            const void* smem) {
   CellCtx c;
   c.rank = (int)cg::this_cluster().block_rank();
   c.cs = cs;
@@ -207,12 +232,16 @@ __device__ __forceinline__ CellCtx make_ctx(int cs, int rows, int nx, int nz, in
   c.r0 = c.rank * rows;
   c.nr = max(0, min(nx, c.r0 + rows) - c.r0);
   c.seg = threadIdx.x / nz;
-  c.z = threadIdx.x - c.seg * nz;
+  c.zi = threadIdx.x - c.seg * nz;
+  c.z = c.zi;
   c.lrow0 = c.seg * rpt;
-  c.W = W;
-  c.seg_last = c.nr > 0 ? (c.nr - 1) / rpt : 0;
+  c.RS = xcol_stride(rows, rpt);
+  c.xo = 0;
   c.has_up = c.rank > 0 && c.nr > 0;
   c.has_dn = c.nr > 0 && c.rank + 1 < cs && (c.rank + 1) * rows < nx;
+  c.lbase = smem_addr(smem);
+  c.rup = c.has_up ? mapa_rank(c.lbase, c.rank - 1) : 0u;
+  c.rdn = c.has_dn ? mapa_rank(c.lbase, c.rank + 1) : 0u;
   return c;
 }
 
@@ -233,6 +262,39 @@ __device__ __forceinline__ bool in_box(const Geo& g, int x, int z) {
   return x >= g.x_lo && x <= g.x_hi && z >= g.z_lo && z <= g.z_hi;
 }
 
+// Column order of the slab: columns holding any damped, receiver, ring or
+// source cell first, plain columns after, so whole warps of plain columns run
+// the fast step.  Sets c.z / c.xo.  scratch: 2 * nz ints of shared memory
+// (the exchange buffers, before they are zeroed).
+__device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx, int txz,
+                                              int* scratch) {
+  const int nz = g.nz;
+  int* plain = scratch;
+  int* order = scratch + nz;
+  for (int z = threadIdx.x; z < nz; z += blockDim.x) {
+    int p = 1;
+    for (int lr = 0; lr < c.nr && p; ++lr) {
+      const int x = c.r0 + lr;
+      if (damping_at(g, x, z) != 0.0 || !in_box(g, x, z) || (x == txx && z == txz) ||
+          (g.row_flag[x] && g.node_slot[(size_t)x * nz + z] >= 0) || ring_index(g, x, z) >= 0)
+        p = 0;
+    }
+    plain[z] = p;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int z = 0; z < nz; ++z)
+      if (!plain[z]) order[k++] = z;
+    for (int z = 0; z < nz; ++z)
+      if (plain[z]) order[k++] = z;
+  }
+  __syncthreads();
+  c.z = order[c.zi];
+  c.xo = (c.z + 1) * c.RS + c.lrow0 + 1;
+  __syncthreads();  // scratch is reused as exchange buffer afterwards
+}
+
 // Static per-cell data loaded once per sweep.
 template <int RPT>
 struct CellStatic {
@@ -242,15 +304,17 @@ struct CellStatic {
   unsigned active, src, interior;
   bool pushes_up, pushes_dn;  // owns the slab's first / last row
   unsigned dn_mask;           // bit j set: register j holds the slab's last row (pushes_dn)
-  bool special;               // any receiver / ring / source / push / history cell
+  bool special;               // any receiver / ring / source cell
   bool undamped;              // every cell has D == 0: (A, B) = (2, -1), no table reads
+  bool fast;                  // whole warp: all rows active, undamped, interior, not special
   const double2* ab;          // shared (A, B) table, row stride nz
 };
 
 template <int RPT>
 __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const CellCtx& c,
                                             size_t pb, int txx, int txz, double2* ab_table,
-                                            const IoStage& io, CellStatic<RPT>& st) {
+                                            const IoStage& io, bool allow_fast,
+                                            CellStatic<RPT>& st) {
   st.active = st.src = st.interior = 0u;
   st.ab = ab_table;
   st.pushes_up = c.has_up && c.lrow0 == 0;
@@ -295,142 +359,122 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
 #pragma unroll
   for (int j = 0; j < RPT; ++j) any = any || st.rl[j] >= 0 || st.gl[j] >= 0;
   st.special = any;
+  const unsigned full = (1u << RPT) - 1u;
+  const bool f = allow_fast && st.active == full && st.interior == full && st.undamped && !any;
+  st.fast = __all_sync(__activemask(), f);  // warp-uniform path choice
 }
 
-// x-neighbours of cell j of a thread column: register when the neighbour is the
-// thread's own cell, else the exchange buffer row (adjacent segment or halo).
-// Row index in the buffer is lr + 1 (row 0 = top halo).
-template <int RPT, class T>
-__device__ __forceinline__ void x_neighbours(const CellCtx& c, const double (&v)[RPT],
-                                             const T* X, double (&xm)[RPT], double (&xp)[RPT]) {
-  const int W = c.W, z = c.z;
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    const int lr = min(c.lrow0 + j, c.rows - 1);
-    xm[j] = j > 0 ? v[j - 1] : (double)X[(size_t)lr * W + z + 1];
-    const bool own_next = j < RPT - 1 && c.lrow0 + j + 1 < c.nr;
-    xp[j] = own_next ? v[j + 1] : (double)X[(size_t)(lr + 2) * W + z + 1];
-  }
-}
-
-// Bulk halo exchange: the threads owning the slab's first (last) row sync on a
-// named barrier, then one of them copies the whole row into the halo row of
-// CTA rank-1 (rank+1).  Needs nz % 32 == 0 so a row's threads are whole warps.
+// Exchange-row pushes to the neighbouring CTAs (DSMEM st.async completing on
+// their mbarrier): the slab's first row -> bottom halo of rank-1, last row ->
+// top halo of rank+1.  A CTA's shared memory is one contiguous range of the
+// cluster window, so remote addresses are the mapped base plus the offset.
 template <class T>
-__device__ __forceinline__ void push_rows(const CellCtx& c, int nz, T* Xw, uint32_t bar_w) {
-  const uint32_t bytes = (uint32_t)(c.W * sizeof(T));
-  if (c.has_up && c.seg == 0) {
-    named_sync(1, nz);
-    if (threadIdx.x == 0)
-      push_row(mapa_rank(smem_addr(Xw + (size_t)(c.rows + 1) * c.W), c.rank - 1), Xw + (size_t)c.W,
-               bytes, mapa_rank(bar_w, c.rank - 1));
-  }
-  if (c.has_dn && c.seg == c.seg_last) {
-    named_sync(2, nz);
-    if (threadIdx.x == c.seg_last * nz)
-      push_row(mapa_rank(smem_addr(Xw), c.rank + 1), Xw + (size_t)c.nr * c.W, bytes,
-               mapa_rank(bar_w, c.rank + 1));
-  }
+__device__ __forceinline__ uint32_t remote(const CellCtx& c, uint32_t rbase, const T* local) {
+  return rbase + (smem_addr(local) - c.lbase);
 }
 
-// ---------------------------------------------------------------------------
-// forward step i (time t = i).  u1 = u[t-1] (read), u2 = u[t-2] -> u[t].
-// Reads exchange buffer Xr (step i-1), writes Xw (step i) and pushes the slab's
-// boundary rows into the neighbours' Xw halo rows (mbarrier `bar_w` remote).
-template <int RPT, class T, int MODE>
-__device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
-                                         double (&u1)[RPT], double (&u2)[RPT], int t, int U,
-                                         int lu, const T* Xr, T* Xw, uint32_t bar_r,
-                                         uint32_t bar_w, uint32_t tx_bytes, double pulse_t,
-                                         const IoStage& io, float* __restrict__ hist, size_t N2,
-                                         bool bulk) {
-  const int W = c.W, z = c.z;
-#ifdef DUFWI_EXP_TIMING
-  const bool tm = blockIdx.x == 5 && (threadIdx.x & 31) == 0;
-  long long T0 = clock64();
-#endif
-#ifndef DUFWI_EXP_NOSYNC
-  __syncthreads();  // exchange rows of step i-1 complete; Xw free for reuse
-#endif
-#ifdef DUFWI_EXP_TIMING
-  long long T1 = clock64();
-#endif
-#ifndef DUFWI_EXP_NOWAIT
-  if (t >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((t - 1) >> 1) & 1);
-#endif
-#ifdef DUFWI_EXP_TIMING
-  long long T2 = clock64();
-#endif
-  if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
-  double xm[RPT], xp[RPT], zm[RPT], zp[RPT], v[RPT];
-#ifdef DUFWI_EXP_NOLDS
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) { xm[j] = xp[j] = zm[j] = zp[j] = u1[j] * 0.25; }
-#else
-  x_neighbours<RPT, T>(c, u1, Xr, xm, xp);
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    const int lr = min(c.lrow0 + j, c.rows - 1);
-    zm[j] = (double)Xr[(size_t)(lr + 1) * W + z];
-    zp[j] = (double)Xr[(size_t)(lr + 1) * W + z + 2];
-  }
-#endif
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    const double lap = (((-4.0 * u1[j] + xm[j]) + xp[j]) + zm[j]) + zp[j];
-    const double2 ab = s.undamped ? make_double2(2.0, -1.0) : s.ab[(size_t)min(c.lrow0 + j, c.rows - 1) * g.nz + z];
-#ifdef DUFWI_EXP_NOCOMPUTE
-    v[j] = u1[j] + zm[j];
-#else
-    v[j] = ab.x * u1[j] + ab.y * u2[j] + s.ed[j] * lap;
-#endif
-    if (s.src & (1u << j)) v[j] += pulse_t;
-  }
-  // common path: state and exchange row (inactive rows only exist in the last segment)
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    if (!(s.active & (1u << j))) continue;
-    u2[j] = v[j];
-    Xw[(size_t)(c.lrow0 + j + 1) * W + z + 1] = (T)v[j];
-  }
-#ifdef DUFWI_EXP_TIMING
-  long long T3 = clock64();
-  if (tm) {
-    const int w = threadIdx.x >> 5;
-    atomicAdd(&g_dbg[w * 4 + 0], (unsigned long long)(T1 - T0));
-    atomicAdd(&g_dbg[w * 4 + 1], (unsigned long long)(T2 - T1));
-    atomicAdd(&g_dbg[w * 4 + 2], (unsigned long long)(T3 - T2));
-  }
-#endif
-  // halo rows to the neighbouring CTAs
-  if (bulk) {
-    push_rows<T>(c, g.nz, Xw, bar_w);
-  } else {
-    if (s.pushes_up)  // my first row -> bottom halo of rank-1
-      push_async(mapa_rank(smem_addr(Xw + (size_t)(c.rows + 1) * W + z + 1), c.rank - 1), (T)v[0],
-                 mapa_rank(bar_w, c.rank - 1));
-    if (s.pushes_dn) {  // my last row -> top halo of rank+1
-      const uint32_t ra = mapa_rank(smem_addr(Xw + z + 1), c.rank + 1);
-      const uint32_t rb = mapa_rank(bar_w, c.rank + 1);
+template <int RPT, class T>
+__device__ __forceinline__ void push_edges(const CellCtx& c, const CellStatic<RPT>& s, T* X,
+                                           const double (&v)[RPT], uint32_t bar_w, bool fast) {
+  const T* col = X + (c.z + 1) * c.RS;
+  if (s.pushes_up)
+    push_async(remote(c, c.rup, col + c.rows + 1), (T)v[0], c.rup + (bar_w - c.lbase));
+  if (s.pushes_dn) {
+    const uint32_t ra = remote(c, c.rdn, col);
+    const uint32_t rb = c.rdn + (bar_w - c.lbase);
+    if (fast) {
+      push_async(ra, (T)v[RPT - 1], rb);
+    } else {
       // explicit predicate per register so v[] is never indexed at run time
 #pragma unroll
       for (int j = 0; j < RPT; ++j) push_if((s.dn_mask >> j) & 1u, ra, (T)v[j], rb);
     }
   }
-  if (!s.special) return;
-  // rare path: receivers, history / ring strips
+}
+
+// ---------------------------------------------------------------------------
+// forward step t.  u1 = u[t-1] (read), u2 = u[t-2] -> u[t].  Reads exchange
+// buffer Xr (step t-1), writes Xw (step t).
+__device__ __forceinline__ void step_sync(const CellCtx& c, int i, uint32_t bar_r, uint32_t bar_w,
+                                          uint32_t tx_bytes) {
+  __syncthreads();  // exchange rows of step i-1 complete; Xw free for reuse
+  if (i >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((i - 1) >> 1) & 1);
+  if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
+}
+
+// Plain cells: undamped, no receiver / ring / source, every row active.
+template <int RPT, class T>
+__device__ __forceinline__ void fwd_fast(const CellCtx& c, const CellStatic<RPT>& s,
+                                         double (&u1)[RPT], double (&u2)[RPT], const T* Xr,
+                                         T* Xw, uint32_t bar_w) {
+  const T* pc = Xr + c.xo;
+  const T* pm = pc - c.RS;
+  const T* pp = pc + c.RS;
+  double v[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const double xm = j > 0 ? u1[j - 1] : (double)pc[-1];
+    const double xp = j + 1 < RPT ? u1[j + 1] : (double)pc[RPT];
+    const double lap = lap5(u1[j], xm, xp, (double)pm[j], (double)pp[j]);
+    v[j] = fwd_update_free(u1[j], u2[j], s.ed[j], lap);
+  }
+  T* q = Xw + c.xo;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    u2[j] = v[j];
+    q[j] = (T)v[j];
+  }
+  push_edges<RPT, T>(c, s, Xw, v, bar_w, true);
+}
+
+template <int RPT, class T, int MODE>
+__device__ __forceinline__ void fwd_generic(const Geo& g, const CellCtx& c,
+                                            const CellStatic<RPT>& s, double (&u1)[RPT],
+                                            double (&u2)[RPT], int t, int U, int lu, const T* Xr,
+                                            T* Xw, uint32_t bar_w, double pulse_t,
+                                            const IoStage& io, float* __restrict__ hist,
+                                            size_t N2) {
+  const T* pc = Xr + c.xo;
+  const T* pm = pc - c.RS;
+  const T* pp = pc + c.RS;
+  double v[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const double xm = j > 0 ? u1[j - 1] : (double)pc[-1];
+    const bool own_next = j + 1 < RPT && c.lrow0 + j + 1 < c.nr;
+    const double xp = own_next ? u1[j + 1] : (double)pc[j + 1];
+    const double lap = lap5(u1[j], xm, xp, (double)pm[j], (double)pp[j]);
+    if (s.undamped) {
+      v[j] = fwd_update_free(u1[j], u2[j], s.ed[j], lap);
+    } else {
+      const double2 ab = s.ab[(size_t)min(c.lrow0 + j, c.rows - 1) * g.nz + c.z];
+      v[j] = fwd_update(ab.x, ab.y, u1[j], u2[j], s.ed[j], lap);
+    }
+  }
+  if (s.src) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+      if (s.src & (1u << j)) v[j] = __dadd_rn(v[j], pulse_t);
+  }
+  T* q = Xw + c.xo;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    if (!(s.active & (1u << j))) continue;
+    u2[j] = v[j];
+    q[j] = (T)v[j];
+  }
+  push_edges<RPT, T>(c, s, Xw, v, bar_w, false);
+  if (!s.special && MODE != 1) return;
+  // receivers, history / ring strips
   const int k = t % kStage;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     if (!(s.active & (1u << j))) continue;
     const float vf = (float)v[j];
     if (s.rl[j] >= 0) io.srec[k * io.maxrec + s.rl[j]] = (double)vf;
-    if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + z] = vf;
+    if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = vf;
     if (MODE == 2 && s.gl[j] >= 0) io.sring[k * io.maxring + s.gl[j]] = vf;
   }
-#ifdef DUFWI_EXP_TIMING
-  if (tm) atomicAdd(&g_dbg[(threadIdx.x >> 5) * 4 + 3], (unsigned long long)(clock64() - T3));
-#endif
 }
 
 // Write the staged receiver samples / ring strips of steps [t0, t0+nk) to HBM.
@@ -453,24 +497,39 @@ __device__ __forceinline__ void flush_stage(const Geo& g, const IoStage& io, int
 }
 
 template <int RPT, class T, int MODE>
+__device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
+                                         double (&u1)[RPT], double (&u2)[RPT], int t, int U,
+                                         int lu, const T* Xr, T* Xw, uint32_t bar_r,
+                                         uint32_t bar_w, uint32_t tx_bytes, double pulse_t,
+                                         const IoStage& io, float* __restrict__ hist, size_t N2) {
+  step_sync(c, t, bar_r, bar_w, tx_bytes);
+  if (s.fast)
+    fwd_fast<RPT, T>(c, s, u1, u2, Xr, Xw, bar_w);
+  else
+    fwd_generic<RPT, T, MODE>(g, c, s, u1, u2, t, U, lu, Xr, Xw, bar_w, pulse_t, io, hist, N2);
+}
+
+template <int RPT, class T, int MODE>
 __global__ void __launch_bounds__(kClusterMaxThreads, 1)
     cluster_fwd_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
                        int unit_begin, int U, float* __restrict__ rec, float* __restrict__ hist,
                        float* __restrict__ strips, float* __restrict__ ubuf) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT, xstride<T>(g.nz));
+  CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT, smem);
   const int lu = blockIdx.x / cs;
   const int u = unit_begin + lu;
   const int b = u / g.S;
   const int s = u - b * g.S;
+  const int txx = g.tx[2 * s], txz = g.tx[2 * s + 1];
   const size_t N2 = (size_t)g.nx * g.nz;
   const size_t pb = (size_t)b * N2;
-  const size_t xe = xbuf_elems<T>(rows, g.nz);
+  const size_t xe = xbuf_elems(rows, RPT, g.nz);
   T* X[2] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem) + xe};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, g.nz, 2));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, RPT, g.nz, 2));
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
+  order_columns(g, c, txx, txz, reinterpret_cast<int*>(smem));
   for (size_t i = threadIdx.x; i < 2 * xe; i += blockDim.x) X[0][i] = T(0);
-  const IoStage io = io_stage(smem + io_offset<T>(rows, g.nz, 2), maxrec, maxring);
+  const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 2), maxrec, maxring);
   if (threadIdx.x == 0) {
     mbar_init(bar[0], 1);
     mbar_init(bar[1], 1);
@@ -479,12 +538,11 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
   }
   __syncthreads();
   CellStatic<RPT> st;
-  load_static<RPT>(g, m, c, pb, g.tx[2 * s], g.tx[2 * s + 1],
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 2)), io, st);
-  if (MODE == 1) st.special = true;  // every cell goes to the history
-  const bool bulk = false;  // measured slower than per-thread st.async (named-barrier + bulk-copy latency)
+  load_static<RPT>(g, m, c, pb, txx, txz,
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)), io,
+                   MODE != 1, st);
   const uint32_t tx_bytes =
-      (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * (bulk ? c.W : g.nz) * sizeof(T);
+      (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T);
   double ua[RPT], ub[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) ua[j] = ub[j] = 0.0;
@@ -493,25 +551,32 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
   cluster_sync_all();  // barriers initialised and buffers zeroed cluster-wide
 
   // step t writes X[t & 1] / bar[t & 1]; ub receives u[t] at even t, ua at odd t
+#ifdef DUFWI_EXP_TIMING
+  const long long TL0 = clock64();
+#endif
   int t = 0;
   for (; t + 1 < g.nt; t += 2) {
     double p = p_next;
     if (owns_src) p_next = g.pulse[t + 1];
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, X[1], X[0], bar[1], bar[0], tx_bytes, p,
-                           io, hist, N2, bulk);
+                           io, hist, N2);
     p = p_next;
     if (owns_src && t + 2 < g.nt) p_next = g.pulse[t + 2];
-    fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, X[0], X[1], bar[0], bar[1], tx_bytes, p,
-                           io, hist, N2, bulk);
+    fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, X[0], X[1], bar[0], bar[1], tx_bytes,
+                           p, io, hist, N2);
     if ((t + 2) % kStage == 0) flush_stage<MODE>(g, io, t + 2 - kStage, kStage, U, lu, rec, strips);
   }
   if (t < g.nt)
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, X[1], X[0], bar[1], bar[0], tx_bytes,
-                           p_next, io, hist, N2, bulk);
+                           p_next, io, hist, N2);
   if (g.nt % kStage) {
     const int t0 = g.nt - g.nt % kStage;
     flush_stage<MODE>(g, io, t0, g.nt - t0, U, lu, rec, strips);
   }
+#ifdef DUFWI_EXP_TIMING
+  if (blockIdx.x == 5 && (threadIdx.x & 31) == 0)
+    atomicAdd(&g_dbg[128 + (threadIdx.x >> 5)], (unsigned long long)(clock64() - TL0));
+#endif
   // drain the last step's incoming pushes before any CTA of the cluster exits
   if (c.has_up || c.has_dn) mbar_wait(bar[(g.nt - 1) & 1], ((g.nt - 1) >> 1) & 1);
   cluster_sync_all();
@@ -535,52 +600,94 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
 // adjoint step i (time t = nt-1-i).  l1 = lam[t+1], l2 = lam[t+2] -> lam[t];
 // ua = u[t] -> u[t-2] (reconstruction, MODE 2), ub = u[t-1].
 // XL: exchange of E*lam, XU: exchange of u (MODE 2).  Buffers/bars indexed by i.
-template <int RPT, class T, int MODE>
-__device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
+template <int RPT, class T>
+__device__ __forceinline__ void adj_fast(const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
-                                         double (&ub)[RPT], double (&acc)[RPT], int i, int U,
-                                         int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
-                                         uint32_t bar_r, uint32_t bar_w, uint32_t tx_bytes,
-                                         double pulse_t, const IoStage& io,
-                                         const float* __restrict__ hist, size_t N2, bool bulk) {
-  const int W = c.W, z = c.z;
-  const int t = g.nt - 1 - i;
-  __syncthreads();
-  // residuals / ring values of this step from the shared-memory stage
-  double rr[RPT];
-  float ring_v[RPT];
-  const int k = i % kStage;
+                                         double (&ub)[RPT], double (&acc)[RPT], int t,
+                                         const T* XLr, T* XLw, const T* XUr, T* XUw,
+                                         uint32_t bar_w) {
+  const int RS = c.RS;
+  // lam[t] = A lam1 + L^T(E lam1) + B lam2
+  double el[RPT], lam[RPT];
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    rr[j] = s.rl[j] >= 0 ? io.srec[k * io.maxrec + s.rl[j]] : 0.0;
-    ring_v[j] = (MODE == 2 && s.gl[j] >= 0) ? io.sring[k * io.maxring + s.gl[j]] : 0.f;
-  }
-  if (i >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((i - 1) >> 1) & 1);
-  if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
-
-  // lam[t] = A lam1 + L^T(E lam1) + B lam2 (+ residual), reference order
-  double el[RPT], xm[RPT], xp[RPT], lam[RPT];
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) el[j] = s.ed[j] * l1[j];
-  x_neighbours<RPT, T>(c, el, XLr, xm, xp);
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    const int lr = min(c.lrow0 + j, c.rows - 1);
-    const size_t o = (size_t)(lr + 1) * W + z + 1;
-    const double adj = (((-4.0 * el[j] + xm[j]) + xp[j]) + (double)XLr[o - 1]) + (double)XLr[o + 1];
-    const double2 ab = s.undamped ? make_double2(2.0, -1.0) : s.ab[(size_t)lr * g.nz + z];
-    lam[j] = ab.x * l1[j] + adj + ab.y * l2[j] + rr[j];
-  }
-  // imaging with L(u[t-1]) and reconstruction of u[t-2]
-  double lapu[RPT];
-  if (MODE == 2) {
-    double fxm[RPT], fxp[RPT];
-    x_neighbours<RPT, T>(c, ub, XUr, fxm, fxp);
+  for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
+  {
+    const T* pc = XLr + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-      const int lr = min(c.lrow0 + j, c.rows - 1);
-      const size_t o = (size_t)(lr + 1) * W + z + 1;
-      lapu[j] = (((-4.0 * ub[j] + fxm[j]) + fxp[j]) + (double)XUr[o - 1]) + (double)XUr[o + 1];
+      const double xm = j > 0 ? el[j - 1] : (double)pc[-1];
+      const double xp = j + 1 < RPT ? el[j + 1] : (double)pc[RPT];
+      const double adj = lap5(el[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
+      lam[j] = adj_update_free(l1[j], l2[j], adj);
+    }
+  }
+  // imaging with L(u[t-1]) and reconstruction of u[t-2]
+  const T* pc = XUr + c.xo;
+  double nu[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const double xm = j > 0 ? ub[j - 1] : (double)pc[-1];
+    const double xp = j + 1 < RPT ? ub[j + 1] : (double)pc[RPT];
+    const double lapu = lap5(ub[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
+    nu[j] = ua[j];
+    if (t >= 1) acc[j] = __fma_rn(lapu, lam[j], acc[j]);
+    if (t >= 2) nu[j] = recon(ub[j], ua[j], s.ed[j], lapu);
+  }
+  T* ql = XLw + c.xo;
+  T* qu = XUw + c.xo;
+  double elw[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    l2[j] = lam[j];
+    ua[j] = nu[j];
+    elw[j] = __dmul_rn(s.ed[j], lam[j]);
+    ql[j] = (T)elw[j];
+    qu[j] = (T)nu[j];
+  }
+  push_edges<RPT, T>(c, s, XLw, elw, bar_w, true);
+  push_edges<RPT, T>(c, s, XUw, nu, bar_w, true);
+}
+
+template <int RPT, class T, int MODE>
+__device__ __forceinline__ void adj_generic(const Geo& g, const CellCtx& c,
+                                            const CellStatic<RPT>& s, double (&l1)[RPT],
+                                            double (&l2)[RPT], double (&ua)[RPT],
+                                            double (&ub)[RPT], double (&acc)[RPT], int i, int U,
+                                            int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
+                                            uint32_t bar_w, double pulse_t, const IoStage& io,
+                                            const float* __restrict__ hist, size_t N2) {
+  const int RS = c.RS, z = c.z;
+  const int t = g.nt - 1 - i;
+  const int k = i % kStage;
+  double el[RPT], lam[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
+  {
+    const T* pc = XLr + c.xo;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const double xm = j > 0 ? el[j - 1] : (double)pc[-1];
+      const bool own_next = j + 1 < RPT && c.lrow0 + j + 1 < c.nr;
+      const double xp = own_next ? el[j + 1] : (double)pc[j + 1];
+      const double adj = lap5(el[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
+      if (s.undamped) {
+        lam[j] = adj_update_free(l1[j], l2[j], adj);
+      } else {
+        const double2 ab = s.ab[(size_t)min(c.lrow0 + j, c.rows - 1) * g.nz + z];
+        lam[j] = adj_update(ab.x, ab.y, l1[j], l2[j], adj);
+      }
+      if (s.rl[j] >= 0) lam[j] = __dadd_rn(lam[j], io.srec[k * io.maxrec + s.rl[j]]);
+    }
+  }
+  double lapu[RPT];
+  if (MODE == 2) {
+    const T* pc = XUr + c.xo;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const double xm = j > 0 ? ub[j - 1] : (double)pc[-1];
+      const bool own_next = j + 1 < RPT && c.lrow0 + j + 1 < c.nr;
+      const double xp = own_next ? ub[j + 1] : (double)pc[j + 1];
+      lapu[j] = lap5(ub[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
     }
   } else {
 #pragma unroll
@@ -594,57 +701,38 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
         const double fxp = x < g.nx - 1 ? (double)F[cell + g.nz] : 0.0;
         const double fzm = z > 0 ? (double)F[cell - 1] : 0.0;
         const double fzp = z < g.nz - 1 ? (double)F[cell + 1] : 0.0;
-        lapu[j] = (((-4.0 * (double)F[cell] + fxm) + fxp) + fzm) + fzp;
+        lapu[j] = lap5((double)F[cell], fxm, fxp, fzm, fzp);
       }
     }
   }
+  T* ql = XLw + c.xo;
+  T* qu = XUw + c.xo;
+  double elw[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
+    elw[j] = __dmul_rn(s.ed[j], lam[j]);
     if (!(s.active & (1u << j))) continue;
-    const int lr = c.lrow0 + j;
-    const size_t o = (size_t)(lr + 1) * W + z + 1;
     l2[j] = lam[j];
-    const T elw = (T)(s.ed[j] * lam[j]);
-    XLw[o] = elw;
+    ql[j] = (T)elw[j];
     if (t >= 1) {
       if (MODE == 1) {
-        acc[j] += lapu[j] * lam[j];
+        acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
       } else if (s.interior & (1u << j)) {
-        acc[j] += lapu[j] * lam[j];
+        acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
         if (t >= 2) {
-          double prev = 2.0 * ub[j] + s.ed[j] * lapu[j] - ua[j];
-          if (s.src & (1u << j)) prev += pulse_t;
+          double prev = recon(ub[j], ua[j], s.ed[j], lapu[j]);
+          if (s.src & (1u << j)) prev = __dadd_rn(prev, pulse_t);
           ua[j] = prev;
         }
       } else if (s.gl[j] >= 0 && t >= 2) {
-        ua[j] = (double)ring_v[j];  // ring cell: the saved strip stands in for the reconstruction
+        // ring cell: the saved strip stands in for the reconstruction
+        ua[j] = (double)io.sring[k * io.maxring + s.gl[j]];
       }
     }
-    if (MODE == 2) XUw[o] = (T)ua[j];
+    if (MODE == 2) qu[j] = (T)ua[j];
   }
-  // halo rows to the neighbouring CTAs
-  if (bulk) {
-    push_rows<T>(c, g.nz, XLw, bar_w);
-    if (MODE == 2) push_rows<T>(c, g.nz, XUw, bar_w);
-    return;
-  }
-  if (s.pushes_up) {
-    const uint32_t rb = mapa_rank(bar_w, c.rank - 1);
-    const size_t ho = (size_t)(c.rows + 1) * W + z + 1;
-    push_async(mapa_rank(smem_addr(XLw + ho), c.rank - 1), (T)(s.ed[0] * l2[0]), rb);
-    if (MODE == 2) push_async(mapa_rank(smem_addr(XUw + ho), c.rank - 1), (T)ua[0], rb);
-  }
-  if (s.pushes_dn) {
-    const uint32_t rb = mapa_rank(bar_w, c.rank + 1);
-    const uint32_t ral = mapa_rank(smem_addr(XLw + z + 1), c.rank + 1);
-    const uint32_t rau = mapa_rank(smem_addr(XUw + z + 1), c.rank + 1);
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const uint32_t on = (s.dn_mask >> j) & 1u;
-      push_if(on, ral, (T)(s.ed[j] * l2[j]), rb);
-      if (MODE == 2) push_if(on, rau, (T)ua[j], rb);
-    }
-  }
+  push_edges<RPT, T>(c, s, XLw, elw, bar_w, false);
+  if (MODE == 2) push_edges<RPT, T>(c, s, XUw, ua, bar_w, false);
 }
 
 // Load residuals of steps [i0, i0+kStage) (t = nt-1-i) and the ring strips they
@@ -671,6 +759,22 @@ __device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, 
 }
 
 template <int RPT, class T, int MODE>
+__device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
+                                         double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
+                                         double (&ub)[RPT], double (&acc)[RPT], int i, int U,
+                                         int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
+                                         uint32_t bar_r, uint32_t bar_w, uint32_t tx_bytes,
+                                         double pulse_t, const IoStage& io,
+                                         const float* __restrict__ hist, size_t N2) {
+  step_sync(c, i, bar_r, bar_w, tx_bytes);
+  if (MODE == 2 && s.fast)
+    adj_fast<RPT, T>(c, s, l1, l2, ua, ub, acc, g.nt - 1 - i, XLr, XLw, XUr, XUw, bar_w);
+  else
+    adj_generic<RPT, T, MODE>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, XLr, XLw, XUr, XUw, bar_w,
+                              pulse_t, io, hist, N2);
+}
+
+template <int RPT, class T, int MODE>
 __global__ void __launch_bounds__(kClusterMaxThreads, 1)
     cluster_adj_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
                        int unit_begin, int U,
@@ -678,22 +782,24 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
                        const float* __restrict__ strips, const float* __restrict__ ubuf,
                        double* __restrict__ acc_part, int acc_off) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT, xstride<T>(g.nz));
+  CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT, smem);
   const int lu = blockIdx.x / cs;
   const int u = unit_begin + lu;
   const int b = u / g.S;
   const int s = u - b * g.S;
+  const int txx = g.tx[2 * s], txz = g.tx[2 * s + 1];
   const size_t N2 = (size_t)g.nx * g.nz;
   const size_t pb = (size_t)b * N2;
-  const int W = c.W;
-  const size_t xe = xbuf_elems<T>(rows, g.nz);
+  const int RS = c.RS;
+  const size_t xe = xbuf_elems(rows, RPT, g.nz);
   T* base = reinterpret_cast<T*>(smem);
   T* XL[2] = {base, base + xe};
   T* XU[2] = {base + 2 * xe, base + 3 * xe};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, g.nz, 4));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, RPT, g.nz, 4));
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
+  order_columns(g, c, txx, txz, reinterpret_cast<int*>(smem));
   for (size_t k = threadIdx.x; k < 4 * xe; k += blockDim.x) base[k] = T(0);
-  const IoStage io = io_stage(smem + io_offset<T>(rows, g.nz, 4), maxrec, maxring);
+  const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 4), maxrec, maxring);
   if (threadIdx.x == 0) {
     mbar_init(bar[0], 1);
     mbar_init(bar[1], 1);
@@ -702,12 +808,12 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
   }
   __syncthreads();
   CellStatic<RPT> st;
-  load_static<RPT>(g, m, c, pb, g.tx[2 * s], g.tx[2 * s + 1],
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, g.nz, 4)), io, st);
+  load_static<RPT>(g, m, c, pb, txx, txz,
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 4)), io,
+                   MODE == 2, st);
   const int per = MODE == 2 ? 2 : 1;
-  const bool bulk = false;  // measured slower than per-thread st.async (named-barrier + bulk-copy latency)
   const uint32_t tx_bytes =
-      (uint32_t)(per * ((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * (bulk ? c.W : g.nz) * sizeof(T));
+      (uint32_t)(per * ((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T));
   const int nt = g.nt;
   const float* u_last = ubuf + ((size_t)((nt - 1) & 1) * U + lu) * N2;
   const float* u_prev = ubuf + ((size_t)((nt - 2) & 1) * U + lu) * N2;
@@ -717,7 +823,9 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
     for (int k = threadIdx.x; k < (c.nr + 2) * g.nz; k += blockDim.x) {
       const int r = k / g.nz, zz = k - r * g.nz;
       const int x = c.r0 - 1 + r;
-      if (x >= 0 && x < g.nx) XU[1][(size_t)r * W + zz + 1] = (T)u_prev[(size_t)x * g.nz + zz];
+      // buffer row r (0: top halo, nr + 1: bottom halo at rows + 1)
+      const int rb = r == c.nr + 1 ? c.rows + 1 : r;
+      if (x >= 0 && x < g.nx) XU[1][(size_t)(zz + 1) * RS + rb] = (T)u_prev[(size_t)x * g.nz + zz];
     }
   }
   double la[RPT], lb[RPT], ua[RPT], ub[RPT], acc[RPT];
@@ -739,15 +847,15 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
     if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
     const double p0 = owns_src ? g.pulse[nt - 1 - i] : 0.0;
     adj_step<RPT, T, MODE>(g, c, st, la, lb, ua, ub, acc, i, U, lu, XL[1], XL[0], XU[1], XU[0],
-                           bar[1], bar[0], tx_bytes, p0, io, hist, N2, bulk);
+                           bar[1], bar[0], tx_bytes, p0, io, hist, N2);
     const double p1 = owns_src ? g.pulse[nt - 2 - i] : 0.0;
     adj_step<RPT, T, MODE>(g, c, st, lb, la, ub, ua, acc, i + 1, U, lu, XL[0], XL[1], XU[0], XU[1],
-                           bar[0], bar[1], tx_bytes, p1, io, hist, N2, bulk);
+                           bar[0], bar[1], tx_bytes, p1, io, hist, N2);
   }
   if (i < nt) {
     if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
     adj_step<RPT, T, MODE>(g, c, st, la, lb, ua, ub, acc, i, U, lu, XL[1], XL[0], XU[1], XU[0],
-                           bar[1], bar[0], tx_bytes, owns_src ? g.pulse[0] : 0.0, io, hist, N2, bulk);
+                           bar[1], bar[0], tx_bytes, owns_src ? g.pulse[0] : 0.0, io, hist, N2);
   }
   if (c.has_up || c.has_dn) mbar_wait(bar[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
   cluster_sync_all();
@@ -797,13 +905,15 @@ inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
   if (threads > kClusterMaxThreads) return false;
   const int maxrec = std::min(g.M, rows * g.nz);
   const int maxring = g.SL > 0 ? std::min(g.SL, 2 * rows + 2 * g.nz) : 0;
-  const size_t sf = cluster_smem_bytes<T>(rows, g.nz, 2, maxrec, maxring);
-  const size_t sa = cluster_smem_bytes<T>(rows, g.nz, 4, maxrec, maxring);
-  if (max_active_clusters(cluster_fwd_kernel<RPT, T, 0>, cs, threads, sf) <= 0) return false;
-  if (max_active_clusters(cluster_fwd_kernel<RPT, T, 1>, cs, threads, sf) <= 0) return false;
-  if (max_active_clusters(cluster_fwd_kernel<RPT, T, 2>, cs, threads, sf) <= 0) return false;
-  if (max_active_clusters(cluster_adj_kernel<RPT, T, 1>, cs, threads, sa) <= 0) return false;
-  if (max_active_clusters(cluster_adj_kernel<RPT, T, 2>, cs, threads, sa) <= 0) return false;
+  const size_t sf = cluster_smem_bytes<T>(rows, RPT, g.nz, 2, maxrec, maxring);
+  const size_t sa = cluster_smem_bytes<T>(rows, RPT, g.nz, 4, maxrec, maxring);
+  // clusters co-resident on the device: the least over the sweep kernels
+  int n = max_active_clusters(cluster_fwd_kernel<RPT, T, 0>, cs, threads, sf);
+  n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 1>, cs, threads, sf));
+  n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 2>, cs, threads, sf));
+  n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 1>, cs, threads, sa));
+  n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 2>, cs, threads, sa));
+  if (n <= 0) return false;
   out->cs = cs;
   out->rows = rows;
   out->rpt = RPT;
@@ -814,10 +924,41 @@ inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
   out->smem_adj = sa;
   out->maxrec = maxrec;
   out->maxring = maxring;
+  out->maxc = n;
   return true;
 }
 
-inline bool cluster_config(const Geo& g, bool rho, ClusterCfg* out) {
+// Rows per thread are a template parameter (register-resident state); the
+// instances below cover up to 8 rows per thread with f64 exchange rows and
+// 2 / 4 with the f32 fallback (large nz, where f64 rows exceed shared memory).
+template <class T>
+inline bool try_cluster_rpt(const Geo& g, int cs, ClusterCfg* out) {
+  const int rows = (g.nx + cs - 1) / cs;
+  const int segmax = kClusterMaxThreads / std::max(g.nz, 1);
+  if (segmax < 1 || rows < 2) return false;
+  int need = (rows + segmax - 1) / segmax;
+  // the fewest rows per thread that fit: more warps per SM hide the step's
+  // latencies better than fuller segments do (measured: 16 rows as 3 x 6 beat
+  // 2 x 8); DUFWI_CLUSTER_RPT pins it (experiments)
+  if (const char* e = getenv("DUFWI_CLUSTER_RPT")) need = std::max(need, atoi(e));
+  const int opts[6] = {2, 4, 5, 6, 7, 8};
+  int pick = 0;
+  for (int r : opts)
+    if (!pick && r >= need && (sizeof(T) == 8 || r <= 4)) pick = r;
+  switch (pick) {
+    case 2: return try_cluster_cfg<2, T>(g, cs, out);
+    case 4: return try_cluster_cfg<4, T>(g, cs, out);
+    case 5: return sizeof(T) == 8 && try_cluster_cfg<5, double>(g, cs, out);
+    case 6: return sizeof(T) == 8 && try_cluster_cfg<6, double>(g, cs, out);
+    case 7: return sizeof(T) == 8 && try_cluster_cfg<7, double>(g, cs, out);
+    case 8: return sizeof(T) == 8 && try_cluster_cfg<8, double>(g, cs, out);
+    default: return false;
+  }
+}
+
+// Every cluster size from 16 down to 2 that fits, each with its co-residency.
+inline bool cluster_candidates(const Geo& g, bool rho, std::vector<ClusterCfg>& out) {
+  out.clear();
   if (rho) return false;  // density runs on the stepwise engine
   int dev = 0, major = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -826,15 +967,30 @@ inline bool cluster_config(const Geo& g, bool rho, ClusterCfg* out) {
     cudaGetLastError();
     return false;
   }
-  for (int cs : {16, 8}) {
+  int only = 0;  // DUFWI_CLUSTER_CS pins the cluster size (experiments)
+  if (const char* e = getenv("DUFWI_CLUSTER_CS")) only = atoi(e);
+  for (int cs = 16; cs >= 2; --cs) {
+    if (only && cs != only) continue;
+    ClusterCfg c;
 #ifndef DUFWI_EXCHANGE_F32
-    if (try_cluster_cfg<4, double>(g, cs, out)) return true;
-    if (try_cluster_cfg<2, double>(g, cs, out)) return true;
+    if (try_cluster_rpt<double>(g, cs, &c)) { out.push_back(c); continue; }
 #endif
-    if (try_cluster_cfg<4, float>(g, cs, out)) return true;
-    if (try_cluster_cfg<2, float>(g, cs, out)) return true;
+    if (try_cluster_rpt<float>(g, cs, &c)) out.push_back(c);
   }
-  return false;
+  return !out.empty();
+}
+
+// Launch shape for U units: the fewest waves of co-resident clusters (a unit's
+// time loop cannot be split, so a second wave doubles the sweep), then the
+// largest cluster (fewest rows per thread).
+inline const ClusterCfg& pick_cluster(const std::vector<ClusterCfg>& c, int U) {
+  size_t best = 0;
+  long best_w = -1;
+  for (size_t i = 0; i < c.size(); ++i) {
+    const long w = (U + c[i].maxc - 1) / c[i].maxc;
+    if (best_w < 0 || w < best_w) { best = i; best_w = w; }
+  }
+  return c[best];
 }
 
 template <class K, class... Args>
@@ -885,27 +1041,29 @@ inline cudaError_t cluster_adjoint_t(const Geo& g, const Model& m, const Cluster
                         c.maxrec, c.maxring, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off);
 }
 
-inline int cluster_forward(const Geo& g, const Model& m, const ClusterCfg& c, bool /*rho*/,
-                           int mode, int unit_begin, int U, float* rec, float* hist,
-                           float* strips, float* ubuf, cudaStream_t st) {
-  cudaError_t e;
-  if (c.rpt == 4 && c.dbl) e = cluster_forward_t<4, double>(g, m, c, mode, unit_begin, U, rec, hist, strips, ubuf, st);
-  else if (c.rpt == 2 && c.dbl) e = cluster_forward_t<2, double>(g, m, c, mode, unit_begin, U, rec, hist, strips, ubuf, st);
-  else if (c.rpt == 4) e = cluster_forward_t<4, float>(g, m, c, mode, unit_begin, U, rec, hist, strips, ubuf, st);
-  else e = cluster_forward_t<2, float>(g, m, c, mode, unit_begin, U, rec, hist, strips, ubuf, st);
-  return (int)e;
+#define DUFWI_CLUSTER_DISPATCH(FN, ...)                                        \
+  (c.dbl ? (c.rpt == 2   ? FN<2, double>(__VA_ARGS__)                          \
+            : c.rpt == 4 ? FN<4, double>(__VA_ARGS__)                          \
+            : c.rpt == 5 ? FN<5, double>(__VA_ARGS__)                          \
+            : c.rpt == 6 ? FN<6, double>(__VA_ARGS__)                          \
+            : c.rpt == 7 ? FN<7, double>(__VA_ARGS__)                          \
+                         : FN<8, double>(__VA_ARGS__))                         \
+         : (c.rpt == 2 ? FN<2, float>(__VA_ARGS__) : FN<4, float>(__VA_ARGS__)))
+
+inline int cluster_forward(const Geo& g, const Model& m, const ClusterCfg& c, int mode,
+                           int unit_begin, int U, float* rec, float* hist, float* strips,
+                           float* ubuf, cudaStream_t st) {
+  return (int)DUFWI_CLUSTER_DISPATCH(cluster_forward_t, g, m, c, mode, unit_begin, U, rec, hist,
+                                     strips, ubuf, st);
 }
 
-inline int cluster_adjoint(const Geo& g, const Model& m, const ClusterCfg& c, bool /*rho*/,
-                           int mode, int unit_begin, int U, const double* rres, const float* hist,
+inline int cluster_adjoint(const Geo& g, const Model& m, const ClusterCfg& c, int mode,
+                           int unit_begin, int U, const double* rres, const float* hist,
                            const float* strips, const float* ubuf, double* acc_part, int acc_off,
                            cudaStream_t st) {
-  cudaError_t e;
-  if (c.rpt == 4 && c.dbl) e = cluster_adjoint_t<4, double>(g, m, c, mode, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off, st);
-  else if (c.rpt == 2 && c.dbl) e = cluster_adjoint_t<2, double>(g, m, c, mode, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off, st);
-  else if (c.rpt == 4) e = cluster_adjoint_t<4, float>(g, m, c, mode, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off, st);
-  else e = cluster_adjoint_t<2, float>(g, m, c, mode, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off, st);
-  return (int)e;
+  return (int)DUFWI_CLUSTER_DISPATCH(cluster_adjoint_t, g, m, c, mode, unit_begin, U, rres, hist,
+                                     strips, ubuf, acc_part, acc_off, st);
 }
+#undef DUFWI_CLUSTER_DISPATCH
 
 }  // namespace dufwi
