@@ -280,10 +280,14 @@ def run_ours(args, rank: int, world: int) -> None:
         pk.unfold_infer(obs_host, c0_host, nets, setup)  # warm the public-API engine
         barrier()
         e0 = time.perf_counter()
+        per = []
         for _ in range(args.steps):
             maps = pk.unfold_infer(obs_host, c0_host, nets, setup)
+            per.append(time.perf_counter())
         torch.cuda.synchronize()
         e_s = time.perf_counter() - e0
+        print("e2e per-step s:", [round(b - a, 4) for a, b in zip([e0] + per[:-1], per)],
+              file=sys.stderr)
         e_t = torch.tensor([e_s], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)

@@ -60,7 +60,10 @@ struct ClusterCfg {
 // global accesses inside every step.
 constexpr int kStage = 16;
 
-constexpr int kClusterMaxThreads = 512;  // 128 registers per thread available
+// Threads per CTA the sweep kernels are compiled for: the register budget per
+// thread (65536 / threads) must hold RPT rows of f64 state (6 per row in the
+// adjoint) without spilling.
+__host__ __device__ constexpr int cluster_max_threads(int rpt) { return rpt >= 7 ? 384 : 512; }
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -119,7 +122,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 
 // ------------------------------------------------------------ smem layout
-// [nbufs exchange buffers] [rows x nz double2 (A, B)] [2 mbarriers] [IO stage]
+// [nbufs exchange buffers] [nz x nseg*RPT double2 (A, B)] [2 mbarriers] [IO stage]
 // An exchange buffer is column-major: cell (buffer row r, column z) at
 // (z + 1) * RS + r, r = local row + 1 (r = 0 / rows + 1: halo rows from the
 // neighbouring CTAs), z = -1 / nz: zero pad columns.  RS >= nseg * RPT + 2 is
@@ -136,9 +139,14 @@ template <class T>
 __host__ __device__ inline size_t ab_offset(int rows, int rpt, int nz, int nbufs) {
   return ((size_t)nbufs * xbuf_elems(rows, rpt, nz) * sizeof(T) + 15) & ~(size_t)15;
 }
+// (A, B) table: column-major like the buffers, >= nseg * RPT row slots per
+// column, odd so 16-byte accesses of consecutive columns are conflict-free
+__host__ __device__ inline int ab_col_stride(int rows, int rpt) {
+  return ((rows + rpt - 1) / rpt * rpt) | 1;
+}
 template <class T>
 __host__ __device__ inline size_t bar_offset(int rows, int rpt, int nz, int nbufs) {
-  return ab_offset<T>(rows, rpt, nz, nbufs) + (size_t)rows * nz * sizeof(double2);
+  return ab_offset<T>(rows, rpt, nz, nbufs) + (size_t)ab_col_stride(rows, rpt) * nz * sizeof(double2);
 }
 // IO stage after the mbarriers: [n_rec, n_ring, pad] [rec_g[maxrec]] [ring_g[maxring]]
 // [double stage_rec[kStage][maxrec]] [float stage_ring[kStage][maxring]]
@@ -306,8 +314,9 @@ struct CellStatic {
   unsigned dn_mask;           // bit j set: register j holds the slab's last row (pushes_dn)
   bool special;               // any receiver / ring / source cell
   bool undamped;              // every cell has D == 0: (A, B) = (2, -1), no table reads
-  bool fast;                  // whole warp: all rows active, undamped, interior, not special
-  const double2* ab;          // shared (A, B) table, row stride nz
+  bool fast;                  // whole warp: full, undamped, interior, not special
+  bool full;                  // whole warp: every row slot active
+  const double2* ab;          // this thread's (A, B) column: ab[j] for row j
 };
 
 template <int RPT>
@@ -316,7 +325,7 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
                                             const IoStage& io, bool allow_fast,
                                             CellStatic<RPT>& st) {
   st.active = st.src = st.interior = 0u;
-  st.ab = ab_table;
+  st.ab = ab_table + (size_t)c.z * ab_col_stride(c.rows, RPT) + c.lrow0;
   st.pushes_up = c.has_up && c.lrow0 == 0;
   st.pushes_dn = false;
   st.dn_mask = 0u;
@@ -332,7 +341,7 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
       st.ed[j] = m.Ed[pb + (size_t)x * g.nz + c.z];
       double A, B;
       ab_coeffs(damping_at(g, x, c.z), g.dt, A, B);
-      ab_table[(size_t)lr * g.nz + c.z] = make_double2(A, B);
+      const_cast<double2*>(st.ab)[j] = make_double2(A, B);
       const int slot = g.row_flag[x] ? g.node_slot[(size_t)x * g.nz + c.z] : -1;
       if (slot >= 0) {
         st.rl[j] = atomicAdd(&io.counts[0], 1);  // storage slot only: order does not matter
@@ -361,7 +370,9 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
   st.special = any;
   const unsigned full = (1u << RPT) - 1u;
   const bool f = allow_fast && st.active == full && st.interior == full && st.undamped && !any;
-  st.fast = __all_sync(__activemask(), f);  // warp-uniform path choice
+  // warp-uniform path choice
+  st.fast = __all_sync(__activemask(), f);
+  st.full = __all_sync(__activemask(), st.active == full);
 }
 
 // Exchange-row pushes to the neighbouring CTAs (DSMEM st.async completing on
@@ -375,14 +386,14 @@ __device__ __forceinline__ uint32_t remote(const CellCtx& c, uint32_t rbase, con
 
 template <int RPT, class T>
 __device__ __forceinline__ void push_edges(const CellCtx& c, const CellStatic<RPT>& s, T* X,
-                                           const double (&v)[RPT], uint32_t bar_w, bool fast) {
+                                           const double (&v)[RPT], uint32_t bar_w, bool full) {
   const T* col = X + (c.z + 1) * c.RS;
   if (s.pushes_up)
     push_async(remote(c, c.rup, col + c.rows + 1), (T)v[0], c.rup + (bar_w - c.lbase));
   if (s.pushes_dn) {
     const uint32_t ra = remote(c, c.rdn, col);
     const uint32_t rb = c.rdn + (bar_w - c.lbase);
-    if (fast) {
+    if (full) {  // every slot active: the slab's last row is register RPT-1
       push_async(ra, (T)v[RPT - 1], rb);
     } else {
       // explicit predicate per register so v[] is never indexed at run time
@@ -402,11 +413,15 @@ __device__ __forceinline__ void step_sync(const CellCtx& c, int i, uint32_t bar_
   if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
 }
 
-// Plain cells: undamped, no receiver / ring / source, every row active.
-template <int RPT, class T>
-__device__ __forceinline__ void fwd_fast(const CellCtx& c, const CellStatic<RPT>& s,
-                                         double (&u1)[RPT], double (&u2)[RPT], const T* Xr,
-                                         T* Xw, uint32_t bar_w) {
+// One forward step of a thread's cells.  FULL: every row slot active (no
+// per-row predicates); PLAIN: undamped, no receiver / ring / source cell
+// (A = 2, B = -1, no IO).  Both are warp-uniform, chosen once per sweep.
+template <int RPT, class T, int MODE, bool FULL, bool PLAIN>
+__device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
+                                         double (&u1)[RPT], double (&u2)[RPT], int t, int U,
+                                         int lu, const T* Xr, T* Xw, uint32_t bar_w,
+                                         double pulse_t, const IoStage& io,
+                                         float* __restrict__ hist, size_t N2) {
   const T* pc = Xr + c.xo;
   const T* pm = pc - c.RS;
   const T* pp = pc + c.RS;
@@ -414,44 +429,17 @@ __device__ __forceinline__ void fwd_fast(const CellCtx& c, const CellStatic<RPT>
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const double xm = j > 0 ? u1[j - 1] : (double)pc[-1];
-    const double xp = j + 1 < RPT ? u1[j + 1] : (double)pc[RPT];
-    const double lap = lap5(u1[j], xm, xp, (double)pm[j], (double)pp[j]);
-    v[j] = fwd_update_free(u1[j], u2[j], s.ed[j], lap);
-  }
-  T* q = Xw + c.xo;
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    u2[j] = v[j];
-    q[j] = (T)v[j];
-  }
-  push_edges<RPT, T>(c, s, Xw, v, bar_w, true);
-}
-
-template <int RPT, class T, int MODE>
-__device__ __forceinline__ void fwd_generic(const Geo& g, const CellCtx& c,
-                                            const CellStatic<RPT>& s, double (&u1)[RPT],
-                                            double (&u2)[RPT], int t, int U, int lu, const T* Xr,
-                                            T* Xw, uint32_t bar_w, double pulse_t,
-                                            const IoStage& io, float* __restrict__ hist,
-                                            size_t N2) {
-  const T* pc = Xr + c.xo;
-  const T* pm = pc - c.RS;
-  const T* pp = pc + c.RS;
-  double v[RPT];
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    const double xm = j > 0 ? u1[j - 1] : (double)pc[-1];
-    const bool own_next = j + 1 < RPT && c.lrow0 + j + 1 < c.nr;
+    const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
     const double xp = own_next ? u1[j + 1] : (double)pc[j + 1];
     const double lap = lap5(u1[j], xm, xp, (double)pm[j], (double)pp[j]);
-    if (s.undamped) {
+    if (PLAIN) {
       v[j] = fwd_update_free(u1[j], u2[j], s.ed[j], lap);
     } else {
-      const double2 ab = s.ab[(size_t)min(c.lrow0 + j, c.rows - 1) * g.nz + c.z];
+      const double2 ab = s.ab[j];
       v[j] = fwd_update(ab.x, ab.y, u1[j], u2[j], s.ed[j], lap);
     }
   }
-  if (s.src) {
+  if (!PLAIN && s.src) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
       if (s.src & (1u << j)) v[j] = __dadd_rn(v[j], pulse_t);
@@ -459,17 +447,17 @@ __device__ __forceinline__ void fwd_generic(const Geo& g, const CellCtx& c,
   T* q = Xw + c.xo;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    if (!(s.active & (1u << j))) continue;
+    if (!FULL && !(s.active & (1u << j))) continue;
     u2[j] = v[j];
     q[j] = (T)v[j];
   }
-  push_edges<RPT, T>(c, s, Xw, v, bar_w, false);
-  if (!s.special && MODE != 1) return;
+  push_edges<RPT, T>(c, s, Xw, v, bar_w, FULL);
+  if (PLAIN || (!s.special && MODE != 1)) return;
   // receivers, history / ring strips
   const int k = t % kStage;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    if (!(s.active & (1u << j))) continue;
+    if (!FULL && !(s.active & (1u << j))) continue;
     const float vf = (float)v[j];
     if (s.rl[j] >= 0) io.srec[k * io.maxrec + s.rl[j]] = (double)vf;
     if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = vf;
@@ -502,15 +490,31 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
                                          int lu, const T* Xr, T* Xw, uint32_t bar_r,
                                          uint32_t bar_w, uint32_t tx_bytes, double pulse_t,
                                          const IoStage& io, float* __restrict__ hist, size_t N2) {
+#ifdef DUFWI_EXP_TIMING
+  const long long T0 = clock64();
+#endif
   step_sync(c, t, bar_r, bar_w, tx_bytes);
+#ifdef DUFWI_EXP_TIMING
+  const long long T1 = clock64();
+#endif
   if (s.fast)
-    fwd_fast<RPT, T>(c, s, u1, u2, Xr, Xw, bar_w);
+    fwd_body<RPT, T, MODE, true, true>(g, c, s, u1, u2, t, U, lu, Xr, Xw, bar_w, pulse_t, io, hist, N2);
+  else if (s.full)
+    fwd_body<RPT, T, MODE, true, false>(g, c, s, u1, u2, t, U, lu, Xr, Xw, bar_w, pulse_t, io, hist, N2);
   else
-    fwd_generic<RPT, T, MODE>(g, c, s, u1, u2, t, U, lu, Xr, Xw, bar_w, pulse_t, io, hist, N2);
+    fwd_body<RPT, T, MODE, false, false>(g, c, s, u1, u2, t, U, lu, Xr, Xw, bar_w, pulse_t, io, hist, N2);
+#ifdef DUFWI_EXP_TIMING
+  if (blockIdx.x == 5 && (threadIdx.x & 31) == 0) {
+    const int w = threadIdx.x >> 5;
+    atomicAdd(&g_dbg[w * 4 + 0], (unsigned long long)(T1 - T0));
+    atomicAdd(&g_dbg[w * 4 + 1], (unsigned long long)(clock64() - T1));
+    atomicAdd(&g_dbg[w * 4 + 2], s.fast ? 1ull : 0ull);
+  }
+#endif
 }
 
 template <int RPT, class T, int MODE>
-__global__ void __launch_bounds__(kClusterMaxThreads, 1)
+__global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
     cluster_fwd_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
                        int unit_begin, int U, float* __restrict__ rec, float* __restrict__ hist,
                        float* __restrict__ strips, float* __restrict__ ubuf) {
@@ -600,65 +604,17 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
 // adjoint step i (time t = nt-1-i).  l1 = lam[t+1], l2 = lam[t+2] -> lam[t];
 // ua = u[t] -> u[t-2] (reconstruction, MODE 2), ub = u[t-1].
 // XL: exchange of E*lam, XU: exchange of u (MODE 2).  Buffers/bars indexed by i.
-template <int RPT, class T>
-__device__ __forceinline__ void adj_fast(const CellCtx& c, const CellStatic<RPT>& s,
+template <int RPT, class T, int MODE, bool FULL, bool PLAIN>
+__device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
-                                         double (&ub)[RPT], double (&acc)[RPT], int t,
-                                         const T* XLr, T* XLw, const T* XUr, T* XUw,
-                                         uint32_t bar_w) {
-  const int RS = c.RS;
-  // lam[t] = A lam1 + L^T(E lam1) + B lam2
-  double el[RPT], lam[RPT];
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
-  {
-    const T* pc = XLr + c.xo;
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const double xm = j > 0 ? el[j - 1] : (double)pc[-1];
-      const double xp = j + 1 < RPT ? el[j + 1] : (double)pc[RPT];
-      const double adj = lap5(el[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
-      lam[j] = adj_update_free(l1[j], l2[j], adj);
-    }
-  }
-  // imaging with L(u[t-1]) and reconstruction of u[t-2]
-  const T* pc = XUr + c.xo;
-  double nu[RPT];
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    const double xm = j > 0 ? ub[j - 1] : (double)pc[-1];
-    const double xp = j + 1 < RPT ? ub[j + 1] : (double)pc[RPT];
-    const double lapu = lap5(ub[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
-    nu[j] = ua[j];
-    if (t >= 1) acc[j] = __fma_rn(lapu, lam[j], acc[j]);
-    if (t >= 2) nu[j] = recon(ub[j], ua[j], s.ed[j], lapu);
-  }
-  T* ql = XLw + c.xo;
-  T* qu = XUw + c.xo;
-  double elw[RPT];
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    l2[j] = lam[j];
-    ua[j] = nu[j];
-    elw[j] = __dmul_rn(s.ed[j], lam[j]);
-    ql[j] = (T)elw[j];
-    qu[j] = (T)nu[j];
-  }
-  push_edges<RPT, T>(c, s, XLw, elw, bar_w, true);
-  push_edges<RPT, T>(c, s, XUw, nu, bar_w, true);
-}
-
-template <int RPT, class T, int MODE>
-__device__ __forceinline__ void adj_generic(const Geo& g, const CellCtx& c,
-                                            const CellStatic<RPT>& s, double (&l1)[RPT],
-                                            double (&l2)[RPT], double (&ua)[RPT],
-                                            double (&ub)[RPT], double (&acc)[RPT], int i, int U,
-                                            int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
-                                            uint32_t bar_w, double pulse_t, const IoStage& io,
-                                            const float* __restrict__ hist, size_t N2) {
+                                         double (&ub)[RPT], double (&acc)[RPT], int i, int U,
+                                         int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
+                                         uint32_t bar_w, double pulse_t, const IoStage& io,
+                                         const float* __restrict__ hist, size_t N2) {
   const int RS = c.RS, z = c.z;
   const int t = g.nt - 1 - i;
   const int k = i % kStage;
+  // lam[t] = A lam1 + L^T(E lam1) + B lam2 (+ residual at receivers)
   double el[RPT], lam[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
@@ -667,25 +623,30 @@ __device__ __forceinline__ void adj_generic(const Geo& g, const CellCtx& c,
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       const double xm = j > 0 ? el[j - 1] : (double)pc[-1];
-      const bool own_next = j + 1 < RPT && c.lrow0 + j + 1 < c.nr;
+      const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
       const double xp = own_next ? el[j + 1] : (double)pc[j + 1];
       const double adj = lap5(el[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
-      if (s.undamped) {
+      if (PLAIN) {
         lam[j] = adj_update_free(l1[j], l2[j], adj);
       } else {
-        const double2 ab = s.ab[(size_t)min(c.lrow0 + j, c.rows - 1) * g.nz + z];
+        const double2 ab = s.ab[j];
         lam[j] = adj_update(ab.x, ab.y, l1[j], l2[j], adj);
       }
-      if (s.rl[j] >= 0) lam[j] = __dadd_rn(lam[j], io.srec[k * io.maxrec + s.rl[j]]);
     }
   }
+  if (!PLAIN && s.special) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
+      if (s.rl[j] >= 0) lam[j] = __dadd_rn(lam[j], io.srec[k * io.maxrec + s.rl[j]]);
+  }
+  // imaging with L(u[t-1]) and reconstruction of u[t-2]
   double lapu[RPT];
   if (MODE == 2) {
     const T* pc = XUr + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       const double xm = j > 0 ? ub[j - 1] : (double)pc[-1];
-      const bool own_next = j + 1 < RPT && c.lrow0 + j + 1 < c.nr;
+      const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
       const double xp = own_next ? ub[j + 1] : (double)pc[j + 1];
       lapu[j] = lap5(ub[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
     }
@@ -693,7 +654,7 @@ __device__ __forceinline__ void adj_generic(const Geo& g, const CellCtx& c,
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       lapu[j] = 0.0;
-      if (t >= 1 && (s.active & (1u << j))) {
+      if (t >= 1 && (FULL || (s.active & (1u << j)))) {
         const float* F = hist + ((size_t)(t - 1) * U + lu) * N2;
         const int x = c.r0 + c.lrow0 + j;
         const size_t cell = (size_t)x * g.nz + z;
@@ -711,17 +672,17 @@ __device__ __forceinline__ void adj_generic(const Geo& g, const CellCtx& c,
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     elw[j] = __dmul_rn(s.ed[j], lam[j]);
-    if (!(s.active & (1u << j))) continue;
+    if (!FULL && !(s.active & (1u << j))) continue;
     l2[j] = lam[j];
     ql[j] = (T)elw[j];
     if (t >= 1) {
       if (MODE == 1) {
         acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
-      } else if (s.interior & (1u << j)) {
+      } else if (PLAIN || (s.interior & (1u << j))) {
         acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
         if (t >= 2) {
           double prev = recon(ub[j], ua[j], s.ed[j], lapu[j]);
-          if (s.src & (1u << j)) prev = __dadd_rn(prev, pulse_t);
+          if (!PLAIN && (s.src & (1u << j))) prev = __dadd_rn(prev, pulse_t);
           ua[j] = prev;
         }
       } else if (s.gl[j] >= 0 && t >= 2) {
@@ -731,8 +692,8 @@ __device__ __forceinline__ void adj_generic(const Geo& g, const CellCtx& c,
     }
     if (MODE == 2) qu[j] = (T)ua[j];
   }
-  push_edges<RPT, T>(c, s, XLw, elw, bar_w, false);
-  if (MODE == 2) push_edges<RPT, T>(c, s, XUw, ua, bar_w, false);
+  push_edges<RPT, T>(c, s, XLw, elw, bar_w, FULL);
+  if (MODE == 2) push_edges<RPT, T>(c, s, XUw, ua, bar_w, FULL);
 }
 
 // Load residuals of steps [i0, i0+kStage) (t = nt-1-i) and the ring strips they
@@ -768,14 +729,18 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
                                          const float* __restrict__ hist, size_t N2) {
   step_sync(c, i, bar_r, bar_w, tx_bytes);
   if (MODE == 2 && s.fast)
-    adj_fast<RPT, T>(c, s, l1, l2, ua, ub, acc, g.nt - 1 - i, XLr, XLw, XUr, XUw, bar_w);
+    adj_body<RPT, T, MODE, true, true>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, XLr, XLw, XUr, XUw,
+                                       bar_w, pulse_t, io, hist, N2);
+  else if (s.full)
+    adj_body<RPT, T, MODE, true, false>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, XLr, XLw, XUr,
+                                        XUw, bar_w, pulse_t, io, hist, N2);
   else
-    adj_generic<RPT, T, MODE>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, XLr, XLw, XUr, XUw, bar_w,
-                              pulse_t, io, hist, N2);
+    adj_body<RPT, T, MODE, false, false>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, XLr, XLw, XUr,
+                                         XUw, bar_w, pulse_t, io, hist, N2);
 }
 
 template <int RPT, class T, int MODE>
-__global__ void __launch_bounds__(kClusterMaxThreads, 1)
+__global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
     cluster_adj_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
                        int unit_begin, int U,
                        const double* __restrict__ rres, const float* __restrict__ hist,
@@ -868,7 +833,7 @@ __global__ void __launch_bounds__(kClusterMaxThreads, 1)
 // ------------------------------------------------------------------ host side
 template <class K>
 inline int max_active_clusters(K kernel, int cs, int threads, size_t smem) {
-  if (smem > 227 * 1024 || threads > kClusterMaxThreads) return 0;
+  if (smem > 227 * 1024) return 0;
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
       (cs > 8 && cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
     cudaGetLastError();
@@ -902,7 +867,7 @@ inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
   if (rows < 2) return false;
   const int nseg = (rows + RPT - 1) / RPT;
   const int threads = g.nz * nseg;
-  if (threads > kClusterMaxThreads) return false;
+  if (threads > cluster_max_threads(RPT)) return false;
   const int maxrec = std::min(g.M, rows * g.nz);
   const int maxring = g.SL > 0 ? std::min(g.SL, 2 * rows + 2 * g.nz) : 0;
   const size_t sf = cluster_smem_bytes<T>(rows, RPT, g.nz, 2, maxrec, maxring);
@@ -932,20 +897,8 @@ inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
 // instances below cover up to 8 rows per thread with f64 exchange rows and
 // 2 / 4 with the f32 fallback (large nz, where f64 rows exceed shared memory).
 template <class T>
-inline bool try_cluster_rpt(const Geo& g, int cs, ClusterCfg* out) {
-  const int rows = (g.nx + cs - 1) / cs;
-  const int segmax = kClusterMaxThreads / std::max(g.nz, 1);
-  if (segmax < 1 || rows < 2) return false;
-  int need = (rows + segmax - 1) / segmax;
-  // the fewest rows per thread that fit: more warps per SM hide the step's
-  // latencies better than fuller segments do (measured: 16 rows as 3 x 6 beat
-  // 2 x 8); DUFWI_CLUSTER_RPT pins it (experiments)
-  if (const char* e = getenv("DUFWI_CLUSTER_RPT")) need = std::max(need, atoi(e));
-  const int opts[6] = {2, 4, 5, 6, 7, 8};
-  int pick = 0;
-  for (int r : opts)
-    if (!pick && r >= need && (sizeof(T) == 8 || r <= 4)) pick = r;
-  switch (pick) {
+inline bool try_cluster_rpt(const Geo& g, int cs, int rpt, ClusterCfg* out) {
+  switch (rpt) {
     case 2: return try_cluster_cfg<2, T>(g, cs, out);
     case 4: return try_cluster_cfg<4, T>(g, cs, out);
     case 5: return sizeof(T) == 8 && try_cluster_cfg<5, double>(g, cs, out);
@@ -956,7 +909,9 @@ inline bool try_cluster_rpt(const Geo& g, int cs, ClusterCfg* out) {
   }
 }
 
-// Every cluster size from 16 down to 2 that fits, each with its co-residency.
+// Every launch shape that fits: cluster sizes 16 .. 2, each with the fewest
+// rows per thread that fit the thread budget and any larger count that splits
+// the slab exactly.  DUFWI_CLUSTER_CS / DUFWI_CLUSTER_RPT pin them (experiments).
 inline bool cluster_candidates(const Geo& g, bool rho, std::vector<ClusterCfg>& out) {
   out.clear();
   if (rho) return false;  // density runs on the stepwise engine
@@ -967,28 +922,57 @@ inline bool cluster_candidates(const Geo& g, bool rho, std::vector<ClusterCfg>& 
     cudaGetLastError();
     return false;
   }
-  int only = 0;  // DUFWI_CLUSTER_CS pins the cluster size (experiments)
-  if (const char* e = getenv("DUFWI_CLUSTER_CS")) only = atoi(e);
+  int only_cs = 0, only_rpt = 0;
+  if (const char* e = getenv("DUFWI_CLUSTER_CS")) only_cs = atoi(e);
+  if (const char* e = getenv("DUFWI_CLUSTER_RPT")) only_rpt = atoi(e);
+  const int opts[6] = {2, 4, 5, 6, 7, 8};
   for (int cs = 16; cs >= 2; --cs) {
-    if (only && cs != only) continue;
-    ClusterCfg c;
+    if (only_cs && cs != only_cs) continue;
+    const int rows = (g.nx + cs - 1) / cs;
+    if (rows < 2 || g.nz < 1) continue;
+    bool first = true;
+    for (int r : opts) {
+      const int nseg = (rows + r - 1) / r;
+      if (g.nz * nseg > cluster_max_threads(r)) continue;
+      const bool take = only_rpt ? r == only_rpt : (first || rows % r == 0);
+      first = false;
+      if (!take) continue;
+      ClusterCfg c;
 #ifndef DUFWI_EXCHANGE_F32
-    if (try_cluster_rpt<double>(g, cs, &c)) { out.push_back(c); continue; }
+      if (try_cluster_rpt<double>(g, cs, r, &c)) { out.push_back(c); continue; }
 #endif
-    if (try_cluster_rpt<float>(g, cs, &c)) out.push_back(c);
+      if (try_cluster_rpt<float>(g, cs, r, &c)) out.push_back(c);
+    }
   }
   return !out.empty();
 }
 
+// Per-step cost model of a shape, in row slots per SM: idle slots of a partial
+// last segment keep its warps off the fast step (x1.3); 7-8 rows per thread
+// run fewer warps with more register pressure (x1.15).  Measured on config 1:
+// 18 slots as 3 x 6 < 16 as 2 x 8 < 18 as 3 x 6 with 16 rows used.
+inline double cluster_cost(const ClusterCfg& c) {
+  double cost = (double)c.nseg * c.rpt;
+  if (c.rows % c.rpt) cost *= 1.3;
+  if (c.rpt >= 7) cost *= 1.15;
+  return cost;
+}
+
 // Launch shape for U units: the fewest waves of co-resident clusters (a unit's
 // time loop cannot be split, so a second wave doubles the sweep), then the
-// largest cluster (fewest rows per thread).
+// cheapest step.
 inline const ClusterCfg& pick_cluster(const std::vector<ClusterCfg>& c, int U) {
   size_t best = 0;
   long best_w = -1;
+  double best_c = 0.0;
   for (size_t i = 0; i < c.size(); ++i) {
     const long w = (U + c[i].maxc - 1) / c[i].maxc;
-    if (best_w < 0 || w < best_w) { best = i; best_w = w; }
+    const double k = cluster_cost(c[i]);
+    if (best_w < 0 || w < best_w || (w == best_w && k < best_c)) {
+      best = i;
+      best_w = w;
+      best_c = k;
+    }
   }
   return c[best];
 }

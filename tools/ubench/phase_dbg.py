@@ -12,6 +12,6 @@ so = _lib.lib()
 buf = (ctypes.c_ulonglong * 256)()
 eng.forward(); so.dufwi_debug_counters(buf, 256)
 obs = eng.forward().double(); so.dufwi_debug_counters(buf, 256)
-print("warp: sync, wait, compute+common-stores, special (cycles per step)")
+print("warp: [sync+wait, compute, fast steps/1000] cycles per step, loop cycles per step")
 for w in range(15):
     print(w, [round(buf[w * 4 + k] / 1000.0) for k in range(4)], "loop", round(buf[128 + w] / 1000.0))
