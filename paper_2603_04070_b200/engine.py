@@ -37,6 +37,14 @@ class NonFiniteResult(FloatingPointError):
     """Raised by the engine when a sweep produced non-finite values."""
 
 
+def raise_nonfinite(flags) -> None:
+    """Raise for host-side flags [traces, gradient] (adjoint.py:75-91 semantics)."""
+    if int(flags[0]):
+        raise NonFiniteResult("simulation diverged: non-finite receiver samples")
+    if int(flags[1]):
+        raise NonFiniteResult("gradient blow-up: non-finite accumulated gradient")
+
+
 def shard_range(n_units: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous block of units for ``rank`` (SURVEY §8(e) partitioning)."""
     base, extra = divmod(n_units, world)
@@ -231,6 +239,9 @@ class PhysicsEngine:
     def chunk_units(self, mode: int, n: int) -> int:
         if self.max_chunk_units:
             return max(1, min(n, self.max_chunk_units))
+        ws = self._ws.get(mode)
+        if ws is not None and ws.buf.numel() >= self._ws_bytes(mode, n):
+            return n  # the held workspace already fits: no device query on the hot path
         free, _ = torch.cuda.mem_get_info(self.device)
         held = sum(w.buf.numel() for w in self._ws.values())
         budget = (free + held) * self.memory_fraction
@@ -343,15 +354,16 @@ class PhysicsEngine:
                                                int(guard_radius), _ptr(grad),
                                                _ptr(self._flag[1:]), st))
         if check_finite:
-            flags = self._flag.cpu()
-            if int(flags[0]):
-                raise NonFiniteResult("simulation diverged: non-finite receiver samples")
-            if int(flags[1]):
-                raise NonFiniteResult("gradient blow-up: non-finite accumulated gradient")
+            raise_nonfinite(self._flag.cpu())
         misfit = self._misfit.clone()
         if return_traces:
             return misfit, grad, traces
         return misfit, grad
+
+    def last_flags(self) -> torch.Tensor:
+        """Device copy of the last call's non-finite flags [traces, gradient] (no sync);
+        pass to :func:`raise_nonfinite` after a host sync to check deferred results."""
+        return self._flag[:2].clone()
 
     # ------------------------------------------------------------ timing
     def time_sweeps(self, obs: torch.Tensor, reps: int = 3, mask: bool = True,

@@ -69,16 +69,23 @@ class Reconstructor:
     def reconstruct(self, obs, c0, keep_gradients: bool = False, check_finite: bool = True):
         import torch
 
+        from .engine import raise_nonfinite
+
         lo, hi = self.bounds
         c = torch.clamp(c0.to(torch.float64), lo, hi)
-        maps, grads = [], []
+        maps, grads, flags = [], [], []
         for net in self.nets:
             self.engine.set_model(c, self.rho)
+            # non-finite checks are deferred to one host sync after the last stage,
+            # so the stages queue back to back on the device
             _, g = self.engine.misfit_and_gradient(obs, guard_radius=self.guard_radius,
-                                                   check_finite=check_finite)
+                                                   check_finite=False)
+            flags.append(self.engine.last_flags())
             if hasattr(net, "predict_update_device"):
                 upd = net.predict_update_device(c, g)
             else:  # a host network (e.g. the reference's NumPy CNN): one round trip per stage
+                if check_finite:
+                    raise_nonfinite(flags[-1].cpu())
                 upd = torch.stack([torch.as_tensor(net.predict_update(ci.cpu().numpy(),
                                                                       gi.cpu().numpy()))
                                    for ci, gi in zip(c, g)]).to(c.device)
@@ -86,6 +93,9 @@ class Reconstructor:
             maps.append(c)
             if keep_gradients:
                 grads.append(g)
+        if check_finite:
+            for f in torch.stack(flags).cpu():  # first failing stage raises
+                raise_nonfinite(f)
         return (maps, grads) if keep_gradients else maps
 
 

@@ -75,3 +75,16 @@ def test_unfold_infer_public_api(gpu):
     maps = rec.reconstruct(torch.as_tensor(obs.traces).to(gpu),
                            torch.full((1,) + grid.shape, 1540.0, dtype=torch.float64, device=gpu))
     assert np.array_equal(maps[-1][0].cpu().numpy(), out[-1].values)
+
+
+def test_unfold_infer_nonfinite_raises(gpu):
+    """Deferred non-finite checks still surface as the reference's NumericError."""
+    from ._cases import ring48
+
+    z, grid, geom, pulse, damp = ring48()
+    obs = pk.ChannelData(z["obs"], geom, grid.dt)
+    big = pk.SourcePulse(np.full(grid.nt, 1e300), grid.dt, 2e5)
+    nets = make_update_nets(2, seed=1, device=gpu)
+    setup = pk.InversionSetup(big, damp, pk.cfl_safe_bounds(grid, (1300.0, 3200.0)))
+    with pytest.raises(pk.NumericError):
+        pk.unfold_infer(obs, pk.homogeneous_map(grid, 1540.0), nets, setup)
