@@ -647,7 +647,7 @@ extern "C" int32_t dufwi_plan_info(const dufwi_plan_t* p, int64_t* out, int32_t 
 extern "C" int dufwi_debug_counters(unsigned long long* out, int n) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * (n < 256 ? n : 256));
-  unsigned long long z[256] = {0};
+  unsigned long long z[256] = {0};  // g_dbg holds 256 counters
   cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
   return 0;
 }

@@ -38,7 +38,17 @@ namespace dufwi {
 
 namespace cg = cooperative_groups;
 #ifdef DUFWI_EXP_TIMING
-__device__ unsigned long long g_dbg[256];
+// per-warp step timing of CTA ranks 0 and 4 of cluster 0: [sweep][cta][warp][sync, body, path]
+__device__ unsigned long long g_dbg[2 * 2 * 16 * 4];
+__device__ __forceinline__ void dbg_step(int sweep, long long T0, long long T1, int path) {
+  if ((blockIdx.x == 0 || blockIdx.x == 4) && (threadIdx.x & 31) == 0) {
+    const int w = threadIdx.x >> 5;
+    unsigned long long* d = g_dbg + ((sweep * 2 + (blockIdx.x ? 1 : 0)) * 16 + w) * 4;
+    atomicAdd(d + 0, (unsigned long long)(T1 - T0));
+    atomicAdd(d + 1, (unsigned long long)(clock64() - T1));
+    atomicAdd(d + 2, (unsigned long long)path);
+  }
+}
 #endif
 
 struct ClusterCfg {
@@ -149,11 +159,14 @@ __host__ __device__ inline size_t bar_offset(int rows, int rpt, int nz, int nbuf
   return ab_offset<T>(rows, rpt, nz, nbufs) + (size_t)ab_col_stride(rows, rpt) * nz * sizeof(double2);
 }
 // IO stage after the mbarriers: [n_rec, n_ring, pad] [rec_g[maxrec]] [ring_g[maxring]]
-// [double stage_rec[kStage][maxrec]] [float stage_ring[kStage][maxring]]
+// [rec_b[maxrec]] [ring_b[maxring]] [double stage_rec[kStage][maxrec]]
+// [float stage_ring[kStage][maxring]].  *_g: HBM slot, *_b: exchange-buffer index.
 struct IoStage {
   int* counts;
   int* rec_g;
   int* ring_g;
+  int* rec_b;
+  int* ring_b;
   double* srec;
   float* sring;
   int maxrec, maxring;
@@ -167,7 +180,7 @@ __host__ __device__ inline size_t io_offset(int rows, int rpt, int nz, int nbufs
 }
 
 __host__ __device__ inline size_t io_bytes(int maxrec, int maxring) {
-  return 16 + al16((size_t)maxrec * 4) + al16((size_t)maxring * 4) +
+  return 16 + 2 * al16((size_t)maxrec * 4) + 2 * al16((size_t)maxring * 4) +
          al16((size_t)kStage * maxrec * 8) + al16((size_t)kStage * maxring * 4);
 }
 
@@ -184,6 +197,10 @@ __device__ __forceinline__ IoStage io_stage(unsigned char* base, int maxrec, int
   io.rec_g = reinterpret_cast<int*>(base + o);
   o += al16((size_t)maxrec * 4);
   io.ring_g = reinterpret_cast<int*>(base + o);
+  o += al16((size_t)maxring * 4);
+  io.rec_b = reinterpret_cast<int*>(base + o);
+  o += al16((size_t)maxrec * 4);
+  io.ring_b = reinterpret_cast<int*>(base + o);
   o += al16((size_t)maxring * 4);
   io.srec = reinterpret_cast<double*>(base + o);
   o += al16((size_t)kStage * maxrec * 8);
@@ -227,6 +244,7 @@ struct CellCtx {
   int seg, zi, z, lrow0;       // thread: column z (= order[zi]), local rows lrow0 ..
   int RS;                      // exchange column stride
   int xo;                      // buffer offset of the thread's first cell
+  uint32_t off_up, off_dn;     // byte offsets of this column's halo cells in a buffer
   bool has_up, has_dn;         // CTA rank-1 / rank+1 exist with rows
   uint32_t lbase, rup, rdn;    // shared-window base: own, rank-1, rank+1
 };
@@ -274,6 +292,7 @@ __device__ __forceinline__ bool in_box(const Geo& g, int x, int z) {
 // source cell first, plain columns after, so whole warps of plain columns run
 // the fast step.  Sets c.z / c.xo.  scratch: 2 * nz ints of shared memory
 // (the exchange buffers, before they are zeroed).
+template <class T>
 __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx, int txz,
                                               int* scratch) {
   const int nz = g.nz;
@@ -300,6 +319,8 @@ __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx,
   __syncthreads();
   c.z = order[c.zi];
   c.xo = (c.z + 1) * c.RS + c.lrow0 + 1;
+  c.off_dn = (uint32_t)((c.z + 1) * c.RS) * (uint32_t)sizeof(T);        // top halo of rank+1
+  c.off_up = c.off_dn + (uint32_t)(c.rows + 1) * (uint32_t)sizeof(T);  // bottom halo of rank-1
   __syncthreads();  // scratch is reused as exchange buffer afterwards
 }
 
@@ -307,8 +328,10 @@ __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx,
 template <int RPT>
 struct CellStatic {
   double ed[RPT];
-  int rl[RPT];  // receiver cell: local index into the IO stage, else -1
-  int gl[RPT];  // ring cell: local index into the IO stage, else -1
+  // receiver / ring rows (bit j = row j) and their first IO-stage index: row j's
+  // entry is base + popc(mask below j) (a thread's entries are contiguous)
+  unsigned rmask, gmask;
+  int rbase, gbase;
   unsigned active, src, interior;
   bool pushes_up, pushes_dn;  // owns the slab's first / last row
   unsigned dn_mask;           // bit j set: register j holds the slab's last row (pushes_dn)
@@ -329,12 +352,11 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
   st.pushes_up = c.has_up && c.lrow0 == 0;
   st.pushes_dn = false;
   st.dn_mask = 0u;
+  st.rmask = st.gmask = 0u;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const int lr = c.lrow0 + j;
     st.ed[j] = 0.0;
-    st.rl[j] = -1;
-    st.gl[j] = -1;
     if (lr < c.nr) {
       const int x = c.r0 + lr;
       st.active |= 1u << j;
@@ -342,16 +364,8 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
       double A, B;
       ab_coeffs(damping_at(g, x, c.z), g.dt, A, B);
       const_cast<double2*>(st.ab)[j] = make_double2(A, B);
-      const int slot = g.row_flag[x] ? g.node_slot[(size_t)x * g.nz + c.z] : -1;
-      if (slot >= 0) {
-        st.rl[j] = atomicAdd(&io.counts[0], 1);  // storage slot only: order does not matter
-        io.rec_g[st.rl[j]] = slot;
-      }
-      const int ring = ring_index(g, x, c.z);
-      if (ring >= 0 && io.maxring > 0) {
-        st.gl[j] = atomicAdd(&io.counts[1], 1);
-        io.ring_g[st.gl[j]] = ring;
-      }
+      if (g.row_flag[x] && g.node_slot[(size_t)x * g.nz + c.z] >= 0) st.rmask |= 1u << j;
+      if (io.maxring > 0 && ring_index(g, x, c.z) >= 0) st.gmask |= 1u << j;
       if (x == txx && c.z == txz) st.src |= 1u << j;
       if (in_box(g, x, c.z)) st.interior |= 1u << j;
       if (lr == c.nr - 1 && c.has_dn) {
@@ -360,13 +374,27 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
       }
     }
   }
+  // IO-stage entries (storage slots only: their order does not matter)
+  st.rbase = st.rmask ? atomicAdd(&io.counts[0], __popc(st.rmask)) : 0;
+  st.gbase = st.gmask ? atomicAdd(&io.counts[1], __popc(st.gmask)) : 0;
+  for (int j = 0, n = 0; j < RPT; ++j)
+    if (st.rmask & (1u << j)) {
+      const int x = c.r0 + c.lrow0 + j;
+      io.rec_g[st.rbase + n] = g.node_slot[(size_t)x * g.nz + c.z];
+      io.rec_b[st.rbase + n] = c.xo + j;
+      ++n;
+    }
+  for (int j = 0, n = 0; j < RPT; ++j)
+    if (st.gmask & (1u << j)) {
+      io.ring_g[st.gbase + n] = ring_index(g, c.r0 + c.lrow0 + j, c.z);
+      io.ring_b[st.gbase + n] = c.xo + j;
+      ++n;
+    }
   st.undamped = true;
 #pragma unroll
   for (int j = 0; j < RPT; ++j)
     if (c.lrow0 + j < c.nr && damping_at(g, c.r0 + c.lrow0 + j, c.z) != 0.0) st.undamped = false;
-  bool any = st.src != 0u;
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) any = any || st.rl[j] >= 0 || st.gl[j] >= 0;
+  const bool any = st.src != 0u || st.rmask != 0u || st.gmask != 0u;
   st.special = any;
   const unsigned full = (1u << RPT) - 1u;
   const bool f = allow_fast && st.active == full && st.interior == full && st.undamped && !any;
@@ -379,20 +407,15 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
 // their mbarrier): the slab's first row -> bottom halo of rank-1, last row ->
 // top halo of rank+1.  A CTA's shared memory is one contiguous range of the
 // cluster window, so remote addresses are the mapped base plus the offset.
-template <class T>
-__device__ __forceinline__ uint32_t remote(const CellCtx& c, uint32_t rbase, const T* local) {
-  return rbase + (smem_addr(local) - c.lbase);
-}
-
+// xb: byte offset of the written buffer from the CTA's shared-memory base
+// (uniform), bb: same for the mbarrier completing the step.
 template <int RPT, class T>
-__device__ __forceinline__ void push_edges(const CellCtx& c, const CellStatic<RPT>& s, T* X,
-                                           const double (&v)[RPT], uint32_t bar_w, bool full) {
-  const T* col = X + (c.z + 1) * c.RS;
-  if (s.pushes_up)
-    push_async(remote(c, c.rup, col + c.rows + 1), (T)v[0], c.rup + (bar_w - c.lbase));
+__device__ __forceinline__ void push_edges(const CellCtx& c, const CellStatic<RPT>& s, uint32_t xb,
+                                           uint32_t bb, const double (&v)[RPT], bool full) {
+  if (s.pushes_up) push_async(c.rup + xb + c.off_up, (T)v[0], c.rup + bb);
   if (s.pushes_dn) {
-    const uint32_t ra = remote(c, c.rdn, col);
-    const uint32_t rb = c.rdn + (bar_w - c.lbase);
+    const uint32_t ra = c.rdn + xb + c.off_dn;
+    const uint32_t rb = c.rdn + bb;
     if (full) {  // every slot active: the slab's last row is register RPT-1
       push_async(ra, (T)v[RPT - 1], rb);
     } else {
@@ -404,25 +427,36 @@ __device__ __forceinline__ void push_edges(const CellCtx& c, const CellStatic<RP
 }
 
 // ---------------------------------------------------------------------------
-// forward step t.  u1 = u[t-1] (read), u2 = u[t-2] -> u[t].  Reads exchange
-// buffer Xr (step t-1), writes Xw (step t).
+// Step synchronisation: the CTA's exchange cells of step i-1 are complete and
+// the buffer written at step i is free again (__syncthreads); the neighbours'
+// halo rows of step i-1 have landed (mbarrier phase of bar_r); bar_w is armed
+// for the bytes the neighbours push during step i.
 __device__ __forceinline__ void step_sync(const CellCtx& c, int i, uint32_t bar_r, uint32_t bar_w,
                                           uint32_t tx_bytes) {
-  __syncthreads();  // exchange rows of step i-1 complete; Xw free for reuse
+  __syncthreads();
   if (i >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((i - 1) >> 1) & 1);
   if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
 }
 
-// One forward step of a thread's cells.  FULL: every row slot active (no
-// per-row predicates); PLAIN: undamped, no receiver / ring / source cell
-// (A = 2, B = -1, no IO).  Both are warp-uniform, chosen once per sweep.
+// Buffers of a step: the one read (r) and the one written (w), as pointers and
+// as byte offsets from the shared-memory base (for the DSMEM pushes).
+template <class T>
+struct StepBufs {
+  const T* r;
+  T* w;
+  uint32_t wb, bar_r, bar_w, bar_wb;
+};
+
+// One forward step of a thread's cells (u1 = u[t-1] -> u2 := u[t]).  FULL:
+// every row slot active (no per-row predicates); PLAIN: undamped and no
+// source (A = 2, B = -1).  Both are warp-uniform, chosen once per sweep.
+// Receiver / ring samples are gathered from the exchange buffer by io_gather.
 template <int RPT, class T, int MODE, bool FULL, bool PLAIN>
 __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&u1)[RPT], double (&u2)[RPT], int t, int U,
-                                         int lu, const T* Xr, T* Xw, uint32_t bar_w,
-                                         double pulse_t, const IoStage& io,
+                                         int lu, const StepBufs<T>& B, double pulse_t,
                                          float* __restrict__ hist, size_t N2) {
-  const T* pc = Xr + c.xo;
+  const T* pc = B.r + c.xo;
   const T* pm = pc - c.RS;
   const T* pp = pc + c.RS;
   double v[RPT];
@@ -444,24 +478,30 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
     for (int j = 0; j < RPT; ++j)
       if (s.src & (1u << j)) v[j] = __dadd_rn(v[j], pulse_t);
   }
-  T* q = Xw + c.xo;
+  T* q = B.w + c.xo;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     if (!FULL && !(s.active & (1u << j))) continue;
     u2[j] = v[j];
     q[j] = (T)v[j];
+    if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = (float)v[j];
   }
-  push_edges<RPT, T>(c, s, Xw, v, bar_w, FULL);
-  if (PLAIN || (!s.special && MODE != 1)) return;
-  // receivers, history / ring strips
+  push_edges<RPT, T>(c, s, B.wb, B.bar_wb, v, FULL);
+}
+
+// Receiver samples / ring cells of step t, read back from the exchange buffer
+// written at step t (complete after the following __syncthreads) into stage
+// slot t % kStage: one cell per thread, no per-row branches in the step bodies.
+template <class T, int MODE>
+__device__ __forceinline__ void io_gather(const IoStage& io, int nrec, int nio, const T* X, int t) {
   const int k = t % kStage;
-#pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    if (!FULL && !(s.active & (1u << j))) continue;
-    const float vf = (float)v[j];
-    if (s.rl[j] >= 0) io.srec[k * io.maxrec + s.rl[j]] = (double)vf;
-    if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = vf;
-    if (MODE == 2 && s.gl[j] >= 0) io.sring[k * io.maxring + s.gl[j]] = vf;
+  for (int i = threadIdx.x; i < nio; i += blockDim.x) {
+    if (i < nrec) {
+      io.srec[k * io.maxrec + i] = (double)(float)X[io.rec_b[i]];
+    } else if (MODE == 2) {
+      const int r = i - nrec;
+      io.sring[k * io.maxring + r] = (float)X[io.ring_b[r]];
+    }
   }
 }
 
@@ -487,29 +527,29 @@ __device__ __forceinline__ void flush_stage(const Geo& g, const IoStage& io, int
 template <int RPT, class T, int MODE>
 __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&u1)[RPT], double (&u2)[RPT], int t, int U,
-                                         int lu, const T* Xr, T* Xw, uint32_t bar_r,
-                                         uint32_t bar_w, uint32_t tx_bytes, double pulse_t,
-                                         const IoStage& io, float* __restrict__ hist, size_t N2) {
+                                         int lu, const StepBufs<T>& B, uint32_t tx_bytes,
+                                         double pulse_t, const IoStage& io, int nrec, int nio,
+                                         float* __restrict__ rec, float* __restrict__ strips,
+                                         float* __restrict__ hist, size_t N2) {
 #ifdef DUFWI_EXP_TIMING
   const long long T0 = clock64();
 #endif
-  step_sync(c, t, bar_r, bar_w, tx_bytes);
+  step_sync(c, t, B.bar_r, B.bar_w, tx_bytes);
+  if (t >= 1) {
+    io_gather<T, MODE>(io, nrec, nio, B.r, t - 1);
+    if (t % kStage == 0) flush_stage<MODE>(g, io, t - kStage, kStage, U, lu, rec, strips);
+  }
 #ifdef DUFWI_EXP_TIMING
   const long long T1 = clock64();
 #endif
   if (s.fast)
-    fwd_body<RPT, T, MODE, true, true>(g, c, s, u1, u2, t, U, lu, Xr, Xw, bar_w, pulse_t, io, hist, N2);
+    fwd_body<RPT, T, MODE, true, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else if (s.full)
-    fwd_body<RPT, T, MODE, true, false>(g, c, s, u1, u2, t, U, lu, Xr, Xw, bar_w, pulse_t, io, hist, N2);
+    fwd_body<RPT, T, MODE, true, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else
-    fwd_body<RPT, T, MODE, false, false>(g, c, s, u1, u2, t, U, lu, Xr, Xw, bar_w, pulse_t, io, hist, N2);
+    fwd_body<RPT, T, MODE, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
 #ifdef DUFWI_EXP_TIMING
-  if (blockIdx.x == 5 && (threadIdx.x & 31) == 0) {
-    const int w = threadIdx.x >> 5;
-    atomicAdd(&g_dbg[w * 4 + 0], (unsigned long long)(T1 - T0));
-    atomicAdd(&g_dbg[w * 4 + 1], (unsigned long long)(clock64() - T1));
-    atomicAdd(&g_dbg[w * 4 + 2], s.fast ? 1ull : 0ull);
-  }
+  dbg_step(0, T0, T1, s.fast ? 0 : s.full ? 1 : 2);
 #endif
 }
 
@@ -529,9 +569,10 @@ __global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
   const size_t pb = (size_t)b * N2;
   const size_t xe = xbuf_elems(rows, RPT, g.nz);
   T* X[2] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem) + xe};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, RPT, g.nz, 2));
+  const uint32_t bar_off = (uint32_t)bar_offset<T>(rows, RPT, g.nz, 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
-  order_columns(g, c, txx, txz, reinterpret_cast<int*>(smem));
+  order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem));
   for (size_t i = threadIdx.x; i < 2 * xe; i += blockDim.x) X[0][i] = T(0);
   const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 2), maxrec, maxring);
   if (threadIdx.x == 0) {
@@ -543,7 +584,8 @@ __global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
   __syncthreads();
   CellStatic<RPT> st;
   load_static<RPT>(g, m, c, pb, txx, txz,
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)), io,
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)),
+                   io,
                    MODE != 1, st);
   const uint32_t tx_bytes =
       (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T);
@@ -552,35 +594,35 @@ __global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
   for (int j = 0; j < RPT; ++j) ua[j] = ub[j] = 0.0;
   const bool owns_src = st.src != 0u;
   double p_next = owns_src ? g.pulse[0] : 0.0;
-  cluster_sync_all();  // barriers initialised and buffers zeroed cluster-wide
+  cluster_sync_all();  // barriers initialised, buffers zeroed, IO lists complete cluster-wide
+  const int nrec = io.counts[0];
+  const int nio = nrec + (MODE == 2 ? io.counts[1] : 0);
 
   // step t writes X[t & 1] / bar[t & 1]; ub receives u[t] at even t, ua at odd t
-#ifdef DUFWI_EXP_TIMING
-  const long long TL0 = clock64();
-#endif
+  const uint32_t xb1 = (uint32_t)(xe * sizeof(T));
+  const StepBufs<T> B0{X[1], X[0], 0u, bar[1], bar[0], bar_off};
+  const StepBufs<T> B1{X[0], X[1], xb1, bar[0], bar[1], bar_off + 8u};
   int t = 0;
   for (; t + 1 < g.nt; t += 2) {
     double p = p_next;
     if (owns_src) p_next = g.pulse[t + 1];
-    fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, X[1], X[0], bar[1], bar[0], tx_bytes, p,
-                           io, hist, N2);
+    fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p, io, nrec, nio, rec,
+                           strips, hist, N2);
     p = p_next;
     if (owns_src && t + 2 < g.nt) p_next = g.pulse[t + 2];
-    fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, X[0], X[1], bar[0], bar[1], tx_bytes,
-                           p, io, hist, N2);
-    if ((t + 2) % kStage == 0) flush_stage<MODE>(g, io, t + 2 - kStage, kStage, U, lu, rec, strips);
+    fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, B1, tx_bytes, p, io, nrec, nio, rec,
+                           strips, hist, N2);
   }
   if (t < g.nt)
-    fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, X[1], X[0], bar[1], bar[0], tx_bytes,
-                           p_next, io, hist, N2);
-  if (g.nt % kStage) {
-    const int t0 = g.nt - g.nt % kStage;
+    fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p_next, io, nrec, nio, rec,
+                           strips, hist, N2);
+  // the last step's samples, then the partial stage
+  __syncthreads();
+  io_gather<T, MODE>(io, nrec, nio, X[(g.nt - 1) & 1], g.nt - 1);
+  {
+    const int t0 = (g.nt - 1) / kStage * kStage;
     flush_stage<MODE>(g, io, t0, g.nt - t0, U, lu, rec, strips);
   }
-#ifdef DUFWI_EXP_TIMING
-  if (blockIdx.x == 5 && (threadIdx.x & 31) == 0)
-    atomicAdd(&g_dbg[128 + (threadIdx.x >> 5)], (unsigned long long)(clock64() - TL0));
-#endif
   // drain the last step's incoming pushes before any CTA of the cluster exits
   if (c.has_up || c.has_dn) mbar_wait(bar[(g.nt - 1) & 1], ((g.nt - 1) >> 1) & 1);
   cluster_sync_all();
@@ -603,14 +645,24 @@ __global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
 // ---------------------------------------------------------------------------
 // adjoint step i (time t = nt-1-i).  l1 = lam[t+1], l2 = lam[t+2] -> lam[t];
 // ua = u[t] -> u[t-2] (reconstruction, MODE 2), ub = u[t-1].
-// XL: exchange of E*lam, XU: exchange of u (MODE 2).  Buffers/bars indexed by i.
-template <int RPT, class T, int MODE, bool FULL, bool PLAIN>
+// Buffers: XL exchange of E*lam, XU exchange of u (MODE 2), indexed by i.
+// T2: t >= 2 (every step but the last two: imaging and reconstruction run).
+template <class T>
+struct AdjBufs {
+  const T* lr;
+  T* lw;
+  const T* ur;
+  T* uw;
+  uint32_t lwb, uwb, bar_r, bar_w, bar_wb;
+};
+
+template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool T2>
 __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
                                          double (&ub)[RPT], double (&acc)[RPT], int i, int U,
-                                         int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
-                                         uint32_t bar_w, double pulse_t, const IoStage& io,
-                                         const float* __restrict__ hist, size_t N2) {
+                                         int lu, const AdjBufs<T>& B, double pulse_t,
+                                         const IoStage& io, const float* __restrict__ hist,
+                                         size_t N2) {
   const int RS = c.RS, z = c.z;
   const int t = g.nt - 1 - i;
   const int k = i % kStage;
@@ -619,7 +671,7 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
 #pragma unroll
   for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
   {
-    const T* pc = XLr + c.xo;
+    const T* pc = B.lr + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       const double xm = j > 0 ? el[j - 1] : (double)pc[-1];
@@ -637,12 +689,14 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
   if (!PLAIN && s.special) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
-      if (s.rl[j] >= 0) lam[j] = __dadd_rn(lam[j], io.srec[k * io.maxrec + s.rl[j]]);
+      if (s.rmask & (1u << j))
+        lam[j] = __dadd_rn(lam[j], io.srec[k * io.maxrec + s.rbase + __popc(s.rmask & ((1u << j) - 1u))]);
   }
   // imaging with L(u[t-1]) and reconstruction of u[t-2]
+  const bool img = T2 || t >= 1;
   double lapu[RPT];
   if (MODE == 2) {
-    const T* pc = XUr + c.xo;
+    const T* pc = B.ur + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       const double xm = j > 0 ? ub[j - 1] : (double)pc[-1];
@@ -654,7 +708,7 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       lapu[j] = 0.0;
-      if (t >= 1 && (FULL || (s.active & (1u << j)))) {
+      if (img && (FULL || (s.active & (1u << j)))) {
         const float* F = hist + ((size_t)(t - 1) * U + lu) * N2;
         const int x = c.r0 + c.lrow0 + j;
         const size_t cell = (size_t)x * g.nz + z;
@@ -666,8 +720,8 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
       }
     }
   }
-  T* ql = XLw + c.xo;
-  T* qu = XUw + c.xo;
+  T* ql = B.lw + c.xo;
+  T* qu = B.uw + c.xo;
   double elw[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
@@ -675,25 +729,25 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
     if (!FULL && !(s.active & (1u << j))) continue;
     l2[j] = lam[j];
     ql[j] = (T)elw[j];
-    if (t >= 1) {
+    if (img) {
       if (MODE == 1) {
         acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
       } else if (PLAIN || (s.interior & (1u << j))) {
         acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
-        if (t >= 2) {
+        if (T2 || t >= 2) {
           double prev = recon(ub[j], ua[j], s.ed[j], lapu[j]);
           if (!PLAIN && (s.src & (1u << j))) prev = __dadd_rn(prev, pulse_t);
           ua[j] = prev;
         }
-      } else if (s.gl[j] >= 0 && t >= 2) {
+      } else if ((s.gmask & (1u << j)) && (T2 || t >= 2)) {
         // ring cell: the saved strip stands in for the reconstruction
-        ua[j] = (double)io.sring[k * io.maxring + s.gl[j]];
+        ua[j] = (double)io.sring[k * io.maxring + s.gbase + __popc(s.gmask & ((1u << j) - 1u))];
       }
     }
     if (MODE == 2) qu[j] = (T)ua[j];
   }
-  push_edges<RPT, T>(c, s, XLw, elw, bar_w, FULL);
-  if (MODE == 2) push_edges<RPT, T>(c, s, XUw, ua, bar_w, FULL);
+  push_edges<RPT, T>(c, s, B.lwb, B.bar_wb, elw, FULL);
+  if (MODE == 2) push_edges<RPT, T>(c, s, B.uwb, B.bar_wb, ua, FULL);
 }
 
 // Load residuals of steps [i0, i0+kStage) (t = nt-1-i) and the ring strips they
@@ -719,24 +773,32 @@ __device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, 
   }
 }
 
-template <int RPT, class T, int MODE>
+template <int RPT, class T, int MODE, bool T2>
 __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
                                          double (&ub)[RPT], double (&acc)[RPT], int i, int U,
-                                         int lu, const T* XLr, T* XLw, const T* XUr, T* XUw,
-                                         uint32_t bar_r, uint32_t bar_w, uint32_t tx_bytes,
+                                         int lu, const AdjBufs<T>& B, uint32_t tx_bytes,
                                          double pulse_t, const IoStage& io,
                                          const float* __restrict__ hist, size_t N2) {
-  step_sync(c, i, bar_r, bar_w, tx_bytes);
+#ifdef DUFWI_EXP_TIMING
+  const long long T0 = clock64();
+#endif
+  step_sync(c, i, B.bar_r, B.bar_w, tx_bytes);
+#ifdef DUFWI_EXP_TIMING
+  const long long T1 = clock64();
+#endif
   if (MODE == 2 && s.fast)
-    adj_body<RPT, T, MODE, true, true>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, XLr, XLw, XUr, XUw,
-                                       bar_w, pulse_t, io, hist, N2);
+    adj_body<RPT, T, MODE, true, true, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B, pulse_t, io,
+                                           hist, N2);
   else if (s.full)
-    adj_body<RPT, T, MODE, true, false>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, XLr, XLw, XUr,
-                                        XUw, bar_w, pulse_t, io, hist, N2);
+    adj_body<RPT, T, MODE, true, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B, pulse_t, io,
+                                            hist, N2);
   else
-    adj_body<RPT, T, MODE, false, false>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, XLr, XLw, XUr,
-                                         XUw, bar_w, pulse_t, io, hist, N2);
+    adj_body<RPT, T, MODE, false, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B, pulse_t,
+                                             io, hist, N2);
+#ifdef DUFWI_EXP_TIMING
+  dbg_step(1, T0, T1, (MODE == 2 && s.fast) ? 0 : s.full ? 1 : 2);
+#endif
 }
 
 template <int RPT, class T, int MODE>
@@ -760,9 +822,10 @@ __global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
   T* base = reinterpret_cast<T*>(smem);
   T* XL[2] = {base, base + xe};
   T* XU[2] = {base + 2 * xe, base + 3 * xe};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_offset<T>(rows, RPT, g.nz, 4));
+  const uint32_t bar_off = (uint32_t)bar_offset<T>(rows, RPT, g.nz, 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
-  order_columns(g, c, txx, txz, reinterpret_cast<int*>(smem));
+  order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem));
   for (size_t k = threadIdx.x; k < 4 * xe; k += blockDim.x) base[k] = T(0);
   const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 4), maxrec, maxring);
   if (threadIdx.x == 0) {
@@ -774,7 +837,8 @@ __global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
   __syncthreads();
   CellStatic<RPT> st;
   load_static<RPT>(g, m, c, pb, txx, txz,
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 4)), io,
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 4)),
+                   io,
                    MODE == 2, st);
   const int per = MODE == 2 ? 2 : 1;
   const uint32_t tx_bytes =
@@ -807,20 +871,29 @@ __global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
   cluster_sync_all();
 
   // step i writes XL[i&1], XU[i&1], bar[i&1]; reads XL[(i+1)&1], XU[(i+1)&1], bar[(i+1)&1]
+  const uint32_t xsz = (uint32_t)(xe * sizeof(T));
+  const AdjBufs<T> B0{XL[1], XL[0], XU[1], XU[0], 0u, 2 * xsz, bar[1], bar[0], bar_off};
+  const AdjBufs<T> B1{XL[0], XL[1], XU[0], XU[1], xsz, 3 * xsz, bar[0], bar[1], bar_off + 8u};
+  // steps with t >= 2 (i <= nt - 3) in pairs, then the tail
   int i = 0;
-  for (; i + 1 < nt; i += 2) {
+  for (; i + 1 < nt - 2; i += 2) {
     if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
     const double p0 = owns_src ? g.pulse[nt - 1 - i] : 0.0;
-    adj_step<RPT, T, MODE>(g, c, st, la, lb, ua, ub, acc, i, U, lu, XL[1], XL[0], XU[1], XU[0],
-                           bar[1], bar[0], tx_bytes, p0, io, hist, N2);
+    adj_step<RPT, T, MODE, true>(g, c, st, la, lb, ua, ub, acc, i, U, lu, B0, tx_bytes, p0, io,
+                                 hist, N2);
     const double p1 = owns_src ? g.pulse[nt - 2 - i] : 0.0;
-    adj_step<RPT, T, MODE>(g, c, st, lb, la, ub, ua, acc, i + 1, U, lu, XL[0], XL[1], XU[0], XU[1],
-                           bar[0], bar[1], tx_bytes, p1, io, hist, N2);
+    adj_step<RPT, T, MODE, true>(g, c, st, lb, la, ub, ua, acc, i + 1, U, lu, B1, tx_bytes, p1, io,
+                                 hist, N2);
   }
-  if (i < nt) {
+  for (; i < nt; ++i) {
     if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
-    adj_step<RPT, T, MODE>(g, c, st, la, lb, ua, ub, acc, i, U, lu, XL[1], XL[0], XU[1], XU[0],
-                           bar[1], bar[0], tx_bytes, owns_src ? g.pulse[0] : 0.0, io, hist, N2);
+    const double p = owns_src ? g.pulse[nt - 1 - i] : 0.0;
+    if (i & 1)
+      adj_step<RPT, T, MODE, false>(g, c, st, lb, la, ub, ua, acc, i, U, lu, B1, tx_bytes, p, io,
+                                    hist, N2);
+    else
+      adj_step<RPT, T, MODE, false>(g, c, st, la, lb, ua, ub, acc, i, U, lu, B0, tx_bytes, p, io,
+                                    hist, N2);
   }
   if (c.has_up || c.has_dn) mbar_wait(bar[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
   cluster_sync_all();

@@ -1,17 +1,37 @@
-import ctypes, os, sys
+"""Per-warp step timing of the cluster sweeps (library built with -DDUFWI_EXP_TIMING):
+CTA rank 0 (x damping band) and rank 4 (interior) of the first cluster."""
+import ctypes
+import os
+import sys
+
 sys.path.insert(0, os.getcwd())
 os.environ["DUFWI_LIB"] = os.path.abspath("tools/ubench/lib_TIMING.so")
-import torch, numpy as np
-import bench
-from paper_2603_04070_b200 import forward as fwd, _lib
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2603_04070_b200 import _lib, forward as fwd  # noqa: E402
+
 torch.cuda.set_device(0)
 wl, grid, geom, pulse, damp, bounds = bench.build_problem(1, 1, 0)
-eng = fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes, pulse.samples, damp, engine="cluster")
+eng = fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes, pulse.samples,
+                     damp, engine="cluster")
+print(eng.info())
 eng.set_model(wl.c_true)
+obs = eng.forward().double()
 so = _lib.lib()
 buf = (ctypes.c_ulonglong * 256)()
-eng.forward(); so.dufwi_debug_counters(buf, 256)
-obs = eng.forward().double(); so.dufwi_debug_counters(buf, 256)
-print("warp: [sync+wait, compute, fast steps/1000] cycles per step, loop cycles per step")
-for w in range(15):
-    print(w, [round(buf[w * 4 + k] / 1000.0) for k in range(4)], "loop", round(buf[128 + w] / 1000.0))
+eng.misfit_and_gradient(obs)
+so.dufwi_debug_counters(buf, 256)
+eng.misfit_and_gradient(obs)
+so.dufwi_debug_counters(buf, 256)
+nt = grid.nt
+paths = {0: "plain", 1: "full", 2: "generic"}
+for sweep in (0, 1):
+    print(["forward", "adjoint"][sweep], "cycles per step: [sync+wait, body] path")
+    for cta in (0, 1):
+        row = []
+        for w in range(15):
+            d = ((sweep * 2 + cta) * 16 + w) * 4
+            p = round(buf[d + 2] / nt)
+            row.append(f"{buf[d] // nt}/{buf[d + 1] // nt}{paths.get(p, '?')[0]}")
+        print("  cta", [0, 4][cta], " ".join(row))
