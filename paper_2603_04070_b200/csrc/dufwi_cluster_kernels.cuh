@@ -73,7 +73,14 @@ constexpr int kStage = 16;
 // Threads per CTA the sweep kernels are compiled for: the register budget per
 // thread (65536 / threads) must hold RPT rows of f64 state (6 per row in the
 // adjoint) without spilling.
-__host__ __device__ constexpr int cluster_max_threads(int rpt) { return rpt >= 7 ? 384 : 512; }
+__host__ __device__ constexpr int cluster_max_threads(int rpt) {
+  return rpt >= 7 ? 384 : 512;
+}
+// registers per thread for that budget (one CTA per SM, multiples of 8; a warp's
+// registers come from one SM sub-partition, 16384 each, so 15 warps cap at 128)
+__host__ __device__ constexpr int cluster_max_regs(int rpt) {
+  return (65536 / cluster_max_threads(rpt)) / 8 * 8;
+}
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -554,7 +561,7 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
 }
 
 template <int RPT, class T, int MODE>
-__global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
+__global__ void __maxnreg__(cluster_max_regs(RPT))
     cluster_fwd_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
                        int unit_begin, int U, float* __restrict__ rec, float* __restrict__ hist,
                        float* __restrict__ strips, float* __restrict__ ubuf) {
@@ -802,7 +809,7 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
 }
 
 template <int RPT, class T, int MODE>
-__global__ void __launch_bounds__(cluster_max_threads(RPT), 1)
+__global__ void __maxnreg__(cluster_max_regs(RPT))
     cluster_adj_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
                        int unit_begin, int U,
                        const double* __restrict__ rres, const float* __restrict__ hist,
@@ -934,6 +941,22 @@ inline int max_active_clusters(K kernel, int cs, int threads, size_t smem) {
   return n;
 }
 
+// Largest number of ring-strip cells (ring_index >= 0, inside the grid) in any
+// slab of `rows` rows: two ring columns per box row plus the ring rows.
+inline int max_ring_cells(const Geo& g, int rows) {
+  const int zc = (g.z_lo - 1 >= 0 ? 1 : 0) + (g.z_hi + 1 < g.nz ? 1 : 0);
+  int best = 0;
+  for (int r0 = 0; r0 < g.nx; r0 += rows) {
+    const int r1 = std::min(g.nx, r0 + rows);  // [r0, r1)
+    const int box = std::max(0, std::min(r1, g.x_hi + 1) - std::max(r0, g.x_lo));
+    int n = zc * box;
+    if (g.x_lo - 1 >= r0 && g.x_lo - 1 < r1) n += g.Lz;
+    if (g.x_hi + 1 >= r0 && g.x_hi + 1 < r1 && g.x_hi + 1 < g.nx) n += g.Lz;
+    best = std::max(best, n);
+  }
+  return best;
+}
+
 template <int RPT, class T>
 inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
   const int rows = (g.nx + cs - 1) / cs;
@@ -942,7 +965,7 @@ inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
   const int threads = g.nz * nseg;
   if (threads > cluster_max_threads(RPT)) return false;
   const int maxrec = std::min(g.M, rows * g.nz);
-  const int maxring = g.SL > 0 ? std::min(g.SL, 2 * rows + 2 * g.nz) : 0;
+  const int maxring = g.SL > 0 ? max_ring_cells(g, rows) : 0;
   const size_t sf = cluster_smem_bytes<T>(rows, RPT, g.nz, 2, maxrec, maxring);
   const size_t sa = cluster_smem_bytes<T>(rows, RPT, g.nz, 4, maxrec, maxring);
   // clusters co-resident on the device: the least over the sweep kernels
