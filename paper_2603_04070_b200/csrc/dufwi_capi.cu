@@ -580,9 +580,9 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
         const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
         if (warps >= 148L * 32) { vtx = c; break; }
       }
-      const dim3 lgrid((g.nz + 127) / 128, (g.nx + kVecWarps * vtx - 1) / (kVecWarps * vtx), U);
-      adjlam_vec_kernel<<<lgrid, kVecWarps * 32, 0, st>>>(g, m, p->ab, t, unit_begin, vtx, l1, l2o,
-                                                          rres_t, has1, has2);
+      const dim3 lgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
+      adjlam_pipe_kernel<<<lgrid, kPipeWarps * 32, sizeof(AdjRing), st>>>(
+          g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
       LAUNCH_CHECK(p);
       if (do_img) {
         const dim3 igrid((g.nz + 127) / 128,

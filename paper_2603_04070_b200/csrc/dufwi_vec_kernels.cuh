@@ -1,20 +1,20 @@
-// Stepwise engine, vectorised forward step (nz % 4 == 0, constant density).
+// Stepwise engine, vectorised kernels (nz % 4 == 0, constant density).
 //
 // A warp owns a 128-wide z strip — each lane 4 consecutive cells, loaded and
 // stored as one float4 — and walks TX x-rows of ONE shot, keeping rows x-1,
-// x, x+1 in f64 registers (every f32 value converted once).  The next row's
-// loads (u[t-1] row x+2, u[t-2] row x+1, E row x+1) are issued before the
-// current row is computed, so each warp keeps a row of loads in flight while
-// it computes.  z-neighbours come from f64 warp shuffles; the strip's outer
-// neighbours (z0-1, z0+128) are two scalar loads per row (L1/L2 hits).
-// DRAM per cell update: read u[t-1], u[t-2]; write u[t] = 12 B.
+// x, x+1 in f64 registers (every f32 value converted once).  The rows ahead
+// stream through a per-lane cp.async ring of kPipe row slots in shared memory,
+// so every warp keeps kPipe-1 rows of loads in flight while it computes.
+// z-neighbours come from f64 warp shuffles; the strip's outer neighbours
+// (z0-1, z0+128) travel in the same ring.
+// DRAM per cell update: forward read u[t-1], u[t-2], write u[t] = 12 B
+// (E is read once per phantom per step and shared by its shots through L2).
 #pragma once
 
 #include "dufwi_step_kernels.cuh"
 
 namespace dufwi {
 
-constexpr int kVecWarps = 8;  // warps per CTA, stacked along x
 
 struct Row4 {
   double v[4];
@@ -251,20 +251,40 @@ constexpr int kVecAdjTX = 8;
 // ---------------------------------------------------------------------------
 // Split vectorised adjoint (constant density, nz % 4 == 0), kernel 1 of 2:
 // lam[t] = A lam[t+1] + L^T(E lam[t+1]) + B lam[t+2] (+ merged residual at the
-// receiver nodes), in place over lam[t+2].  Same streaming/prefetch structure
-// as fwd_vec_kernel, one shot per warp.  DRAM: 12 B per cell update.
-__global__ void __launch_bounds__(kVecWarps * 32)
-    adjlam_vec_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
-                      const float* __restrict__ l1, float* l2o, const double* __restrict__ rres_t,
-                      int has1, int has2) {
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+// receiver nodes), in place over lam[t+2], one shot per warp.  DRAM: 12 B per
+// cell update (E is shared by the phantom's shots through L2).
+// Pipelined variant of the lam update: the rows of lam[t+1] (+ E, + strip
+// edges) and lam[t+2] stream through a per-lane cp.async ring of kPipe rows,
+// as in fwd_vec_kernel, so each warp keeps kPipe-1 rows of loads in flight.
+struct AdjRing {
+  float4 l1[kPipe][kPipeWarps * 32];      // lam[t+1] row r+1
+  double2 e[kPipe][2][kPipeWarps * 32];   // E row r+1
+  float4 l2[kPipe][kPipeWarps * 32];      // lam[t+2] row r
+  float2 edl[kPipe][kPipeWarps * 32];     // lam[t+1] row r+1 at z0-1 / z0+128
+  double2 ede[kPipe][kPipeWarps * 32];    // E row r+1 at z0-1 / z0+128
+};
+
+__device__ __forceinline__ void cp8(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(ok ? 8 : 0)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kPipeWarps * 32)
+    adjlam_pipe_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
+                       const float* __restrict__ l1, float* l2o, const double* __restrict__ rres_t,
+                       int has1, int has2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  AdjRing& ring = *reinterpret_cast<AdjRing*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
   const int nz = g.nz, nx = g.nx;
   const int z0 = blockIdx.x * 128;
   const int z4 = z0 + 4 * lane;
   const bool act = z4 < nz;
-  const int x0 = (blockIdx.y * kVecWarps + warp) * TX;
-  if (x0 >= nx) return;
+  const int x0 = (blockIdx.y * kPipeWarps + warp) * TX;
+  if (x0 >= nx) return;  // warp-uniform
   const int x1 = min(nx, x0 + TX);
   const int lu = blockIdx.z;
   const int b = (unit_begin + lu) / g.S;
@@ -278,7 +298,28 @@ __global__ void __launch_bounds__(kVecWarps * 32)
     for (int k = 0; k < 4; ++k) lane_damped |= __ldg(T.pz + min(z4 + k, nz - 1)) != 0.0;
   }
   const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
-  // E*lam1 of row x: 4 own cells + the strip's two outer cells
+  const int zc = act ? z4 : 0;
+  const int zl = edge_l ? z0 - 1 : 0, zr = edge_r ? z0 + 128 : 0;
+  const bool has1a = has1 && act, has2a = has2 && act;
+
+  // copies of "row r": lam1 / E row r+1 (+ edges), lam2 row r
+  auto issue = [&](int r) {
+    const int sl = r & (kPipe - 1);
+    const bool okn = r + 1 < nx;
+    const int on = okn ? (r + 1) * nz : 0;
+    const int orr = r * nz;
+    cp16(&ring.l1[sl][tid], L1 + on + zc, has1a && okn);
+    cp16(&ring.e[sl][0][tid], Ed + on + zc, act && okn);
+    cp16(&ring.e[sl][1][tid], Ed + on + zc + 2, act && okn);
+    cp16(&ring.l2[sl][tid], L2 + orr + zc, has2a);
+    float* el = reinterpret_cast<float*>(&ring.edl[sl][tid]);
+    double* ee = reinterpret_cast<double*>(&ring.ede[sl][tid]);
+    cp4(el, L1 + on + zl, has1 && okn && edge_l);
+    cp4(el + 1, L1 + on + zr, has1 && okn && edge_r);
+    cp8(ee, Ed + on + zl, okn && edge_l);
+    cp8(ee + 1, Ed + on + zr, okn && edge_r);
+  };
+  // E*lam1 of row x (4 own cells, strip edges) and raw lam1, loaded directly
   struct ERow {
     double e[4], l[4], el, er;
   };
@@ -302,29 +343,40 @@ __global__ void __launch_bounds__(kVecWarps * 32)
     return r;
   };
   ERow rm = ld(x0 - 1), rc = ld(x0);
-  ERow rn = ld(x0 + 1);
-  float4 p_l2 = (has2 && act) ? *reinterpret_cast<const float4*>(L2 + (size_t)x0 * nz + z4)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < kPipe - 1; ++k) {
+    if (x0 + k < x1) issue(x0 + k);
+    cp_commit();
+  }
   for (int x = x0; x < x1; ++x) {
-    const ERow rp = rn;
-    const float4 c_l2 = p_l2;
-    if (x + 1 < x1) {
-      rn = ld(x + 2);
-      p_l2 = (has2 && act) ? *reinterpret_cast<const float4*>(L2 + (size_t)(x + 1) * nz + z4)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (x + kPipe - 1 < x1) issue(x + kPipe - 1);
+    cp_commit();
+    cp_wait<kPipe - 1>();  // the group of row x has landed
+    const int sl = x & (kPipe - 1);
+    // row x+1 from the ring
+    ERow rp;
+    {
+      const float4 f = ring.l1[sl][tid];
+      const double2 a = ring.e[sl][0][tid], c = ring.e[sl][1][tid];
+      rp.l[0] = f.x; rp.l[1] = f.y; rp.l[2] = f.z; rp.l[3] = f.w;
+      rp.e[0] = a.x * rp.l[0]; rp.e[1] = a.y * rp.l[1]; rp.e[2] = c.x * rp.l[2]; rp.e[3] = c.y * rp.l[3];
+      const float2 fl = ring.edl[sl][tid];
+      const double2 el = ring.ede[sl][tid];
+      rp.el = el.x * (double)fl.x;
+      rp.er = el.y * (double)fl.y;
     }
-    const Row4 w2 = to_d(c_l2);
-    double zl = __shfl_up_sync(0xffffffffu, rc.e[3], 1);
-    double zr = __shfl_down_sync(0xffffffffu, rc.e[0], 1);
-    if (lane == 0) zl = rc.el;
-    if (lane == 31) zr = rc.er;
+    const Row4 w2 = to_d(ring.l2[sl][tid]);
+    double zm0 = __shfl_up_sync(0xffffffffu, rc.e[3], 1);
+    double zp3 = __shfl_down_sync(0xffffffffu, rc.e[0], 1);
+    if (lane == 0) zm0 = rc.el;
+    if (lane == 31) zp3 = rc.er;
     double A[4], B[4];
     ab4(T, x, z4, nz, lane_damped, A, B);
     double lam[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const double zm = k == 0 ? zl : rc.e[k - 1];
-      const double zp = k == 3 ? zr : rc.e[k + 1];
+      const double zm = k == 0 ? zm0 : rc.e[k - 1];
+      const double zp = k == 3 ? zp3 : rc.e[k + 1];
       const double adj = (((-4.0 * rc.e[k] + rm.e[k]) + rp.e[k]) + zm) + zp;
       lam[k] = (A[k] * rc.l[k] + adj) + B[k] * w2.v[k];
     }
@@ -343,6 +395,7 @@ __global__ void __launch_bounds__(kVecWarps * 32)
     rm = rc;
     rc = rp;
   }
+  cp_wait<0>();
 }
 
 // Split vectorised adjoint, kernel 2 of 2: imaging sum_t L(u[t-1]) lam[t] over
@@ -495,5 +548,6 @@ __global__ void __launch_bounds__(kVecAdjWarps * 32)
       for (int k = 0; k < 4; ++k) dst[(size_t)x * nz + z4 + k] += acc[x - xb][4 * lane + k];
   }
 }
+
 
 }  // namespace dufwi
