@@ -42,8 +42,16 @@ def raw(rep):
 
 
 md = [f"# ncu summaries — round {R}\n"]
+traffic = {}
 for rep in sorted(G.glob(f"{R}_*.ncu-rep")):
     for k in raw(rep):
+        if "cluster_adj" in k["kernel"]:
+            def num(v):
+                x, u = v.split()[0], v.split()[-1]
+                return float(x.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+            b = num(k["dram__bytes_read.sum"]) + num(k["dram__bytes_write.sum"])
+            # configs 0 and 1 run the same sweep shape (prof_case.py --config 0)
+            traffic["config0:cluster:adjoint"] = traffic["config1:cluster:adjoint"] = b
         md.append(f"## {rep.name}: `{k['kernel'][:110]}`\n")
         for key in KEYS:
             md.append(f"- {key}: {k[key]}")
@@ -70,4 +78,6 @@ if lf.exists():
     for name, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         md.append(f"| `{name[:70]}` | {n} | {t/1e6:.3f} ms | {t/total:.1%} |")
 (OUT / f"{R}_ncu_summary.md").write_text("\n".join(md) + "\n")
+if traffic:
+    (OUT / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 print("\n".join(md)[:3000])
