@@ -346,6 +346,7 @@ struct CellStatic {
   bool undamped;              // every cell has D == 0: (A, B) = (2, -1), no table reads
   bool fast;                  // whole warp: full, undamped, interior, not special
   bool full;                  // whole warp: every row slot active
+  bool unif;                  // whole warp: full, and one (A, B) per thread for all its rows
   const double2* ab;          // this thread's (A, B) column: ab[j] for row j
 };
 
@@ -408,6 +409,13 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
   // warp-uniform path choice
   st.fast = __all_sync(__activemask(), f);
   st.full = __all_sync(__activemask(), st.active == full);
+  bool same = true;  // one damping value (hence one (A, B)) down the thread's column
+#pragma unroll
+  for (int j = 1; j < RPT; ++j)
+    if (c.lrow0 + j < c.nr &&
+        damping_at(g, c.r0 + c.lrow0 + j, c.z) != damping_at(g, c.r0 + c.lrow0, c.z))
+      same = false;
+  st.unif = __all_sync(__activemask(), st.active == full && same);
 }
 
 // Exchange-row pushes to the neighbouring CTAs (DSMEM st.async completing on
@@ -458,7 +466,7 @@ struct StepBufs {
 // every row slot active (no per-row predicates); PLAIN: undamped and no
 // source (A = 2, B = -1).  Both are warp-uniform, chosen once per sweep.
 // Receiver / ring samples are gathered from the exchange buffer by io_gather.
-template <int RPT, class T, int MODE, bool FULL, bool PLAIN>
+template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF>
 __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&u1)[RPT], double (&u2)[RPT], int t, int U,
                                          int lu, const StepBufs<T>& B, double pulse_t,
@@ -467,6 +475,7 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
   const T* pm = pc - c.RS;
   const T* pp = pc + c.RS;
   double v[RPT];
+  const double2 ab0 = (!PLAIN && UNIF) ? s.ab[0] : make_double2(2.0, -1.0);
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const double xm = j > 0 ? u1[j - 1] : (double)pc[-1];
@@ -476,7 +485,7 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
     if (PLAIN) {
       v[j] = fwd_update_free(u1[j], u2[j], s.ed[j], lap);
     } else {
-      const double2 ab = s.ab[j];
+      const double2 ab = UNIF ? ab0 : s.ab[j];
       v[j] = fwd_update(ab.x, ab.y, u1[j], u2[j], s.ed[j], lap);
     }
   }
@@ -549,12 +558,13 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
 #ifdef DUFWI_EXP_TIMING
   const long long T1 = clock64();
 #endif
+  // (the forward's FULL step is measured faster than the single-(A, B) one)
   if (s.fast)
-    fwd_body<RPT, T, MODE, true, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
+    fwd_body<RPT, T, MODE, true, true, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else if (s.full)
-    fwd_body<RPT, T, MODE, true, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
+    fwd_body<RPT, T, MODE, true, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else
-    fwd_body<RPT, T, MODE, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
+    fwd_body<RPT, T, MODE, false, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
 #ifdef DUFWI_EXP_TIMING
   dbg_step(0, T0, T1, s.fast ? 0 : s.full ? 1 : 2);
 #endif
@@ -663,7 +673,7 @@ struct AdjBufs {
   uint32_t lwb, uwb, bar_r, bar_w, bar_wb;
 };
 
-template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool T2>
+template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF, bool T2>
 __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
                                          double (&ub)[RPT], double (&acc)[RPT], int i, int U,
@@ -675,6 +685,7 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
   const int k = i % kStage;
   // lam[t] = A lam1 + L^T(E lam1) + B lam2 (+ residual at receivers)
   double el[RPT], lam[RPT];
+  const double2 ab0 = (!PLAIN && UNIF) ? s.ab[0] : make_double2(2.0, -1.0);
 #pragma unroll
   for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
   {
@@ -688,7 +699,7 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
       if (PLAIN) {
         lam[j] = adj_update_free(l1[j], l2[j], adj);
       } else {
-        const double2 ab = s.ab[j];
+        const double2 ab = UNIF ? ab0 : s.ab[j];
         lam[j] = adj_update(ab.x, ab.y, l1[j], l2[j], adj);
       }
     }
@@ -795,16 +806,19 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
   const long long T1 = clock64();
 #endif
   if (MODE == 2 && s.fast)
-    adj_body<RPT, T, MODE, true, true, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B, pulse_t, io,
-                                           hist, N2);
+    adj_body<RPT, T, MODE, true, true, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B,
+                                                  pulse_t, io, hist, N2);
+  else if (s.unif)
+    adj_body<RPT, T, MODE, true, false, true, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B,
+                                                  pulse_t, io, hist, N2);
   else if (s.full)
-    adj_body<RPT, T, MODE, true, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B, pulse_t, io,
-                                            hist, N2);
+    adj_body<RPT, T, MODE, true, false, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B,
+                                                   pulse_t, io, hist, N2);
   else
-    adj_body<RPT, T, MODE, false, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B, pulse_t,
-                                             io, hist, N2);
+    adj_body<RPT, T, MODE, false, false, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B,
+                                                    pulse_t, io, hist, N2);
 #ifdef DUFWI_EXP_TIMING
-  dbg_step(1, T0, T1, (MODE == 2 && s.fast) ? 0 : s.full ? 1 : 2);
+  dbg_step(1, T0, T1, (MODE == 2 && s.fast) ? 0 : s.unif ? 3 : s.full ? 1 : 2);
 #endif
 }
 

@@ -550,4 +550,5 @@ __global__ void __launch_bounds__(kVecAdjWarps * 32)
 }
 
 
+
 }  // namespace dufwi

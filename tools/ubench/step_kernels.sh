@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 python tools/time_config.py --config ${CFG:-4} --units ${UNITS:-64} --nt 40 --reps 1 > gpurun_out/sk_plain.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    -k regex:"vec_kernel|pipe_kernel|stream_kernel|residual|reduce_groups|finalize" -s 60 -c 40 \
+    -k regex:"vec_kernel|pipe_kernel|batch_kernel|stream_kernel|residual|reduce_groups|finalize" -s 60 -c 40 \
     python tools/time_config.py --config ${CFG:-4} --units ${UNITS:-64} --nt 40 --reps 1 > gpurun_out/sk_ncu.csv 2>/dev/null
 python - <<'PY'
 import csv, io, collections
