@@ -234,9 +234,13 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   std::vector<int> rx_slot((size_t)S * R), rx_next((size_t)S * R, -1);
   std::vector<unsigned char> rx_head((size_t)S * R, 1);
   int M = 0;
+  std::vector<int2> rx_nodes;  // distinct receiver nodes (cluster IO staging bounds)
   for (int i = 0; i < S * R; ++i) {
     const size_t cell = (size_t)geo->rx_host[2 * i] * nz + geo->rx_host[2 * i + 1];
-    if (node_slot[cell] < 0) node_slot[cell] = M++;
+    if (node_slot[cell] < 0) {
+      node_slot[cell] = M++;
+      rx_nodes.push_back(make_int2(geo->rx_host[2 * i], geo->rx_host[2 * i + 1]));
+    }
     rx_slot[i] = node_slot[cell];
     row_flag[geo->rx_host[2 * i]] = 1;
   }
@@ -348,7 +352,7 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.tx = p->tx;
   g.node_slot = p->node_slot;
   g.row_flag = p->row_flag;
-  p->cluster_ok = cluster_candidates(g, p->has_rho != 0, p->ccands);
+  p->cluster_ok = cluster_candidates(g, p->has_rho != 0, rx_nodes, p->ccands);
   if (p->cluster_ok) p->ccfg = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots);
   *plan_out = p;
   return DUFWI_OK;

@@ -58,7 +58,7 @@ struct ClusterCfg {
   int nseg = 0;     // thread segments per column
   int threads = 0;  // threads per CTA = nz * nseg
   int dbl = 0;      // exchange rows in f64 (1) or f32 (0)
-  int maxrec = 0;   // receiver cells per CTA (upper bound) staged in shared memory
+  int maxrec = 0;   // receiver stage entries per CTA: RPT per thread holding receivers
   int maxring = 0;  // ring-strip cells per CTA (upper bound) staged in shared memory
   int maxc = 0;     // clusters co-resident on the device (one wave)
   size_t smem_fwd = 0, smem_adj = 0;
@@ -132,6 +132,11 @@ __device__ __forceinline__ void push_if(uint32_t on, uint32_t raddr, float v, ui
       "@q st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2]; }" ::"r"(raddr),
       "r"(__float_as_uint(v)), "r"(rbar), "r"(on)
       : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -295,33 +300,36 @@ __device__ __forceinline__ bool in_box(const Geo& g, int x, int z) {
   return x >= g.x_lo && x <= g.x_hi && z >= g.z_lo && z <= g.z_hi;
 }
 
-// Column order of the slab: columns holding any damped, receiver, ring or
-// source cell first, plain columns after, so whole warps of plain columns run
-// the fast step.  Sets c.z / c.xo.  scratch: 2 * nz ints of shared memory
-// (the exchange buffers, before they are zeroed).
+// Column order of the slab, in three classes so that warps are uniform:
+// columns with no cell in the undamped box (PML, incl. ring columns) first,
+// then columns holding any damped, receiver, ring or source cell, then plain
+// columns (every warp of those runs the fast step).  Sets c.z / c.xo.
+// scratch: 2 * nz ints of shared memory (the exchange buffers, before they
+// are zeroed).
 template <class T>
 __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx, int txz,
                                               int* scratch) {
   const int nz = g.nz;
-  int* plain = scratch;
+  int* cls = scratch;
   int* order = scratch + nz;
   for (int z = threadIdx.x; z < nz; z += blockDim.x) {
-    int p = 1;
-    for (int lr = 0; lr < c.nr && p; ++lr) {
+    int plain = 1, boxed = 0;
+    for (int lr = 0; lr < c.nr; ++lr) {
       const int x = c.r0 + lr;
-      if (damping_at(g, x, z) != 0.0 || !in_box(g, x, z) || (x == txx && z == txz) ||
+      const bool inb = in_box(g, x, z);
+      boxed |= inb;
+      if (damping_at(g, x, z) != 0.0 || !inb || (x == txx && z == txz) ||
           (g.row_flag[x] && g.node_slot[(size_t)x * nz + z] >= 0) || ring_index(g, x, z) >= 0)
-        p = 0;
+        plain = 0;
     }
-    plain[z] = p;
+    cls[z] = plain ? 2 : boxed ? 1 : 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     int k = 0;
-    for (int z = 0; z < nz; ++z)
-      if (!plain[z]) order[k++] = z;
-    for (int z = 0; z < nz; ++z)
-      if (plain[z]) order[k++] = z;
+    for (int q = 0; q < 3; ++q)
+      for (int z = 0; z < nz; ++z)
+        if (cls[z] == q) order[k++] = z;
   }
   __syncthreads();
   c.z = order[c.zi];
@@ -335,18 +343,23 @@ __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx,
 template <int RPT>
 struct CellStatic {
   double ed[RPT];
-  // receiver / ring rows (bit j = row j) and their first IO-stage index: row j's
-  // entry is base + popc(mask below j) (a thread's entries are contiguous)
+  // receiver / ring rows (bit j = row j) and their first IO-stage index.  A
+  // thread holding receivers owns RPT consecutive receiver entries (row j at
+  // base + j; slot -1 where row j has none), ring row j's entry is
+  // gbase + popc(gmask below j)
   unsigned rmask, gmask;
   int rbase, gbase;
+  uint32_t gsa;  // shared address of the thread's first ring stage entry (slot 0)
   unsigned active, src, interior;
   bool pushes_up, pushes_dn;  // owns the slab's first / last row
   unsigned dn_mask;           // bit j set: register j holds the slab's last row (pushes_dn)
   bool special;               // any receiver / ring / source cell
   bool undamped;              // every cell has D == 0: (A, B) = (2, -1), no table reads
   bool fast;                  // whole warp: full, undamped, interior, not special
+  bool plainio;               // whole warp: full, undamped, interior (receivers / source allowed)
   bool full;                  // whole warp: every row slot active
   bool unif;                  // whole warp: full, and one (A, B) per thread for all its rows
+  bool pml;                   // whole warp: full, and no cell in the undamped box
   const double2* ab;          // this thread's (A, B) column: ab[j] for row j
 };
 
@@ -383,14 +396,14 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
     }
   }
   // IO-stage entries (storage slots only: their order does not matter)
-  st.rbase = st.rmask ? atomicAdd(&io.counts[0], __popc(st.rmask)) : 0;
+  st.rbase = st.rmask ? atomicAdd(&io.counts[0], RPT) : 0;
   st.gbase = st.gmask ? atomicAdd(&io.counts[1], __popc(st.gmask)) : 0;
-  for (int j = 0, n = 0; j < RPT; ++j)
-    if (st.rmask & (1u << j)) {
+  st.gsa = smem_addr(io.sring + st.gbase);
+  if (st.rmask)
+    for (int j = 0; j < RPT; ++j) {
       const int x = c.r0 + c.lrow0 + j;
-      io.rec_g[st.rbase + n] = g.node_slot[(size_t)x * g.nz + c.z];
-      io.rec_b[st.rbase + n] = c.xo + j;
-      ++n;
+      io.rec_g[st.rbase + j] = (st.rmask & (1u << j)) ? g.node_slot[(size_t)x * g.nz + c.z] : -1;
+      io.rec_b[st.rbase + j] = c.xo + j;
     }
   for (int j = 0, n = 0; j < RPT; ++j)
     if (st.gmask & (1u << j)) {
@@ -408,6 +421,8 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
   const bool f = allow_fast && st.active == full && st.interior == full && st.undamped && !any;
   // warp-uniform path choice
   st.fast = __all_sync(__activemask(), f);
+  st.plainio = __all_sync(__activemask(), allow_fast && st.active == full &&
+                                              st.interior == full && st.undamped);
   st.full = __all_sync(__activemask(), st.active == full);
   bool same = true;  // one damping value (hence one (A, B)) down the thread's column
 #pragma unroll
@@ -416,6 +431,7 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
         damping_at(g, c.r0 + c.lrow0 + j, c.z) != damping_at(g, c.r0 + c.lrow0, c.z))
       same = false;
   st.unif = __all_sync(__activemask(), st.active == full && same);
+  st.pml = __all_sync(__activemask(), st.active == full && st.interior == 0u);
 }
 
 // Exchange-row pushes to the neighbouring CTAs (DSMEM st.async completing on
@@ -463,10 +479,11 @@ struct StepBufs {
 };
 
 // One forward step of a thread's cells (u1 = u[t-1] -> u2 := u[t]).  FULL:
-// every row slot active (no per-row predicates); PLAIN: undamped and no
-// source (A = 2, B = -1).  Both are warp-uniform, chosen once per sweep.
+// every row slot active (no per-row predicates); PLAIN: undamped cells of the
+// box (A = 2, B = -1); IO: a PLAIN thread may hold the source (receivers are
+// gathered separately).  All warp-uniform, chosen once per sweep.
 // Receiver / ring samples are gathered from the exchange buffer by io_gather.
-template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF>
+template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF, bool IO>
 __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&u1)[RPT], double (&u2)[RPT], int t, int U,
                                          int lu, const StepBufs<T>& B, double pulse_t,
@@ -489,7 +506,7 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
       v[j] = fwd_update(ab.x, ab.y, u1[j], u2[j], s.ed[j], lap);
     }
   }
-  if (!PLAIN && s.src) {
+  if ((!PLAIN || IO) && s.src) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
       if (s.src & (1u << j)) v[j] = __dadd_rn(v[j], pulse_t);
@@ -530,7 +547,8 @@ __device__ __forceinline__ void flush_stage(const Geo& g, const IoStage& io, int
   const int nrec = io.counts[0], nring = io.counts[1];
   for (int idx = threadIdx.x; idx < nk * nrec; idx += blockDim.x) {
     const int k = idx / nrec, i = idx - k * nrec;
-    rec[((size_t)(t0 + k) * U + lu) * g.M + io.rec_g[i]] = (float)io.srec[k * io.maxrec + i];
+    const int slot = io.rec_g[i];
+    if (slot >= 0) rec[((size_t)(t0 + k) * U + lu) * g.M + slot] = (float)io.srec[k * io.maxrec + i];
   }
   if (MODE == 2) {
     for (int idx = threadIdx.x; idx < nk * nring; idx += blockDim.x) {
@@ -560,13 +578,15 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
 #endif
   // (the forward's FULL step is measured faster than the single-(A, B) one)
   if (s.fast)
-    fwd_body<RPT, T, MODE, true, true, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
+    fwd_body<RPT, T, MODE, true, true, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
+  else if (s.plainio)
+    fwd_body<RPT, T, MODE, true, true, false, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else if (s.full)
-    fwd_body<RPT, T, MODE, true, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
+    fwd_body<RPT, T, MODE, true, false, false, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else
-    fwd_body<RPT, T, MODE, false, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
+    fwd_body<RPT, T, MODE, false, false, false, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
 #ifdef DUFWI_EXP_TIMING
-  dbg_step(0, T0, T1, s.fast ? 0 : s.full ? 1 : 2);
+  dbg_step(0, T0, T1, s.fast ? 0 : s.plainio ? 5 : s.full ? 1 : 2);
 #endif
 }
 
@@ -673,7 +693,10 @@ struct AdjBufs {
   uint32_t lwb, uwb, bar_r, bar_w, bar_wb;
 };
 
-template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF, bool T2>
+// NOIMG (MODE 2): no cell of the thread lies in the undamped box, so there is
+// no imaging and no reconstruction; only ring cells carry u (from the strips).
+template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF, bool IO, bool NOIMG,
+          bool T2>
 __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
                                          double (&ub)[RPT], double (&acc)[RPT], int i, int U,
@@ -704,16 +727,16 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
       }
     }
   }
-  if (!PLAIN && s.special) {
+  if ((!PLAIN || IO) && !NOIMG && s.rmask) {
+    // one entry per row (0 where the row has no receiver: adding it is exact)
+    const double* r = io.srec + (size_t)k * io.maxrec + s.rbase;
 #pragma unroll
-    for (int j = 0; j < RPT; ++j)
-      if (s.rmask & (1u << j))
-        lam[j] = __dadd_rn(lam[j], io.srec[k * io.maxrec + s.rbase + __popc(s.rmask & ((1u << j) - 1u))]);
+    for (int j = 0; j < RPT; ++j) lam[j] = __dadd_rn(lam[j], r[j]);
   }
   // imaging with L(u[t-1]) and reconstruction of u[t-2]
   const bool img = T2 || t >= 1;
   double lapu[RPT];
-  if (MODE == 2) {
+  if (MODE == 2 && !NOIMG) {
     const T* pc = B.ur + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
@@ -722,7 +745,7 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
       const double xp = own_next ? ub[j + 1] : (double)pc[j + 1];
       lapu[j] = lap5(ub[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
     }
-  } else {
+  } else if (MODE == 1) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       lapu[j] = 0.0;
@@ -747,6 +770,14 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
     if (!FULL && !(s.active & (1u << j))) continue;
     l2[j] = lam[j];
     ql[j] = (T)elw[j];
+    if (MODE == 2 && NOIMG) {
+      if (s.gmask & (1u << j)) {
+        if (T2 || t >= 2)
+          ua[j] = (double)lds_f32(s.gsa + 4u * (uint32_t)(k * io.maxring + __popc(s.gmask & ((1u << j) - 1u))));
+        qu[j] = (T)ua[j];
+      }
+      continue;
+    }
     if (img) {
       if (MODE == 1) {
         acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
@@ -754,12 +785,12 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
         acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
         if (T2 || t >= 2) {
           double prev = recon(ub[j], ua[j], s.ed[j], lapu[j]);
-          if (!PLAIN && (s.src & (1u << j))) prev = __dadd_rn(prev, pulse_t);
+          if ((!PLAIN || IO) && (s.src & (1u << j))) prev = __dadd_rn(prev, pulse_t);
           ua[j] = prev;
         }
       } else if ((s.gmask & (1u << j)) && (T2 || t >= 2)) {
         // ring cell: the saved strip stands in for the reconstruction
-        ua[j] = (double)io.sring[k * io.maxring + s.gbase + __popc(s.gmask & ((1u << j) - 1u))];
+        ua[j] = (double)lds_f32(s.gsa + 4u * (uint32_t)(k * io.maxring + __popc(s.gmask & ((1u << j) - 1u))));
       }
     }
     if (MODE == 2) qu[j] = (T)ua[j];
@@ -780,7 +811,8 @@ __device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, 
   for (int idx = threadIdx.x; idx < nk * nrec; idx += blockDim.x) {
     const int k = idx / nrec, r = idx - k * nrec;
     const int t = g.nt - 1 - (i0 + k);
-    io.srec[k * io.maxrec + r] = rres[((size_t)t * U + lu) * g.M + io.rec_g[r]];
+    const int slot = io.rec_g[r];
+    io.srec[k * io.maxrec + r] = slot >= 0 ? rres[((size_t)t * U + lu) * g.M + slot] : 0.0;
   }
   if (MODE == 2) {
     for (int idx = threadIdx.x; idx < nk * nring; idx += blockDim.x) {
@@ -805,20 +837,26 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
 #ifdef DUFWI_EXP_TIMING
   const long long T1 = clock64();
 #endif
+#define DUFWI_ADJ_BODY(FULL, PLAIN, UNIF, IO, NOIMG)                                           \
+  adj_body<RPT, T, MODE, FULL, PLAIN, UNIF, IO, NOIMG, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, \
+                                                           B, pulse_t, io, hist, N2)
   if (MODE == 2 && s.fast)
-    adj_body<RPT, T, MODE, true, true, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B,
-                                                  pulse_t, io, hist, N2);
+    DUFWI_ADJ_BODY(true, true, false, false, false);
+  else if (MODE == 2 && s.plainio)
+    DUFWI_ADJ_BODY(true, true, false, true, false);
+  else if (MODE == 2 && s.pml && s.unif)
+    DUFWI_ADJ_BODY(true, false, true, true, true);
+  else if (MODE == 2 && s.pml)
+    DUFWI_ADJ_BODY(true, false, false, true, true);
   else if (s.unif)
-    adj_body<RPT, T, MODE, true, false, true, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B,
-                                                  pulse_t, io, hist, N2);
+    DUFWI_ADJ_BODY(true, false, true, true, false);
   else if (s.full)
-    adj_body<RPT, T, MODE, true, false, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B,
-                                                   pulse_t, io, hist, N2);
+    DUFWI_ADJ_BODY(true, false, false, true, false);
   else
-    adj_body<RPT, T, MODE, false, false, false, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, B,
-                                                    pulse_t, io, hist, N2);
+    DUFWI_ADJ_BODY(false, false, false, true, false);
+#undef DUFWI_ADJ_BODY
 #ifdef DUFWI_EXP_TIMING
-  dbg_step(1, T0, T1, (MODE == 2 && s.fast) ? 0 : s.unif ? 3 : s.full ? 1 : 2);
+  dbg_step(1, T0, T1, (MODE == 2 && s.fast) ? 0 : (MODE == 2 && s.plainio) ? 5 : (MODE == 2 && s.pml) ? 4 : s.unif ? 3 : s.full ? 1 : 2);
 #endif
 }
 
@@ -971,14 +1009,33 @@ inline int max_ring_cells(const Geo& g, int rows) {
   return best;
 }
 
+// Receiver stage entries of the fullest slab: RPT per (column, segment) that
+// holds a receiver node (`rxn`: distinct receiver nodes, host copy).
+inline int max_rec_entries(const Geo& g, int rows, int rpt, const std::vector<int2>& rxn) {
+  int best = 0;
+  std::vector<char> seen;
+  for (int r0 = 0; r0 < g.nx; r0 += rows) {
+    const int nseg = (rows + rpt - 1) / rpt;
+    seen.assign((size_t)nseg * g.nz, 0);
+    int n = 0;
+    for (const int2& p : rxn)
+      if (p.x >= r0 && p.x < r0 + rows) {
+        char& f = seen[(size_t)((p.x - r0) / rpt) * g.nz + p.y];
+        if (!f) { f = 1; ++n; }
+      }
+    best = std::max(best, n * rpt);
+  }
+  return best;
+}
+
 template <int RPT, class T>
-inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
+inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, ClusterCfg* out) {
   const int rows = (g.nx + cs - 1) / cs;
   if (rows < 2) return false;
   const int nseg = (rows + RPT - 1) / RPT;
   const int threads = g.nz * nseg;
   if (threads > cluster_max_threads(RPT)) return false;
-  const int maxrec = std::min(g.M, rows * g.nz);
+  const int maxrec = max_rec_entries(g, rows, RPT, rxn);
   const int maxring = g.SL > 0 ? max_ring_cells(g, rows) : 0;
   const size_t sf = cluster_smem_bytes<T>(rows, RPT, g.nz, 2, maxrec, maxring);
   const size_t sa = cluster_smem_bytes<T>(rows, RPT, g.nz, 4, maxrec, maxring);
@@ -1007,14 +1064,15 @@ inline bool try_cluster_cfg(const Geo& g, int cs, ClusterCfg* out) {
 // instances below cover up to 8 rows per thread with f64 exchange rows and
 // 2 / 4 with the f32 fallback (large nz, where f64 rows exceed shared memory).
 template <class T>
-inline bool try_cluster_rpt(const Geo& g, int cs, int rpt, ClusterCfg* out) {
+inline bool try_cluster_rpt(const Geo& g, int cs, int rpt, const std::vector<int2>& rxn,
+                            ClusterCfg* out) {
   switch (rpt) {
-    case 2: return try_cluster_cfg<2, T>(g, cs, out);
-    case 4: return try_cluster_cfg<4, T>(g, cs, out);
-    case 5: return sizeof(T) == 8 && try_cluster_cfg<5, double>(g, cs, out);
-    case 6: return sizeof(T) == 8 && try_cluster_cfg<6, double>(g, cs, out);
-    case 7: return sizeof(T) == 8 && try_cluster_cfg<7, double>(g, cs, out);
-    case 8: return sizeof(T) == 8 && try_cluster_cfg<8, double>(g, cs, out);
+    case 2: return try_cluster_cfg<2, T>(g, cs, rxn, out);
+    case 4: return try_cluster_cfg<4, T>(g, cs, rxn, out);
+    case 5: return sizeof(T) == 8 && try_cluster_cfg<5, double>(g, cs, rxn, out);
+    case 6: return sizeof(T) == 8 && try_cluster_cfg<6, double>(g, cs, rxn, out);
+    case 7: return sizeof(T) == 8 && try_cluster_cfg<7, double>(g, cs, rxn, out);
+    case 8: return sizeof(T) == 8 && try_cluster_cfg<8, double>(g, cs, rxn, out);
     default: return false;
   }
 }
@@ -1022,7 +1080,8 @@ inline bool try_cluster_rpt(const Geo& g, int cs, int rpt, ClusterCfg* out) {
 // Every launch shape that fits: cluster sizes 16 .. 2, each with the fewest
 // rows per thread that fit the thread budget and any larger count that splits
 // the slab exactly.  DUFWI_CLUSTER_CS / DUFWI_CLUSTER_RPT pin them (experiments).
-inline bool cluster_candidates(const Geo& g, bool rho, std::vector<ClusterCfg>& out) {
+inline bool cluster_candidates(const Geo& g, bool rho, const std::vector<int2>& rxn,
+                               std::vector<ClusterCfg>& out) {
   out.clear();
   if (rho) return false;  // density runs on the stepwise engine
   int dev = 0, major = 0;
@@ -1049,9 +1108,9 @@ inline bool cluster_candidates(const Geo& g, bool rho, std::vector<ClusterCfg>& 
       if (!take) continue;
       ClusterCfg c;
 #ifndef DUFWI_EXCHANGE_F32
-      if (try_cluster_rpt<double>(g, cs, r, &c)) { out.push_back(c); continue; }
+      if (try_cluster_rpt<double>(g, cs, r, rxn, &c)) { out.push_back(c); continue; }
 #endif
-      if (try_cluster_rpt<float>(g, cs, r, &c)) out.push_back(c);
+      if (try_cluster_rpt<float>(g, cs, r, rxn, &c)) out.push_back(c);
     }
   }
   return !out.empty();
@@ -1059,12 +1118,13 @@ inline bool cluster_candidates(const Geo& g, bool rho, std::vector<ClusterCfg>& 
 
 // Per-step cost model of a shape, in row slots per SM: idle slots of a partial
 // last segment keep its warps off the fast step (x1.3); 7-8 rows per thread
-// run fewer warps with more register pressure (x1.15).  Measured on config 1:
-// 18 slots as 3 x 6 < 16 as 2 x 8 < 18 as 3 x 6 with 16 rows used.
+// run fewer warps with more register pressure (x1.05).  Measured on config 1
+// (forward + adjoint ms): 16 rows as 2 x 8 (0.84 + 1.71) < 18 as 3 x 6
+// (0.87 + 1.82) < 18 slots as 3 x 6 with 16 rows used.
 inline double cluster_cost(const ClusterCfg& c) {
   double cost = (double)c.nseg * c.rpt;
   if (c.rows % c.rpt) cost *= 1.3;
-  if (c.rpt >= 7) cost *= 1.15;
+  if (c.rpt >= 7) cost *= 1.05;
   return cost;
 }
 

@@ -25,7 +25,7 @@ so.dufwi_debug_counters(buf, 256)
 eng.misfit_and_gradient(obs)
 so.dufwi_debug_counters(buf, 256)
 nt = grid.nt
-paths = {0: "plain", 1: "full", 2: "generic", 3: "unif"}
+paths = {0: "plain", 1: "full", 2: "generic", 3: "unif", 4: "xpml", 5: "io-plain"}
 for sweep in (0, 1):
     print(["forward", "adjoint"][sweep], "cycles per step: [sync+wait, body] path")
     for cta in (0, 1):
