@@ -118,7 +118,8 @@ def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) ->
     eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
                      setup.pulse.samples, damping, has_rho=rho is not None)
     rec = Reconstructor(eng, nets, setup.bounds, rho=rho)
-    obs = torch.as_tensor(m_obs.traces, dtype=torch.float64).to(eng.device)
+    # ChannelData arrays are read-only views: a writable host copy for torch
+    obs = torch.from_numpy(np.require(m_obs.traces, np.float64, ["C", "W"])).to(eng.device)
     c = torch.as_tensor(c0.values, dtype=torch.float64).to(eng.device)[None]
     try:
         maps = rec.reconstruct(obs, c)
