@@ -12,6 +12,7 @@
 #include "dufwi_cluster_kernels.cuh"
 #include "dufwi_step_kernels.cuh"
 #include "dufwi_vec_kernels.cuh"
+#include "dufwi_lean_kernels.cuh"
 
 using namespace dufwi;
 
@@ -55,7 +56,7 @@ struct dufwi_plan {
   int *tx = nullptr, *rx_slot = nullptr, *rx_next = nullptr, *node_slot = nullptr;
   int* elements = nullptr;
   int* rx_slot_unused = nullptr;
-  unsigned char *row_flag = nullptr, *rx_head = nullptr;
+  unsigned char *row_flag = nullptr, *col_flag = nullptr, *rx_head = nullptr;
   double *Ed = nullptr, *dEdc = nullptr, *rho = nullptr, *q = nullptr;
   int* flag = nullptr;
   std::vector<void*> owned;
@@ -64,6 +65,7 @@ struct dufwi_plan {
   std::vector<ClusterCfg> ccands;  // launch shapes that fit, one per cluster size
   ClusterCfg ccfg{};                // the shape for all units at once (plan_info)
   bool cluster_ok = false;
+  int lean_nsl = 3;  // ring depth of the lean stepwise kernels (0: use the vec kernels)
 };
 
 namespace {
@@ -122,8 +124,11 @@ Groups fwd_groups(const Geo& g, int unit_begin, int U) { return make_groups(g, u
 
 // Adjoint: as many shots per group as the warp target allows (one f64
 // accumulator read-modify-write per cell, group and step).
-Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec) {
+Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec, bool lean) {
   if (per_unit) return make_groups(g, unit_begin, U, 1);
+  // lean imaging kernel: ~8 groups, enough CTAs for several waves; the
+  // accumulator read-modify-write costs 16 B / gs per cell update
+  if (lean) return make_groups(g, unit_begin, U, std::max(1, (U + 7) / 8));
   const long wpg = vec ? (long)((g.nz + 127) / 128) * ((g.nx + kVecAdjTX - 1) / kVecAdjTX)
                        : warps_per_group(g);
   const long target = vec ? 148L * 32 : kTargetWarps;
@@ -135,9 +140,11 @@ Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec) 
 
 // Vectorised stepwise kernels: constant density, rows made of whole float4s.
 bool use_vec(const dufwi_plan_t* p) { return !p->has_rho && p->geo.nz % 4 == 0; }
+// Lean kernels: additionally separable damping with a rectangular undamped box.
+bool use_lean(const dufwi_plan_t* p) { return use_vec(p) && p->ab.px && p->box_ok && p->lean_nsl > 0; }
 
 Groups groups_for(const dufwi_plan_t* p, int unit_begin, int U, bool per_unit) {
-  return adj_groups(p->geo, unit_begin, U, per_unit, use_vec(p));
+  return adj_groups(p->geo, unit_begin, U, per_unit, use_vec(p), use_lean(p));
 }
 
 // Upper bound of the group count over every placement of U units.
@@ -230,7 +237,7 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
 
   // receiver-node slots: one slot per distinct receiver node of the geometry
   std::vector<int> node_slot((size_t)nx * nz, -1);
-  std::vector<unsigned char> row_flag(nx, 0);
+  std::vector<unsigned char> row_flag(nx, 0), col_flag(nz, 0);
   std::vector<int> rx_slot((size_t)S * R), rx_next((size_t)S * R, -1);
   std::vector<unsigned char> rx_head((size_t)S * R, 1);
   int M = 0;
@@ -243,6 +250,7 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
     }
     rx_slot[i] = node_slot[cell];
     row_flag[geo->rx_host[2 * i]] = 1;
+    col_flag[geo->rx_host[2 * i + 1]] = 1;
   }
   for (int s = 0; s < S; ++s) {  // chain duplicate receiver nodes within a shot
     for (int r = 0; r < R; ++r) {
@@ -328,6 +336,7 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   rc = rc ? rc : upload(p, &p->rx_head, rx_head.data(), rx_head.size());
   rc = rc ? rc : upload(p, &p->node_slot, node_slot.data(), node_slot.size());
   rc = rc ? rc : upload(p, &p->row_flag, row_flag.data(), row_flag.size());
+  rc = rc ? rc : upload(p, &p->col_flag, col_flag.data(), col_flag.size());
   if (p->E > 0) rc = rc ? rc : upload(p, &p->elements, geo->elements_host, 2 * (size_t)p->E);
   const size_t BN2 = (size_t)g.B * nx * nz;
   rc = rc ? rc : dev_alloc(p, &p->Ed, BN2);
@@ -352,6 +361,21 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.tx = p->tx;
   g.node_slot = p->node_slot;
   g.row_flag = p->row_flag;
+  g.col_flag = p->col_flag;
+  if (const char* e = getenv("DUFWI_LEAN_NSL")) p->lean_nsl = atoi(e);
+  if (p->lean_nsl != 0 && p->lean_nsl != 3 && p->lean_nsl != 6) p->lean_nsl = 3;
+  {  // lean rings may exceed the 48 KB default of dynamic shared memory
+    for (auto f : {fwd_lean_kernel<0, 3>, fwd_lean_kernel<1, 3>, fwd_lean_kernel<2, 3>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanFwdRing<3>));
+    for (auto f : {fwd_lean_kernel<0, 6>, fwd_lean_kernel<1, 6>, fwd_lean_kernel<2, 6>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanFwdRing<6>));
+    cudaFuncSetAttribute(adjlam_lean_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         sizeof(LeanAdjRing<3>));
+    cudaFuncSetAttribute(adjlam_lean_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         sizeof(LeanAdjRing<6>));
+    for (auto f : {img_lean_kernel<1>, img_lean_kernel<2>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanImgRing));
+  }
   p->cluster_ok = cluster_candidates(g, p->has_rho != 0, rx_nodes, p->ccands);
   if (p->cluster_ok) p->ccfg = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots);
   *plan_out = p;
@@ -455,6 +479,8 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
       if (warps >= 148L * 32) { vtx = c; break; }
     }
     const dim3 vgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
+    const bool lean = use_lean(p);
+    const dim3 lgrid((g.nz + 127) / 128, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx), U);
     dim3 block(kWarpsX * 32);
     dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXF - 1) / (kWarpsX * kRXF), G.ngroups);
     for (int t = 0; t < g.nt; ++t) {
@@ -478,7 +504,16 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
 #define DUFWI_VEC(M)                                                                            \
   fwd_vec_kernel<M><<<vgrid, kPipeWarps * 32, sizeof(FwdRing), st>>>(g, m, p->ab, t, unit_begin, \
                                                       vtx, u1, u2, uo, rec_t, st_t, has1, has2)
-      if (vec) {
+#define DUFWI_LEAN(M, NS)                                                                       \
+  fwd_lean_kernel<M, NS><<<lgrid, kLeanWarps * 32, sizeof(LeanFwdRing<NS>), st>>>(               \
+      g, m, p->ab, t, unit_begin, vtx, u1, u2, uo, rec_t, st_t, has1, has2)
+      if (lean) {
+        if (p->lean_nsl == 6) {
+          if (mode == 0) DUFWI_LEAN(0, 6); else if (mode == 1) DUFWI_LEAN(1, 6); else DUFWI_LEAN(2, 6);
+        } else {
+          if (mode == 0) DUFWI_LEAN(0, 3); else if (mode == 1) DUFWI_LEAN(1, 3); else DUFWI_LEAN(2, 3);
+        }
+      } else if (vec) {
         if (mode == 0) DUFWI_VEC(0); else if (mode == 1) DUFWI_VEC(1); else DUFWI_VEC(2);
       } else if (p->has_rho) {
         if (mode == 0) DUFWI_FWD(true, 0); else if (mode == 1) DUFWI_FWD(true, 1); else DUFWI_FWD(true, 2);
@@ -487,6 +522,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
       }
 #undef DUFWI_FWD
 #undef DUFWI_VEC
+#undef DUFWI_LEAN
       LAUNCH_CHECK(p);
     }
   }
@@ -584,11 +620,33 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
         const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
         if (warps >= 148L * 32) { vtx = c; break; }
       }
-      const dim3 lgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
-      adjlam_pipe_kernel<<<lgrid, kPipeWarps * 32, sizeof(AdjRing), st>>>(
-          g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
+      if (use_lean(p)) {
+        const dim3 lgrid((g.nz + 127) / 128, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx), U);
+        if (p->lean_nsl == 6)
+          adjlam_lean_kernel<6><<<lgrid, kLeanWarps * 32, sizeof(LeanAdjRing<6>), st>>>(
+              g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
+        else
+          adjlam_lean_kernel<3><<<lgrid, kLeanWarps * 32, sizeof(LeanAdjRing<3>), st>>>(
+              g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
+      } else {
+        const dim3 lgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
+        adjlam_pipe_kernel<<<lgrid, kPipeWarps * 32, sizeof(AdjRing), st>>>(
+            g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
+      }
       LAUNCH_CHECK(p);
-      if (do_img) {
+      if (do_img && use_lean(p)) {
+        const int rows = mode == DUFWI_STORE_STRIPS ? g.Lx : g.nx;
+        const dim3 igrid((g.nz + 127) / 128, (rows + kLeanWarps * kImgTX - 1) / (kLeanWarps * kImgTX),
+                         G.ngroups);
+        const float* st_tm2 = (mode == DUFWI_STORE_STRIPS && do_recon) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
+        if (mode == DUFWI_STORE_FULL)
+          img_lean_kernel<1><<<igrid, kLeanWarps * 32, sizeof(LeanImgRing), st>>>(
+              g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm2, acc_part, do_recon);
+        else
+          img_lean_kernel<2><<<igrid, kLeanWarps * 32, sizeof(LeanImgRing), st>>>(
+              g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm2, acc_part, do_recon);
+        LAUNCH_CHECK(p);
+      } else if (do_img) {
         const dim3 igrid((g.nz + 127) / 128,
                          (g.nx + kVecAdjWarps * kVecAdjTX - 1) / (kVecAdjWarps * kVecAdjTX), G.ngroups);
         if (mode == DUFWI_STORE_FULL)

@@ -25,6 +25,7 @@ struct Geo {
   const int* tx;               // [S][2]
   const int* node_slot;        // [nx][nz] receiver-node slot or -1
   const unsigned char* row_flag;  // [nx] 1 if the row holds any slot
+  const unsigned char* col_flag;  // [nz] 1 if the column holds any slot
 };
 
 // Per-phantom coefficient arrays.
@@ -79,6 +80,34 @@ __device__ __forceinline__ RhoW rho_weights(const double* rho, const double* q, 
 __device__ __forceinline__ double rho_in_weight(const double* rho, const double* q, size_t c,
                                                 size_t j) {
   return __ldg(rho + j) * (0.5 * (__ldg(q + j) + __ldg(q + c)));
+}
+
+// ------------------------------------------------------------ f64 arithmetic
+// Explicit roundings, shared by the fast and the generic step so both produce
+// the same bits: the reference's 5-point sum (((-4c + xm) + xp) + zm) + zp and
+// the update A u1 + B u2 + E lap (forward.py:301-308).
+__device__ __forceinline__ double lap5(double c, double xm, double xp, double zm, double zp) {
+  return __dadd_rn(__dadd_rn(__dadd_rn(__fma_rn(-4.0, c, xm), xp), zm), zp);
+}
+__device__ __forceinline__ double fwd_update(double A, double B, double u1, double u2, double e,
+                                             double lap) {
+  return __fma_rn(e, lap, __fma_rn(A, u1, __dmul_rn(B, u2)));
+}
+// (A, B) = (2, -1): B u2 = -u2 exactly, so this equals fwd_update bit for bit.
+__device__ __forceinline__ double fwd_update_free(double u1, double u2, double e, double lap) {
+  return __fma_rn(e, lap, __fma_rn(2.0, u1, -u2));
+}
+// lam = (A lam1 + L^T(E lam1)) + B lam2 (adjoint.py:119-131)
+__device__ __forceinline__ double adj_update(double A, double B, double l1, double l2,
+                                             double adj) {
+  return __fma_rn(B, l2, __fma_rn(A, l1, adj));
+}
+__device__ __forceinline__ double adj_update_free(double l1, double l2, double adj) {
+  return __dadd_rn(__fma_rn(2.0, l1, adj), -l2);
+}
+// u[t-2] = 2 u[t-1] + E L u[t-1] - u[t] (+ source), the forward step solved backwards
+__device__ __forceinline__ double recon(double ub, double ua, double e, double lapu) {
+  return __dadd_rn(__fma_rn(e, lapu, 2.0 * ub), -ua);
 }
 
 }  // namespace dufwi

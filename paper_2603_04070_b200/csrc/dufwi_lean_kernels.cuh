@@ -1,0 +1,643 @@
+// Stepwise engine, lean streaming kernels (constant density, nz % 4 == 0,
+// separable damping with a rectangular undamped box: every BASELINE config
+// without density, e.g. config 4).
+//
+// Same data movement as fwd_vec_kernel / adjlam_pipe_kernel — a warp owns a
+// 128-wide z strip (4 cells per lane, float4 loads/stores) and walks TX x-rows
+// of one shot, rows ahead streaming through a per-lane cp.async ring — but
+// shaped for instruction count, which ncu showed to be the limiter of those
+// kernels (~420 warp instructions per 128-cell row, issue-bound at 27% of
+// DRAM peak):
+//   * the x loop is unrolled by the ring depth NSL (a multiple of 3), so ring
+//     slots are immediate offsets and the 3-row register window (x-1, x, x+1)
+//     rotates by renaming instead of 16 register moves per row;
+//   * addresses are one IMAD.WIDE from a per-lane base and a 32-bit row offset;
+//   * per-lane constants hoisted out of the loop: (A, B) of the z-damping band
+//     (only for warps touching it, template switch), the lane's receiver
+//     columns, ring columns and source cell; per-row work is warp-uniform
+//     compares against the undamped box / receiver rows;
+//   * one edge value per lane per row (lane 0: z0-1, lane 31: z0+128).
+// Arithmetic is the explicitly rounded f64 of dufwi_common.cuh (lap5,
+// fwd_update, adj_update): the same bits as the cluster engine.
+// DRAM per cell update: forward 12 B (read u[t-1], u[t-2], write u[t]); lam
+// update 12 B (read lam[t+1], lam[t+2], write lam[t]); E comes from L2.
+#pragma once
+
+#include "dufwi_vec_kernels.cuh"
+
+namespace dufwi {
+
+#ifndef DUFWI_LEAN_WARPS
+#define DUFWI_LEAN_WARPS 4
+#endif
+#ifndef DUFWI_LEAN_MINB
+#define DUFWI_LEAN_MINB 1
+#endif
+constexpr int kLeanWarps = DUFWI_LEAN_WARPS;  // warps per CTA
+constexpr int kLeanMinB = DUFWI_LEAN_MINB;    // min resident CTAs per SM (register cap)
+
+template <int NSL>
+struct LeanFwdRing {
+  float4 u1[NSL][kLeanWarps * 32];   // u[t-1] row r+1
+  float4 u2[NSL][kLeanWarps * 32];   // u[t-2] row r
+  double2 e0[NSL][kLeanWarps * 32];  // E row r, cells 0-1
+  double2 e1[NSL][kLeanWarps * 32];  // E row r, cells 2-3
+  float edge[NSL][kLeanWarps * 32];  // u[t-1] row r+1 at z0-1 (lane 0) / z0+128 (lane 31)
+};
+
+// Per-lane constants of a 4-cell z segment.
+struct LaneInfo {
+  int z4;
+  bool act;
+  unsigned rxk;    // cells on a receiver column
+  unsigned boxk;   // cells with z in [z_lo, z_hi]
+  int ringl, ringr;  // cell index on ring column z_lo-1 / z_hi+1, or -1
+  bool zd;           // any cell in the z damping band
+};
+
+__device__ __forceinline__ LaneInfo lane_info(const Geo& g, const ABTables& T, int z4) {
+  LaneInfo L;
+  L.z4 = z4;
+  L.act = z4 < g.nz;
+  L.rxk = L.boxk = 0u;
+  L.ringl = L.ringr = -1;
+  L.zd = false;
+  if (L.act) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int z = z4 + k;
+      if (__ldg(g.col_flag + z)) L.rxk |= 1u << k;
+      if (z >= g.z_lo && z <= g.z_hi) L.boxk |= 1u << k;
+      if (z == g.z_lo - 1) L.ringl = k;
+      if (z == g.z_hi + 1) L.ringr = k;
+      if (__ldg(T.pz + z) != 0.0) L.zd = true;
+    }
+  }
+  return L;
+}
+
+// Hide a per-lane base pointer from re-association, so base + 32-bit row
+// offset compiles to one IMAD.WIDE instead of a 64-bit add chain.
+template <class P>
+__device__ __forceinline__ P* opaque(P* p) {
+  asm volatile("" : "+l"(p));
+  return p;
+}
+
+// (A, B) of cell (x, z) in a damped row: D = max(px[x], pz[z]) picks the table.
+__device__ __forceinline__ double2 ab_row_damped(const ABTables& T, double pxx, double Axx,
+                                                 double Bxx, int z) {
+  return pxx >= __ldg(T.pz + z) ? make_double2(Axx, Bxx)
+                                : make_double2(__ldg(T.Az + z), __ldg(T.Bz + z));
+}
+
+// ----------------------------------------------------------------- forward
+template <int MODE, int NSL, bool ZD>
+__device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, const LaneInfo& L,
+                                              LeanFwdRing<NSL>& ring, int tid, int lane, int z0,
+                                              int x0, int x1, int lu, int txx, int tk,
+                                              double pulse_t, const float* f1, const float* f2,
+                                              const double* Ed, float* fo, float* rec_t,
+                                              float* strip_t, bool has1, bool has2, bool wrx,
+                                              bool wring) {
+  const int nz = g.nz, nx = g.nx;
+  const int zc = L.act ? L.z4 : 0;
+  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < g.nz;
+  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + 128 : 0;
+  const bool has_edge = has1 && (edge_l || edge_r);
+  const bool ok1 = has1 && L.act, ok2 = has2 && L.act;
+  const float* b1 = opaque(f1 + zc);
+  const float* b2 = opaque(f2 + zc);
+  const double* be = opaque(Ed + zc);
+  const float* bl = opaque(f1 + ze);
+  float* bo = opaque(fo + zc);
+  double Az[4], Bz[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    Az[k] = 2.0;
+    Bz[k] = -1.0;
+    if (ZD && L.act && L.zd) {
+      Az[k] = __ldg(T.Az + L.z4 + k);
+      Bz[k] = __ldg(T.Bz + L.z4 + k);
+    }
+  }
+  // copies of "row r": u[t-1] row r+1 (+ edge), u[t-2] row r, E row r
+  auto issue = [&](int r, int sl) {
+    const bool okn = r + 1 < nx;
+    const int on = okn ? (r + 1) * nz : 0;
+    const int orr = r * nz;
+    cp16(&ring.u1[sl][tid], b1 + on, ok1 && okn);
+    cp16(&ring.u2[sl][tid], b2 + orr, ok2);
+    cp16(&ring.e0[sl][tid], be + orr, L.act);
+    cp16(&ring.e1[sl][tid], be + orr + 2, L.act);
+    cp4(&ring.edge[sl][tid], bl + on, has_edge && okn);
+  };
+  // register window: W[(k) % 3] = row x-1, W[(k+1) % 3] = row x, W[(k+2) % 3] = row x+1
+  double W[3][4];
+  double Eg[3];  // edge value of the row in the same slot of W
+#pragma unroll
+  for (int k = 0; k < 4; ++k) W[0][k] = W[1][k] = W[2][k] = 0.0;
+  Eg[0] = Eg[1] = Eg[2] = 0.0;
+  if (has1) {
+    if (x0 >= 1) {
+      if (L.act) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(b1 + (x0 - 1) * nz));
+        W[0][0] = f.x; W[0][1] = f.y; W[0][2] = f.z; W[0][3] = f.w;
+      }
+    }
+    if (L.act) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(b1 + x0 * nz));
+      W[1][0] = f.x; W[1][1] = f.y; W[1][2] = f.z; W[1][3] = f.w;
+    }
+    if (edge_l || edge_r) Eg[1] = (double)__ldg(bl + x0 * nz);
+  }
+#pragma unroll
+  for (int k = 0; k < NSL - 1; ++k) {
+    if (x0 + k < x1) issue(x0 + k, k);
+    cp_commit();
+  }
+  for (int xb = x0; xb < x1; xb += NSL) {
+#pragma unroll
+    for (int k = 0; k < NSL; ++k) {
+      const int x = xb + k;
+      if (x >= x1) break;
+      const int im = k % 3, ic = (k + 1) % 3, ip = (k + 2) % 3;
+      if (x + NSL - 1 < x1) issue(x + NSL - 1, (k + NSL - 1) % NSL);
+      cp_commit();
+      cp_wait<NSL - 1>();  // the group of row x has landed
+      {
+        const float4 f = ring.u1[k][tid];
+        W[ip][0] = f.x; W[ip][1] = f.y; W[ip][2] = f.z; W[ip][3] = f.w;
+        Eg[ip] = (double)ring.edge[k][tid];
+      }
+      const float4 w2 = ring.u2[k][tid];
+      const double2 e0 = ring.e0[k][tid], e1 = ring.e1[k][tid];
+      const double u2v[4] = {w2.x, w2.y, w2.z, w2.w};
+      const double ed[4] = {e0.x, e0.y, e1.x, e1.y};
+      double zl = __shfl_up_sync(0xffffffffu, W[ic][3], 1);
+      double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1);
+      if (lane == 0) zl = Eg[ic];
+      if (lane == 31) zr = Eg[ic];
+      double v[4];
+      if (x >= g.x_lo && x <= g.x_hi) {  // undamped row: (A, B) of the lane's z band
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double zm = c == 0 ? zl : W[ic][c - 1];
+          const double zp = c == 3 ? zr : W[ic][c + 1];
+          const double lap = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
+          v[c] = ZD ? fwd_update(Az[c], Bz[c], W[ic][c], u2v[c], ed[c], lap)
+                    : fwd_update_free(W[ic][c], u2v[c], ed[c], lap);
+        }
+      } else {  // damped row (x band of the PML)
+        const double pxx = __ldg(T.px + x), Axx = __ldg(T.Ax + x), Bxx = __ldg(T.Bx + x);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double zm = c == 0 ? zl : W[ic][c - 1];
+          const double zp = c == 3 ? zr : W[ic][c + 1];
+          const double lap = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
+          const double2 ab = ab_row_damped(T, pxx, Axx, Bxx, min(L.z4 + c, nz - 1));
+          v[c] = fwd_update(ab.x, ab.y, W[ic][c], u2v[c], ed[c], lap);
+        }
+      }
+      if (x == txx) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c == tk) v[c] = __dadd_rn(v[c], pulse_t);
+      }
+      if (L.act) {
+        const int orow = x * nz;
+        *reinterpret_cast<float4*>(bo + orow) =
+            make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
+        if (wrx && L.rxk && __ldg(g.row_flag + x)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (L.rxk & (1u << c)) {
+              const int slot = __ldg(g.node_slot + orow + L.z4 + c);
+              if (slot >= 0) rec_t[(size_t)lu * g.M + slot] = (float)v[c];
+            }
+        }
+        if (MODE == 2) {
+          float* st = strip_t + (size_t)lu * g.SL;
+          if (x == g.x_lo - 1 || x == g.x_hi + 1) {
+            const int base = (x == g.x_lo - 1 ? 0 : g.Lz) - g.z_lo + L.z4;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (L.boxk & (1u << c)) st[base + c] = (float)v[c];
+          } else if (wring && x >= g.x_lo && x <= g.x_hi) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if (c == L.ringl) st[2 * g.Lz + x - g.x_lo] = (float)v[c];
+              if (c == L.ringr) st[2 * g.Lz + g.Lx + x - g.x_lo] = (float)v[c];
+            }
+          }
+        }
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+template <int MODE, int NSL>
+__global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
+    fwd_lean_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
+                    const float* __restrict__ u1, const float* u2, float* uo,
+                    float* __restrict__ rec_t, float* __restrict__ strip_t, int has1, int has2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LeanFwdRing<NSL>& ring = *reinterpret_cast<LeanFwdRing<NSL>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int z0 = blockIdx.x * 128;
+  const int x0 = (blockIdx.y * kLeanWarps + warp) * TX;
+  if (x0 >= g.nx) return;  // warp-uniform
+  const int x1 = min(g.nx, x0 + TX);
+  const int lu = blockIdx.z;
+  const int u = unit_begin + lu;
+  const int b = u / g.S;
+  const int s = u - b * g.S;
+  const size_t N2 = (size_t)g.nx * g.nz;
+  const LaneInfo L = lane_info(g, T, z0 + 4 * lane);
+  const int txx = __ldg(g.tx + 2 * s), txz = __ldg(g.tx + 2 * s + 1);
+  const int tk = (L.act && txz >= L.z4 && txz < L.z4 + 4) ? txz - L.z4 : -1;
+  const double pulse_t = __ldg(g.pulse + t);
+  const bool wrx = __any_sync(0xffffffffu, L.rxk != 0u);
+  const bool wring = __any_sync(0xffffffffu, L.ringl >= 0 || L.ringr >= 0);
+  const bool wzd = __any_sync(0xffffffffu, L.zd);
+  const float* f1 = u1 + (size_t)lu * N2;
+  const float* f2 = u2 + (size_t)lu * N2;
+  float* fo = uo + (size_t)lu * N2;
+  const double* Ed = m.Ed + (size_t)b * N2;
+  if (wzd)
+    fwd_lean_rows<MODE, NSL, true>(g, T, L, ring, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t, f1,
+                                   f2, Ed, fo, rec_t, strip_t, has1, has2, wrx, wring);
+  else
+    fwd_lean_rows<MODE, NSL, false>(g, T, L, ring, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t, f1,
+                                    f2, Ed, fo, rec_t, strip_t, has1, has2, wrx, wring);
+}
+
+// --------------------------------------------------------------- lam update
+// lam[t] = A lam[t+1] + L^T(E lam[t+1]) + B lam[t+2] (+ merged residual at the
+// receiver nodes), in place over lam[t+2] (adjoint.py:119-131).
+template <int NSL>
+struct LeanAdjRing {
+  float4 l1[NSL][kLeanWarps * 32];    // lam[t+1] row r+1
+  double2 e0[NSL][kLeanWarps * 32];   // E row r+1, cells 0-1
+  double2 e1[NSL][kLeanWarps * 32];   // E row r+1, cells 2-3
+  float4 l2[NSL][kLeanWarps * 32];    // lam[t+2] row r
+  float edl[NSL][kLeanWarps * 32];    // lam[t+1] row r+1 at the lane's edge column
+  double ede[NSL][kLeanWarps * 32];   // E row r+1 at the lane's edge column
+};
+
+template <int NSL, bool ZD>
+__device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T,
+                                                 const LaneInfo& L, LeanAdjRing<NSL>& ring,
+                                                 int tid, int lane, int z0, int x0, int x1,
+                                                 int lu, const float* L1, float* L2,
+                                                 const double* Ed, const double* rres_t,
+                                                 bool has1, bool has2, bool wrx) {
+  const int nz = g.nz, nx = g.nx;
+  const int zc = L.act ? L.z4 : 0;
+  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < g.nz;
+  const bool has_edge = edge_l || edge_r;
+  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + 128 : 0;
+  const bool ok1 = has1 && L.act, ok2 = has2 && L.act;
+  const float* b1 = opaque(L1 + zc);
+  float* b2 = opaque(L2 + zc);
+  const double* be = opaque(Ed + zc);
+  const float* bl = opaque(L1 + ze);
+  const double* bel = opaque(Ed + ze);
+  double Az[4], Bz[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    Az[k] = 2.0;
+    Bz[k] = -1.0;
+    if (ZD && L.act && L.zd) {
+      Az[k] = __ldg(T.Az + L.z4 + k);
+      Bz[k] = __ldg(T.Bz + L.z4 + k);
+    }
+  }
+  auto issue = [&](int r, int sl) {
+    const bool okn = r + 1 < nx;
+    const int on = okn ? (r + 1) * nz : 0;
+    const int orr = r * nz;
+    cp16(&ring.l1[sl][tid], b1 + on, ok1 && okn);
+    cp16(&ring.e0[sl][tid], be + on, L.act && okn);
+    cp16(&ring.e1[sl][tid], be + on + 2, L.act && okn);
+    cp16(&ring.l2[sl][tid], b2 + orr, ok2);
+    cp4(&ring.edl[sl][tid], bl + on, has1 && has_edge && okn);
+    cp8(&ring.ede[sl][tid], bel + on, has_edge && okn);
+  };
+  // window of E*lam1 (EL) and raw lam1 (RL): slot (k)%3 = row x-1, (k+1)%3 = x, (k+2)%3 = x+1
+  double EL[3][4], RL[3][4], EG[3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) EL[0][k] = EL[1][k] = EL[2][k] = RL[0][k] = RL[1][k] = RL[2][k] = 0.0;
+  EG[0] = EG[1] = EG[2] = 0.0;
+  if (has1) {
+    auto ld = [&](int x, int w) {
+      if (L.act) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(b1 + x * nz));
+        const double2 a = __ldg(reinterpret_cast<const double2*>(be + x * nz));
+        const double2 c = __ldg(reinterpret_cast<const double2*>(be + x * nz + 2));
+        RL[w][0] = f.x; RL[w][1] = f.y; RL[w][2] = f.z; RL[w][3] = f.w;
+        EL[w][0] = __dmul_rn(a.x, RL[w][0]);
+        EL[w][1] = __dmul_rn(a.y, RL[w][1]);
+        EL[w][2] = __dmul_rn(c.x, RL[w][2]);
+        EL[w][3] = __dmul_rn(c.y, RL[w][3]);
+      }
+      if (has_edge) EG[w] = __dmul_rn(__ldg(bel + x * nz), (double)__ldg(bl + x * nz));
+    };
+    if (x0 >= 1) ld(x0 - 1, 0);
+    ld(x0, 1);
+  }
+#pragma unroll
+  for (int k = 0; k < NSL - 1; ++k) {
+    if (x0 + k < x1) issue(x0 + k, k);
+    cp_commit();
+  }
+  for (int xb = x0; xb < x1; xb += NSL) {
+#pragma unroll
+    for (int k = 0; k < NSL; ++k) {
+      const int x = xb + k;
+      if (x >= x1) break;
+      const int im = k % 3, ic = (k + 1) % 3, ip = (k + 2) % 3;
+      if (x + NSL - 1 < x1) issue(x + NSL - 1, (k + NSL - 1) % NSL);
+      cp_commit();
+      cp_wait<NSL - 1>();
+      {
+        const float4 f = ring.l1[k][tid];
+        const double2 a = ring.e0[k][tid], c = ring.e1[k][tid];
+        RL[ip][0] = f.x; RL[ip][1] = f.y; RL[ip][2] = f.z; RL[ip][3] = f.w;
+        EL[ip][0] = __dmul_rn(a.x, RL[ip][0]);
+        EL[ip][1] = __dmul_rn(a.y, RL[ip][1]);
+        EL[ip][2] = __dmul_rn(c.x, RL[ip][2]);
+        EL[ip][3] = __dmul_rn(c.y, RL[ip][3]);
+        EG[ip] = __dmul_rn(ring.ede[k][tid], (double)ring.edl[k][tid]);
+      }
+      const float4 w2 = ring.l2[k][tid];
+      const double l2v[4] = {w2.x, w2.y, w2.z, w2.w};
+      double zl = __shfl_up_sync(0xffffffffu, EL[ic][3], 1);
+      double zr = __shfl_down_sync(0xffffffffu, EL[ic][0], 1);
+      if (lane == 0) zl = EG[ic];
+      if (lane == 31) zr = EG[ic];
+      double lam[4];
+      if (x >= g.x_lo && x <= g.x_hi) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double zm = c == 0 ? zl : EL[ic][c - 1];
+          const double zp = c == 3 ? zr : EL[ic][c + 1];
+          const double adj = lap5(EL[ic][c], EL[im][c], EL[ip][c], zm, zp);
+          lam[c] = ZD ? adj_update(Az[c], Bz[c], RL[ic][c], l2v[c], adj)
+                      : adj_update_free(RL[ic][c], l2v[c], adj);
+        }
+      } else {
+        const double pxx = __ldg(T.px + x), Axx = __ldg(T.Ax + x), Bxx = __ldg(T.Bx + x);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double zm = c == 0 ? zl : EL[ic][c - 1];
+          const double zp = c == 3 ? zr : EL[ic][c + 1];
+          const double adj = lap5(EL[ic][c], EL[im][c], EL[ip][c], zm, zp);
+          const double2 ab = ab_row_damped(T, pxx, Axx, Bxx, min(L.z4 + c, nz - 1));
+          lam[c] = adj_update(ab.x, ab.y, RL[ic][c], l2v[c], adj);
+        }
+      }
+      if (L.act) {
+        const int orow = x * nz;
+        if (wrx && L.rxk && __ldg(g.row_flag + x)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (L.rxk & (1u << c)) {
+              const int slot = __ldg(g.node_slot + orow + L.z4 + c);
+              if (slot >= 0) lam[c] = __dadd_rn(lam[c], __ldg(rres_t + (size_t)lu * g.M + slot));
+            }
+        }
+        *reinterpret_cast<float4*>(b2 + orow) =
+            make_float4((float)lam[0], (float)lam[1], (float)lam[2], (float)lam[3]);
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+template <int NSL>
+__global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
+    adjlam_lean_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
+                       const float* __restrict__ l1, float* l2o, const double* __restrict__ rres_t,
+                       int has1, int has2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LeanAdjRing<NSL>& ring = *reinterpret_cast<LeanAdjRing<NSL>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int z0 = blockIdx.x * 128;
+  const int x0 = (blockIdx.y * kLeanWarps + warp) * TX;
+  if (x0 >= g.nx) return;  // warp-uniform
+  const int x1 = min(g.nx, x0 + TX);
+  const int lu = blockIdx.z;
+  const int b = (unit_begin + lu) / g.S;
+  const size_t N2 = (size_t)g.nx * g.nz;
+  const LaneInfo L = lane_info(g, T, z0 + 4 * lane);
+  const bool wrx = __any_sync(0xffffffffu, L.rxk != 0u);
+  const bool wzd = __any_sync(0xffffffffu, L.zd);
+  const float* L1 = l1 + (size_t)lu * N2;
+  float* L2 = l2o + (size_t)lu * N2;
+  const double* Ed = m.Ed + (size_t)b * N2;
+  if (wzd)
+    adjlam_lean_rows<NSL, true>(g, T, L, ring, tid, lane, z0, x0, x1, lu, L1, L2, Ed, rres_t,
+                                has1, has2, wrx);
+  else
+    adjlam_lean_rows<NSL, false>(g, T, L, ring, tid, lane, z0, x0, x1, lu, L1, L2, Ed, rres_t,
+                                 has1, has2, wrx);
+}
+
+
+// ------------------------------------------------------ imaging + reconstruction
+// sum_t L(u[t-1]) lam[t] over a group of gs shots of one phantom (adjoint.py:128-130)
+// and, MODE 2, the reconstruction u[t-2] = 2 u[t-1] + E L u[t-1] + s[t] d_tx - u[t]
+// in place over u[t] on the undamped box.
+//
+// A warp owns a 128-wide z strip x kImgTX box rows and walks the group's shots
+// one after the other as ONE stream of ring items (kImgTX + 2 per shot): item i
+// of a shot carries u[t-1] row x0-1+i (+ the lane's edge value) and, for i >= 2,
+// lam[t], u[t] and E of row x0+i-2, so the pipeline never drains between shots.
+// The imaging sums of the warp's kImgTX x 4 cells per lane stay in registers for
+// the whole group; one f64 read-modify-write of acc_part[group] per cell at the end.
+//
+// MODE 2 keeps u[t-1] complete on the box AND its 1-cell ring in the field
+// buffer: the reconstruction writes the box cells of u[t-2], and the ring cells
+// of u[t-2] are copied from strips[t-2] (lanes on ring columns inline, the first
+// and last warps for the ring rows).  The forward leaves u[nt-1], u[nt-2] complete,
+// so the stencil of every box cell reads the field buffer only.
+// MODE 1 reads u[t-1] from the full history (F = hist[t-1]) over the whole grid.
+// DRAM per cell update: MODE 2 read u[t-1], u[t], lam[t], write u[t-2] = 16 B
+// (+16 B / gs for the accumulator); MODE 1 read u[t-1], lam[t] = 8 B.
+constexpr int kImgTX = 4;
+constexpr int kImgItems = kImgTX + 2;  // ring items per shot (multiple of 3)
+static_assert(kImgItems % 3 == 0, "ring/window rotation needs items % 3 == 0");
+
+struct LeanImgRing {
+  float4 u1[3][kLeanWarps * 32];    // u[t-1] row x0-1+i
+  float4 lam[3][kLeanWarps * 32];   // lam[t] row x0+i-2
+  float4 ut[3][kLeanWarps * 32];    // u[t] row x0+i-2 (MODE 2)
+  double2 e0[3][kLeanWarps * 32];   // E row x0+i-2, cells 0-1 (MODE 2)
+  double2 e1[3][kLeanWarps * 32];   // cells 2-3
+  float edge[3][kLeanWarps * 32];   // u[t-1] row x0-1+i at the lane's edge column
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
+    img_lean_kernel(Geo g, Model m, int t, int unit_begin, int U, int gs,
+                    const float* __restrict__ lam_t, const float* __restrict__ F, float* ut,
+                    const float* __restrict__ utm1, const float* __restrict__ strip_tm2,
+                    double* __restrict__ acc_part, int do_recon) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LeanImgRing& ring = *reinterpret_cast<LeanImgRing*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int nz = g.nz, nx = g.nx;
+  const int z0 = blockIdx.x * 128;
+  const int rlo = MODE == 2 ? g.x_lo : 0, rhi = MODE == 2 ? g.x_hi + 1 : nx;  // rows [rlo, rhi)
+  const int x0 = rlo + (blockIdx.y * kLeanWarps + warp) * kImgTX;
+  if (x0 >= rhi) return;  // warp-uniform
+  const int x1 = min(rhi, x0 + kImgTX);
+  const ShotGroup sg = shot_group(g, blockIdx.z, unit_begin, U, gs);
+  if (sg.n == 0) return;
+  const size_t N2 = (size_t)nx * nz;
+  const int z4 = z0 + 4 * lane;
+  const bool act = z4 < nz;
+  const int zc = act ? z4 : 0;
+  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
+  const bool has_edge = edge_l || edge_r;
+  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + 128 : 0;
+  unsigned boxk = 0u;
+  int ringl = -1, ringr = -1;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int z = z4 + k;
+    if (MODE == 1 ? act : (act && z >= g.z_lo && z <= g.z_hi)) boxk |= 1u << k;
+    if (MODE == 2 && act && z == g.z_lo - 1) ringl = k;
+    if (MODE == 2 && act && z == g.z_hi + 1) ringr = k;
+  }
+  const bool recon_on = MODE == 2 && do_recon;
+  const double pulse_t = __ldg(g.pulse + t);
+  const double* Ed = m.Ed + (size_t)sg.b * N2;
+  const double* be = opaque(Ed + zc);
+  // row r of the u[t-1] field / lam / u[t] of chunk-local unit lu
+  const float* U1 = MODE == 1 ? F : utm1;
+  auto issue = [&](int k, int i, int sl) {  // item i of the group's k-th shot
+    if (k >= sg.n) return;
+    const size_t fo = (size_t)(sg.lu0 + k) * N2;
+    const int ru = x0 - 1 + i;  // u[t-1] row
+    const bool oku = ru >= 0 && ru < nx && (MODE == 1 || (ru >= g.x_lo - 1 && ru <= g.x_hi + 1));
+    const int ou = oku ? ru * nz : 0;
+    cp16(&ring.u1[sl][tid], U1 + fo + zc + ou, oku && act);
+    cp4(&ring.edge[sl][tid], U1 + fo + ze + ou, oku && has_edge);
+    if (i >= 2) {
+      const int rx = x0 + i - 2;
+      const bool okx = rx < x1;
+      const int ox = okx ? rx * nz : 0;
+      cp16(&ring.lam[sl][tid], lam_t + fo + zc + ox, okx && act);
+      if (recon_on) {
+        cp16(&ring.ut[sl][tid], ut + fo + zc + ox, okx && act);
+        cp16(&ring.e0[sl][tid], be + ox, okx && act);
+        cp16(&ring.e1[sl][tid], be + ox + 2, okx && act);
+      }
+    }
+  };
+  double acc[kImgTX][4];
+#pragma unroll
+  for (int r = 0; r < kImgTX; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  // prologue: items 0, 1 of shot 0
+  issue(0, 0, 0);
+  cp_commit();
+  issue(0, 1, 1);
+  cp_commit();
+  double W[3][4], Eg[3];
+  for (int k = 0; k < sg.n; ++k) {
+    const int lu = sg.lu0 + k;
+    const int s = (unit_begin + lu) % g.S;
+    const int txx = __ldg(g.tx + 2 * s), txz = __ldg(g.tx + 2 * s + 1);
+    const int tk = (act && txz >= z4 && txz < z4 + 4) ? txz - z4 : -1;
+    float* uo = ut + (size_t)lu * N2 + zc;
+    const float* st = MODE == 2 ? strip_tm2 + (size_t)lu * g.SL : nullptr;
+#pragma unroll
+    for (int i = 0; i < kImgItems; ++i) {
+      const int sl = i % 3;
+      // keep two items in flight: item i+2 of this shot or of the next one
+      if (i + 2 < kImgItems) issue(k, i + 2, (i + 2) % 3);
+      else issue(k + 1, i + 2 - kImgItems, (i + 2) % 3);
+      cp_commit();
+      cp_wait<2>();
+      {
+        const float4 f = ring.u1[sl][tid];
+        W[sl][0] = f.x; W[sl][1] = f.y; W[sl][2] = f.z; W[sl][3] = f.w;
+        Eg[sl] = (double)ring.edge[sl][tid];
+      }
+      if (i < 2) continue;
+      const int r = i - 2;
+      const int x = x0 + r;
+      const int im = (i + 1) % 3, ic = (i + 2) % 3, ip = i % 3;  // rows x-1, x, x+1
+      double zl = __shfl_up_sync(0xffffffffu, W[ic][3], 1);
+      double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1);
+      if (lane == 0) zl = Eg[ic];
+      if (lane == 31) zr = Eg[ic];
+      if (x >= x1) continue;  // warp-uniform (last row block)
+      const float4 lf = ring.lam[sl][tid];
+      const double lam[4] = {lf.x, lf.y, lf.z, lf.w};
+      double lapu[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double zm = c == 0 ? zl : W[ic][c - 1];
+        const double zp = c == 3 ? zr : W[ic][c + 1];
+        lapu[c] = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
+        if (boxk & (1u << c)) acc[r][c] = __fma_rn(lapu[c], lam[c], acc[r][c]);
+      }
+      if (recon_on && act) {
+        const float4 uf = ring.ut[sl][tid];
+        const double2 e0 = ring.e0[sl][tid], e1 = ring.e1[sl][tid];
+        const double ua[4] = {uf.x, uf.y, uf.z, uf.w};
+        const double ed[4] = {e0.x, e0.y, e1.x, e1.y};
+        float o[4] = {uf.x, uf.y, uf.z, uf.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (boxk & (1u << c)) {
+            double prev = recon(W[ic][c], ua[c], ed[c], lapu[c]);
+            if (x == txx && c == tk) prev = __dadd_rn(prev, pulse_t);
+            o[c] = (float)prev;
+          }
+          if (c == ringl) o[c] = __ldg(st + 2 * g.Lz + x - g.x_lo);
+          if (c == ringr) o[c] = __ldg(st + 2 * g.Lz + g.Lx + x - g.x_lo);
+        }
+        *reinterpret_cast<float4*>(uo + x * nz) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    if (recon_on && act) {  // ring rows of u[t-2]
+      if (x0 == g.x_lo && g.x_lo > 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (boxk & (1u << c)) uo[(g.x_lo - 1) * nz + c] = __ldg(st + z4 + c - g.z_lo);
+      }
+      if (x1 == g.x_hi + 1 && g.x_hi + 1 < nx) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (boxk & (1u << c)) uo[(g.x_hi + 1) * nz + c] = __ldg(st + g.Lz + z4 + c - g.z_lo);
+      }
+    }
+  }
+  cp_wait<0>();
+  if (act) {
+    double* dst = acc_part + (size_t)blockIdx.z * N2 + zc;
+#pragma unroll
+    for (int r = 0; r < kImgTX; ++r) {
+      if (x0 + r >= x1) break;
+      double2* p = reinterpret_cast<double2*>(dst + (x0 + r) * nz);
+      double2 a = p[0], b = p[1];
+      a.x += acc[r][0]; a.y += acc[r][1]; b.x += acc[r][2]; b.y += acc[r][3];
+      p[0] = a;
+      p[1] = b;
+    }
+  }
+}
+}  // namespace dufwi
