@@ -66,6 +66,7 @@ struct dufwi_plan {
   ClusterCfg ccfg{};                // the shape for all units at once (plan_info)
   bool cluster_ok = false;
   int lean_nsl = 3;  // ring depth of the lean stepwise kernels (0: use the vec kernels)
+  int img_nsl = 3;   // ring depth of the lean imaging kernel
 };
 
 namespace {
@@ -364,6 +365,7 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.col_flag = p->col_flag;
   if (const char* e = getenv("DUFWI_LEAN_NSL")) p->lean_nsl = atoi(e);
   if (p->lean_nsl != 0 && p->lean_nsl != 3 && p->lean_nsl != 6) p->lean_nsl = 3;
+  if (const char* e = getenv("DUFWI_IMG_NSL")) p->img_nsl = atoi(e) == 6 ? 6 : 3;
   {  // lean rings may exceed the 48 KB default of dynamic shared memory
     for (auto f : {fwd_lean_kernel<0, 3>, fwd_lean_kernel<1, 3>, fwd_lean_kernel<2, 3>})
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanFwdRing<3>));
@@ -373,8 +375,10 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
                          sizeof(LeanAdjRing<3>));
     cudaFuncSetAttribute(adjlam_lean_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          sizeof(LeanAdjRing<6>));
-    for (auto f : {img_lean_kernel<1>, img_lean_kernel<2>})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanImgRing));
+    for (auto f : {img_lean_kernel<1, 3>, img_lean_kernel<2, 3>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanImgRing<3>));
+    for (auto f : {img_lean_kernel<1, 6>, img_lean_kernel<2, 6>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanImgRing<6>));
   }
   p->cluster_ok = cluster_candidates(g, p->has_rho != 0, rx_nodes, p->ccands);
   if (p->cluster_ok) p->ccfg = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots);
@@ -639,12 +643,16 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
         const dim3 igrid((g.nz + 127) / 128, (rows + kLeanWarps * kImgTX - 1) / (kLeanWarps * kImgTX),
                          G.ngroups);
         const float* st_tm2 = (mode == DUFWI_STORE_STRIPS && do_recon) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
-        if (mode == DUFWI_STORE_FULL)
-          img_lean_kernel<1><<<igrid, kLeanWarps * 32, sizeof(LeanImgRing), st>>>(
-              g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm2, acc_part, do_recon);
-        else
-          img_lean_kernel<2><<<igrid, kLeanWarps * 32, sizeof(LeanImgRing), st>>>(
-              g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm2, acc_part, do_recon);
+#define DUFWI_IMG(M, NS)                                                                        \
+  img_lean_kernel<M, NS><<<igrid, kLeanWarps * 32, sizeof(LeanImgRing<NS>), st>>>(               \
+      g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm2, acc_part, do_recon)
+        const int ins = p->img_nsl;
+        if (mode == DUFWI_STORE_FULL) {
+          if (ins == 6) DUFWI_IMG(1, 6); else DUFWI_IMG(1, 3);
+        } else {
+          if (ins == 6) DUFWI_IMG(2, 6); else DUFWI_IMG(2, 3);
+        }
+#undef DUFWI_IMG
         LAUNCH_CHECK(p);
       } else if (do_img) {
         const dim3 igrid((g.nz + 127) / 128,

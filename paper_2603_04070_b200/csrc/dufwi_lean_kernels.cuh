@@ -31,7 +31,7 @@ namespace dufwi {
 #define DUFWI_LEAN_WARPS 4
 #endif
 #ifndef DUFWI_LEAN_MINB
-#define DUFWI_LEAN_MINB 1
+#define DUFWI_LEAN_MINB 4
 #endif
 constexpr int kLeanWarps = DUFWI_LEAN_WARPS;  // warps per CTA
 constexpr int kLeanMinB = DUFWI_LEAN_MINB;    // min resident CTAs per SM (register cap)
@@ -474,23 +474,25 @@ constexpr int kImgTX = 4;
 constexpr int kImgItems = kImgTX + 2;  // ring items per shot (multiple of 3)
 static_assert(kImgItems % 3 == 0, "ring/window rotation needs items % 3 == 0");
 
+template <int NSL>  // ring slots: 3 or 6 (divides kImgItems)
 struct LeanImgRing {
-  float4 u1[3][kLeanWarps * 32];    // u[t-1] row x0-1+i
-  float4 lam[3][kLeanWarps * 32];   // lam[t] row x0+i-2
-  float4 ut[3][kLeanWarps * 32];    // u[t] row x0+i-2 (MODE 2)
-  double2 e0[3][kLeanWarps * 32];   // E row x0+i-2, cells 0-1 (MODE 2)
-  double2 e1[3][kLeanWarps * 32];   // cells 2-3
-  float edge[3][kLeanWarps * 32];   // u[t-1] row x0-1+i at the lane's edge column
+  float4 u1[NSL][kLeanWarps * 32];    // u[t-1] row x0-1+i
+  float4 lam[NSL][kLeanWarps * 32];   // lam[t] row x0+i-2
+  float4 ut[NSL][kLeanWarps * 32];    // u[t] row x0+i-2 (MODE 2)
+  double2 e0[NSL][kLeanWarps * 32];   // E row x0+i-2, cells 0-1 (MODE 2)
+  double2 e1[NSL][kLeanWarps * 32];   // cells 2-3
+  float edge[NSL][kLeanWarps * 32];   // u[t-1] row x0-1+i at the lane's edge column
 };
 
-template <int MODE>
+template <int MODE, int NSL>
 __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
     img_lean_kernel(Geo g, Model m, int t, int unit_begin, int U, int gs,
                     const float* __restrict__ lam_t, const float* __restrict__ F, float* ut,
                     const float* __restrict__ utm1, const float* __restrict__ strip_tm2,
                     double* __restrict__ acc_part, int do_recon) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LeanImgRing& ring = *reinterpret_cast<LeanImgRing*>(smem_raw);
+  static_assert(kImgItems % NSL == 0, "ring slots must divide the items per shot");
+  LeanImgRing<NSL>& ring = *reinterpret_cast<LeanImgRing<NSL>*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -549,11 +551,12 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
   for (int r = 0; r < kImgTX; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-  // prologue: items 0, 1 of shot 0
-  issue(0, 0, 0);
-  cp_commit();
-  issue(0, 1, 1);
-  cp_commit();
+  // prologue: items 0 .. NSL-2 of shot 0
+#pragma unroll
+  for (int i = 0; i < NSL - 1; ++i) {
+    issue(0, i, i);
+    cp_commit();
+  }
   double W[3][4], Eg[3];
   for (int k = 0; k < sg.n; ++k) {
     const int lu = sg.lu0 + k;
@@ -564,16 +567,16 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
     const float* st = MODE == 2 ? strip_tm2 + (size_t)lu * g.SL : nullptr;
 #pragma unroll
     for (int i = 0; i < kImgItems; ++i) {
-      const int sl = i % 3;
-      // keep two items in flight: item i+2 of this shot or of the next one
-      if (i + 2 < kImgItems) issue(k, i + 2, (i + 2) % 3);
-      else issue(k + 1, i + 2 - kImgItems, (i + 2) % 3);
+      const int sl = i % NSL, wi = i % 3;
+      // keep NSL-1 items in flight: item i+NSL-1 of this shot or of the next one
+      if (i + NSL - 1 < kImgItems) issue(k, i + NSL - 1, (i + NSL - 1) % NSL);
+      else issue(k + 1, i + NSL - 1 - kImgItems, (i + NSL - 1) % NSL);
       cp_commit();
-      cp_wait<2>();
+      cp_wait<NSL - 1>();
       {
         const float4 f = ring.u1[sl][tid];
-        W[sl][0] = f.x; W[sl][1] = f.y; W[sl][2] = f.z; W[sl][3] = f.w;
-        Eg[sl] = (double)ring.edge[sl][tid];
+        W[wi][0] = f.x; W[wi][1] = f.y; W[wi][2] = f.z; W[wi][3] = f.w;
+        Eg[wi] = (double)ring.edge[sl][tid];
       }
       if (i < 2) continue;
       const int r = i - 2;
