@@ -32,6 +32,32 @@ __global__ void set_model_kernel(Geo g, const double* __restrict__ c, const doub
   (void)inv_dx2_div;
 }
 
+// Density tables of the lean kernels (see Model): Er = rho * Ed, face factors
+// f = 0.5 * (q_c + q_j) as in the oracle's rho_face_weights, outer faces = own q.
+__global__ void rho_faces_kernel(Geo g, int B, const double* __restrict__ Ed,
+                                 const double* __restrict__ rho, const double* __restrict__ q,
+                                 double* __restrict__ Er, double* __restrict__ fxe,
+                                 double* __restrict__ fz, double* __restrict__ fz0) {
+  const int nx = g.nx, nz = g.nz;
+  const size_t N2 = (size_t)nx * nz, NE = N2 + nz;
+  const size_t total = (size_t)B * NE;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / NE);
+    const size_t e = i % NE;
+    const int r = (int)(e / nz), z = (int)(e % nz);  // r in [0, nx]
+    const double* qb = q + (size_t)b * N2;
+    fxe[i] = r == 0 ? qb[z] : r == nx ? qb[(size_t)(nx - 1) * nz + z]
+                                      : 0.5 * (qb[(size_t)(r - 1) * nz + z] + qb[(size_t)r * nz + z]);
+    if (r < nx) {
+      const size_t c = (size_t)b * N2 + (size_t)r * nz + z;
+      Er[c] = rho[c] * Ed[c];
+      fz[c] = z == nz - 1 ? q[c] : 0.5 * (q[c] + q[c + 1]);
+      if (z == 0) fz0[(size_t)b * nx + r] = q[c];
+    }
+  }
+}
+
 // traces[lu][r][t] = rec[t][lu][slot(s, r)] — the (P,R,nt) ChannelData layout
 // (grid.py:164-183).  Flags non-finite samples (forward.py:309-310).
 __global__ void gather_traces_kernel(Geo g, int unit_begin, int U, const float* __restrict__ rec,
@@ -113,7 +139,7 @@ __global__ void misfit_sum_kernel(Geo g, int unit_begin, int U, const double* __
 // then `gpp` per further phantom (empty tail groups hold zeros).
 __global__ void reduce_groups_kernel(Geo g, int b0, int nb, int first, int gpp,
                                      const double* __restrict__ acc_part,
-                                     double* __restrict__ acc) {
+                                     double* __restrict__ acc, const double* __restrict__ scale) {
   const size_t N2 = (size_t)g.nx * g.nz;
   const size_t total = (size_t)nb * N2;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
@@ -124,6 +150,8 @@ __global__ void reduce_groups_kernel(Geo g, int b0, int nb, int first, int gpp,
     const int g1 = bl == 0 ? first : g0 + gpp;
     double sum = 0.0;
     for (int k = g0; k < g1; ++k) sum += acc_part[(size_t)k * N2 + cell];
+    // scale: rho for the lean density kernels, whose imaging sums D(u) lam (L_rho = rho D)
+    if (scale) sum = scale[(size_t)(b0 + bl) * N2 + cell] * sum;
     acc[(size_t)(b0 + bl) * N2 + cell] += sum;
   }
 }

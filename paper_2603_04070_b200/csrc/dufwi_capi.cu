@@ -65,8 +65,8 @@ struct dufwi_plan {
   std::vector<ClusterCfg> ccands;  // launch shapes that fit, one per cluster size
   ClusterCfg ccfg{};                // the shape for all units at once (plan_info)
   bool cluster_ok = false;
-  int lean_nsl = 3;  // ring depth of the lean stepwise kernels (0: use the vec kernels)
-  int img_nsl = 3;   // ring depth of the lean imaging kernel
+  bool lean_on = true;  // lean stepwise kernels (DUFWI_LEAN=0: the first vec/stream kernels)
+  double *Er = nullptr, *fxe = nullptr, *fz = nullptr, *fz0 = nullptr;  // density tables
 };
 
 namespace {
@@ -142,7 +142,11 @@ Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec, 
 // Vectorised stepwise kernels: constant density, rows made of whole float4s.
 bool use_vec(const dufwi_plan_t* p) { return !p->has_rho && p->geo.nz % 4 == 0; }
 // Lean kernels: additionally separable damping with a rectangular undamped box.
-bool use_lean(const dufwi_plan_t* p) { return use_vec(p) && p->ab.px && p->box_ok && p->lean_nsl > 0; }
+// Lean kernels: rows of whole float4s, separable damping with a rectangular
+// undamped box; constant or variable density.
+bool use_lean(const dufwi_plan_t* p) {
+  return p->geo.nz % 4 == 0 && p->ab.px && p->box_ok && p->lean_on;
+}
 
 Groups groups_for(const dufwi_plan_t* p, int unit_begin, int U, bool per_unit) {
   return adj_groups(p->geo, unit_begin, U, per_unit, use_vec(p), use_lean(p));
@@ -186,7 +190,9 @@ int max_groups(const dufwi_plan_t* p, int U, bool per_unit) {
   return std::max(best, 1);
 }
 
-Model model_of(const dufwi_plan_t* p) { return Model{p->Ed, p->has_rho ? p->rho : nullptr, p->q}; }
+Model model_of(const dufwi_plan_t* p) {
+  return Model{p->Ed, p->has_rho ? p->rho : nullptr, p->q, p->Er, p->fxe, p->fz, p->fz0};
+}
 
 int check_units(const dufwi_plan_t* p, int unit_begin, int U) {
   const int total = p->geo.B * p->geo.S;
@@ -345,6 +351,10 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   if (p->has_rho) {
     rc = rc ? rc : dev_alloc(p, &p->rho, BN2);
     rc = rc ? rc : dev_alloc(p, &p->q, BN2);
+    rc = rc ? rc : dev_alloc(p, &p->Er, BN2);
+    rc = rc ? rc : dev_alloc(p, &p->fxe, (size_t)g.B * (nx + 1) * nz);
+    rc = rc ? rc : dev_alloc(p, &p->fz, BN2);
+    rc = rc ? rc : dev_alloc(p, &p->fz0, (size_t)g.B * nx);
   }
   rc = rc ? rc : dev_alloc(p, &p->flag, 4);
   if (!rc && cudaMemset(p->flag, 0, 4 * sizeof(int)) != cudaSuccess)
@@ -363,22 +373,23 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.node_slot = p->node_slot;
   g.row_flag = p->row_flag;
   g.col_flag = p->col_flag;
-  if (const char* e = getenv("DUFWI_LEAN_NSL")) p->lean_nsl = atoi(e);
-  if (p->lean_nsl != 0 && p->lean_nsl != 3 && p->lean_nsl != 6) p->lean_nsl = 3;
-  if (const char* e = getenv("DUFWI_IMG_NSL")) p->img_nsl = atoi(e) == 6 ? 6 : 3;
+  if (const char* e = getenv("DUFWI_LEAN")) p->lean_on = atoi(e) != 0;
   {  // lean rings may exceed the 48 KB default of dynamic shared memory
-    for (auto f : {fwd_lean_kernel<0, 3>, fwd_lean_kernel<1, 3>, fwd_lean_kernel<2, 3>})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanFwdRing<3>));
-    for (auto f : {fwd_lean_kernel<0, 6>, fwd_lean_kernel<1, 6>, fwd_lean_kernel<2, 6>})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanFwdRing<6>));
-    cudaFuncSetAttribute(adjlam_lean_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         sizeof(LeanAdjRing<3>));
-    cudaFuncSetAttribute(adjlam_lean_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         sizeof(LeanAdjRing<6>));
-    for (auto f : {img_lean_kernel<1, 3>, img_lean_kernel<2, 3>})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanImgRing<3>));
-    for (auto f : {img_lean_kernel<1, 6>, img_lean_kernel<2, 6>})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(LeanImgRing<6>));
+    auto big = [](const void* f, size_t bytes) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    };
+    big((const void*)fwd_lean_kernel<0, false>, sizeof(LeanFwdRing<kNSL, false>));
+    big((const void*)fwd_lean_kernel<1, false>, sizeof(LeanFwdRing<kNSL, false>));
+    big((const void*)fwd_lean_kernel<2, false>, sizeof(LeanFwdRing<kNSL, false>));
+    big((const void*)fwd_lean_kernel<0, true>, sizeof(LeanFwdRing<kNSL, true>));
+    big((const void*)fwd_lean_kernel<1, true>, sizeof(LeanFwdRing<kNSL, true>));
+    big((const void*)fwd_lean_kernel<2, true>, sizeof(LeanFwdRing<kNSL, true>));
+    big((const void*)adjlam_lean_kernel<false>, sizeof(LeanAdjRing<kNSL, false>));
+    big((const void*)adjlam_lean_kernel<true>, sizeof(LeanAdjRing<kNSL, true>));
+    big((const void*)img_lean_kernel<1, false>, sizeof(LeanImgRing<false>));
+    big((const void*)img_lean_kernel<2, false>, sizeof(LeanImgRing<false>));
+    big((const void*)img_lean_kernel<1, true>, sizeof(LeanImgRing<true>));
+    big((const void*)img_lean_kernel<2, true>, sizeof(LeanImgRing<true>));
   }
   p->cluster_ok = cluster_candidates(g, p->has_rho != 0, rx_nodes, p->ccands);
   if (p->cluster_ok) p->ccfg = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots);
@@ -405,6 +416,13 @@ extern "C" int dufwi_set_model(dufwi_plan_t* p, const double* c_dev, const doubl
       g, c_dev, p->has_rho ? rho_dev : nullptr, p->Ed, p->dEdc, p->rho, p->q, 0.0,
       p->dx * p->dx, total);
   LAUNCH_CHECK(p);
+  if (p->has_rho) {
+    const size_t te = (size_t)g.B * (g.nx + 1) * g.nz;
+    const int b2 = (int)std::min<size_t>((te + threads - 1) / threads, 148 * 16);
+    rho_faces_kernel<<<b2, threads, 0, (cudaStream_t)stream>>>(g, g.B, p->Ed, p->rho, p->q, p->Er,
+                                                               p->fxe, p->fz, p->fz0);
+    LAUNCH_CHECK(p);
+  }
   return DUFWI_OK;
 }
 
@@ -508,14 +526,14 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
 #define DUFWI_VEC(M)                                                                            \
   fwd_vec_kernel<M><<<vgrid, kPipeWarps * 32, sizeof(FwdRing), st>>>(g, m, p->ab, t, unit_begin, \
                                                       vtx, u1, u2, uo, rec_t, st_t, has1, has2)
-#define DUFWI_LEAN(M, NS)                                                                       \
-  fwd_lean_kernel<M, NS><<<lgrid, kLeanWarps * 32, sizeof(LeanFwdRing<NS>), st>>>(               \
+#define DUFWI_LEAN(M, R)                                                                        \
+  fwd_lean_kernel<M, R><<<lgrid, kLeanT, sizeof(LeanFwdRing<kNSL, R>), st>>>(                     \
       g, m, p->ab, t, unit_begin, vtx, u1, u2, uo, rec_t, st_t, has1, has2)
       if (lean) {
-        if (p->lean_nsl == 6) {
-          if (mode == 0) DUFWI_LEAN(0, 6); else if (mode == 1) DUFWI_LEAN(1, 6); else DUFWI_LEAN(2, 6);
+        if (p->has_rho) {
+          if (mode == 0) DUFWI_LEAN(0, true); else if (mode == 1) DUFWI_LEAN(1, true); else DUFWI_LEAN(2, true);
         } else {
-          if (mode == 0) DUFWI_LEAN(0, 3); else if (mode == 1) DUFWI_LEAN(1, 3); else DUFWI_LEAN(2, 3);
+          if (mode == 0) DUFWI_LEAN(0, false); else if (mode == 1) DUFWI_LEAN(1, false); else DUFWI_LEAN(2, false);
         }
       } else if (vec) {
         if (mode == 0) DUFWI_VEC(0); else if (mode == 1) DUFWI_VEC(1); else DUFWI_VEC(2);
@@ -617,44 +635,45 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     const float* utm1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
     const float* st_tm1 = (mode == DUFWI_STORE_STRIPS && do_img) ? strips + (size_t)(t - 1) * U * g.SL : nullptr;
     const int do_recon = t >= 2;
-    if (use_vec(p)) {
+    int vtx = 4;  // rows per warp of the lam update: enough warps for the device
+    for (int c : {32, 16, 8, 4}) {
+      const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
+      if (warps >= 148L * 32) { vtx = c; break; }
+    }
+    if (use_lean(p)) {
       // split adjoint: lam update (12 B/update) then imaging + reconstruction
-      int vtx = 4;
-      for (int c : {32, 16, 8, 4}) {
-        const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
-        if (warps >= 148L * 32) { vtx = c; break; }
-      }
-      if (use_lean(p)) {
-        const dim3 lgrid((g.nz + 127) / 128, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx), U);
-        if (p->lean_nsl == 6)
-          adjlam_lean_kernel<6><<<lgrid, kLeanWarps * 32, sizeof(LeanAdjRing<6>), st>>>(
-              g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
-        else
-          adjlam_lean_kernel<3><<<lgrid, kLeanWarps * 32, sizeof(LeanAdjRing<3>), st>>>(
-              g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
-      } else {
-        const dim3 lgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
-        adjlam_pipe_kernel<<<lgrid, kPipeWarps * 32, sizeof(AdjRing), st>>>(
+      const dim3 lgrid((g.nz + 127) / 128, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx), U);
+      if (p->has_rho)
+        adjlam_lean_kernel<true><<<lgrid, kLeanT, sizeof(LeanAdjRing<kNSL, true>), st>>>(
             g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
-      }
+      else
+        adjlam_lean_kernel<false><<<lgrid, kLeanT, sizeof(LeanAdjRing<kNSL, false>), st>>>(
+            g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
       LAUNCH_CHECK(p);
-      if (do_img && use_lean(p)) {
+      if (do_img) {
         const int rows = mode == DUFWI_STORE_STRIPS ? g.Lx : g.nx;
         const dim3 igrid((g.nz + 127) / 128, (rows + kLeanWarps * kImgTX - 1) / (kLeanWarps * kImgTX),
                          G.ngroups);
         const float* st_tm2 = (mode == DUFWI_STORE_STRIPS && do_recon) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
-#define DUFWI_IMG(M, NS)                                                                        \
-  img_lean_kernel<M, NS><<<igrid, kLeanWarps * 32, sizeof(LeanImgRing<NS>), st>>>(               \
+#define DUFWI_IMG(M, R)                                                                         \
+  img_lean_kernel<M, R><<<igrid, kLeanT, sizeof(LeanImgRing<R>), st>>>(                          \
       g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm2, acc_part, do_recon)
-        const int ins = p->img_nsl;
         if (mode == DUFWI_STORE_FULL) {
-          if (ins == 6) DUFWI_IMG(1, 6); else DUFWI_IMG(1, 3);
+          if (p->has_rho) DUFWI_IMG(1, true); else DUFWI_IMG(1, false);
         } else {
-          if (ins == 6) DUFWI_IMG(2, 6); else DUFWI_IMG(2, 3);
+          if (p->has_rho) DUFWI_IMG(2, true); else DUFWI_IMG(2, false);
         }
 #undef DUFWI_IMG
         LAUNCH_CHECK(p);
-      } else if (do_img) {
+      }
+      continue;
+    }
+    if (use_vec(p)) {
+      const dim3 lgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
+      adjlam_pipe_kernel<<<lgrid, kPipeWarps * 32, sizeof(AdjRing), st>>>(
+          g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
+      LAUNCH_CHECK(p);
+      if (do_img) {
         const dim3 igrid((g.nz + 127) / 128,
                          (g.nx + kVecAdjWarps * kVecAdjTX - 1) / (kVecAdjWarps * kVecAdjTX), G.ngroups);
         if (mode == DUFWI_STORE_FULL)
@@ -681,7 +700,10 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   {
     const size_t total = (size_t)G.nb * N2;
     const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
-    reduce_groups_kernel<<<blocks, 256, 0, st>>>(g, G.b0, G.nb, G.first, G.gpp, acc_part, acc_dev);
+    // the lean density kernels sum D(u) lam; L_rho = rho D: scale by rho once here
+    const double* scale = (!clus && p->has_rho && use_lean(p)) ? p->rho : nullptr;
+    reduce_groups_kernel<<<blocks, 256, 0, st>>>(g, G.b0, G.nb, G.first, G.gpp, acc_part, acc_dev,
+                                                 scale);
     LAUNCH_CHECK(p);
   }
   return DUFWI_OK;

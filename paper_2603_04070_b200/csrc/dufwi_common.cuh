@@ -33,6 +33,11 @@ struct Model {
   const double* Ed;    // [B][nx][nz]  c^2 dt^2 / (1 + D dt) / dx^2
   const double* rho;   // [B][nx][nz]  density or nullptr
   const double* q;     // [B][nx][nz]  1/rho
+  // density operator tables of the lean stepwise kernels (dufwi_lean_kernels.cuh)
+  const double* Er;    // [B][nx][nz]    rho E / dx^2
+  const double* fxe;   // [B][nx+1][nz]  x faces (q_{x-1} + q_x)/2; rows 0 and nx: outer = own q
+  const double* fz;    // [B][nx][nz]    z faces (q_z + q_{z+1})/2; z = nz-1: outer = own q
+  const double* fz0;   // [B][nx]        outer z face left of z = 0: q(x, 0)
 };
 
 __device__ __forceinline__ double damping_at(const Geo& g, int x, int z) {

@@ -1,26 +1,41 @@
-// Stepwise engine, lean streaming kernels (constant density, nz % 4 == 0,
-// separable damping with a rectangular undamped box: every BASELINE config
-// without density, e.g. config 4).
+// Stepwise engine, lean streaming kernels (nz % 4 == 0, separable damping with
+// a rectangular undamped box: every BASELINE config, configs 2/3 with density).
 //
-// Same data movement as fwd_vec_kernel / adjlam_pipe_kernel — a warp owns a
-// 128-wide z strip (4 cells per lane, float4 loads/stores) and walks TX x-rows
-// of one shot, rows ahead streaming through a per-lane cp.async ring — but
-// shaped for instruction count, which ncu showed to be the limiter of those
-// kernels (~420 warp instructions per 128-cell row, issue-bound at 27% of
-// DRAM peak):
-//   * the x loop is unrolled by the ring depth NSL (a multiple of 3), so ring
-//     slots are immediate offsets and the 3-row register window (x-1, x, x+1)
-//     rotates by renaming instead of 16 register moves per row;
-//   * addresses are one IMAD.WIDE from a per-lane base and a 32-bit row offset;
+// A warp owns a 128-wide z strip (4 cells per lane, float4 loads/stores) and
+// walks x-rows, rows ahead streaming through a per-lane cp.async ring of 3
+// slots.  Shaped for instruction count, which ncu showed to be the limiter of
+// the first stepwise kernels (~420 warp instructions per 128-cell row,
+// issue-bound at 27% of DRAM peak):
+//   * the x loop is unrolled by the ring depth (a multiple of 3), so ring slots
+//     are immediate offsets and the 3-row register window (x-1, x, x+1)
+//     rotates by renaming instead of register moves;
+//   * addresses are one IMAD.WIDE from an opaque per-lane base and a 32-bit
+//     row offset;
 //   * per-lane constants hoisted out of the loop: (A, B) of the z-damping band
-//     (only for warps touching it, template switch), the lane's receiver
-//     columns, ring columns and source cell; per-row work is warp-uniform
-//     compares against the undamped box / receiver rows;
-//   * one edge value per lane per row (lane 0: z0-1, lane 31: z0+128).
-// Arithmetic is the explicitly rounded f64 of dufwi_common.cuh (lap5,
-// fwd_update, adj_update): the same bits as the cluster engine.
+//     (only for warps touching it, template switch), receiver / ring columns,
+//     source cell; per-row work is warp-uniform compares;
+//   * one edge value per lane per row (lane 0: z0-1, lane 31: z0+128);
+//   * 128-register cap: 4 CTAs of 4 warps per SM.
+//
+// Variable density (RHO).  The oracle's operator is
+// L_rho u = rho_c sum_j f_cj (u_j - u_c) with face factors f_cj = (q_c + q_j)/2,
+// q = 1/rho, outer faces f = q_c and u = 0 outside (oracle rho_face_weights).
+// Writing D u = sum_j f_cj u_j - S_c u_c (S_c = sum of the 4 face factors),
+// L_rho = diag(rho) D with D symmetric, so per phantom only three tables are
+// streamed: Er = rho E / dx^2, fxe (x faces, nx+1 rows incl. the outer ones)
+// and fz (z faces; the outer face of z = nz-1 in the last column, of z = 0 in
+// fz0[x]):
+//   forward   u[t]  = A u1 + B u2 + Er * D(u1)
+//   adjoint   lam   = A l1 + B l2 + D(Er * l1)        ((E L_rho)^T = D diag(Er))
+//   imaging   acc  += D(u[t-1]) * lam, scaled by rho once in reduce_groups
+//   recon     u[t-2] = 2 u1 + Er * D(u1) - u[t] (+ source)
+// The same f64 values as the oracle up to summation order (parity by tolerance).
+//
+// Arithmetic: explicitly rounded f64 (dufwi_common.cuh).  Constant density
+// uses lap5 / fwd_update / adj_update: the same bits as the cluster engine.
 // DRAM per cell update: forward 12 B (read u[t-1], u[t-2], write u[t]); lam
-// update 12 B (read lam[t+1], lam[t+2], write lam[t]); E comes from L2.
+// update 12 B; imaging + reconstruction 16 B (+16 B / gs accumulator);
+// coefficient tables come from L2 (shared by the phantom's shots).
 #pragma once
 
 #include "dufwi_vec_kernels.cuh"
@@ -34,23 +49,20 @@ namespace dufwi {
 #define DUFWI_LEAN_MINB 4
 #endif
 constexpr int kLeanWarps = DUFWI_LEAN_WARPS;  // warps per CTA
-constexpr int kLeanMinB = DUFWI_LEAN_MINB;    // min resident CTAs per SM (register cap)
-
-template <int NSL>
-struct LeanFwdRing {
-  float4 u1[NSL][kLeanWarps * 32];   // u[t-1] row r+1
-  float4 u2[NSL][kLeanWarps * 32];   // u[t-2] row r
-  double2 e0[NSL][kLeanWarps * 32];  // E row r, cells 0-1
-  double2 e1[NSL][kLeanWarps * 32];  // E row r, cells 2-3
-  float edge[NSL][kLeanWarps * 32];  // u[t-1] row r+1 at z0-1 (lane 0) / z0+128 (lane 31)
-};
+#ifndef DUFWI_LEAN_MINB_RHO
+#define DUFWI_LEAN_MINB_RHO 3
+#endif
+constexpr int kLeanMinB = DUFWI_LEAN_MINB;        // min resident CTAs per SM (register cap)
+constexpr int kLeanMinBRho = DUFWI_LEAN_MINB_RHO;  // density kernels: more live f64 state
+constexpr int kLeanT = kLeanWarps * 32;
+constexpr int kNSL = 3;                       // ring slots (measured best: 3 > 6)
 
 // Per-lane constants of a 4-cell z segment.
 struct LaneInfo {
   int z4;
   bool act;
-  unsigned rxk;    // cells on a receiver column
-  unsigned boxk;   // cells with z in [z_lo, z_hi]
+  unsigned rxk;      // cells on a receiver column
+  unsigned boxk;     // cells with z in [z_lo, z_hi]
   int ringl, ringr;  // cell index on ring column z_lo-1 / z_hi+1, or -1
   bool zd;           // any cell in the z damping band
 };
@@ -91,15 +103,81 @@ __device__ __forceinline__ double2 ab_row_damped(const ABTables& T, double pxx, 
                                 : make_double2(__ldg(T.Az + z), __ldg(T.Bz + z));
 }
 
+// D(u)_c = sum_j f_cj u_j - S_c u_c (variable-density operator without rho_c).
+__device__ __forceinline__ double lapf(double c, double xm, double xp, double zm, double zp,
+                                       double fxm, double fxp, double fzm, double fzp) {
+  const double S = __dadd_rn(__dadd_rn(__dadd_rn(fxm, fxp), fzm), fzp);
+  return __fma_rn(fzp, zp, __fma_rn(fzm, zm, __fma_rn(fxp, xp, __fma_rn(fxm, xm, __dmul_rn(-S, c)))));
+}
+
+// Face tables of the density operator, streamed alongside the fields.
+template <int NSL>
+struct FaceRing {
+  double2 fx0[NSL][kLeanT], fx1[NSL][kLeanT];  // fxe row (cells 0-1, 2-3)
+  double2 fz0[NSL][kLeanT], fz1[NSL][kLeanT];  // fz row
+  double fze[NSL][kLeanT];                     // z face left of the strip (lane 0)
+};
+template <int NSL, bool RHO>
+struct FaceRingOpt {};
+template <int NSL>
+struct FaceRingOpt<NSL, true> {
+  FaceRing<NSL> f;
+};
+
+// Per-lane view of the face tables of one phantom.
+struct FaceLane {
+  const double* fx;   // fxe + zc (row r at r * nz)
+  const double* fz;   // fz + zc
+  const double* fze;  // lane 0: fz + z0-1 (stride nz) or fz0 (stride 1)
+  int fze_stride;
+};
+
+__device__ __forceinline__ FaceLane face_lane(const Model& m, const Geo& g, int b, int zc, int z0) {
+  FaceLane F;
+  const size_t N2 = (size_t)g.nx * g.nz;
+  F.fx = opaque(m.fxe + (size_t)b * (N2 + g.nz) + zc);
+  F.fz = opaque(m.fz + (size_t)b * N2 + zc);
+  if (z0 > 0) {
+    F.fze = opaque(m.fz + (size_t)b * N2 + z0 - 1);
+    F.fze_stride = g.nz;
+  } else {
+    F.fze = opaque(m.fz0 + (size_t)b * g.nx);
+    F.fze_stride = 1;
+  }
+  return F;
+}
+
+template <int NSL>
+__device__ __forceinline__ void issue_faces(FaceRing<NSL>& R, const FaceLane& F, int tid, int sl,
+                                            int rfx, bool okfx, int rfz, bool okfz, bool act,
+                                            bool lane0, int nz) {
+  cp16(&R.fx0[sl][tid], F.fx + rfx * nz, okfx && act);
+  cp16(&R.fx1[sl][tid], F.fx + rfx * nz + 2, okfx && act);
+  cp16(&R.fz0[sl][tid], F.fz + rfz * nz, okfz && act);
+  cp16(&R.fz1[sl][tid], F.fz + rfz * nz + 2, okfz && act);
+  cp8(&R.fze[sl][tid], F.fze + rfz * F.fze_stride, okfz && lane0);
+}
+
 // ----------------------------------------------------------------- forward
-template <int MODE, int NSL, bool ZD>
+template <int NSL, bool RHO>
+struct LeanFwdRing {
+  float4 u1[NSL][kLeanT];   // u[t-1] row r+1
+  float4 u2[NSL][kLeanT];   // u[t-2] row r
+  double2 e0[NSL][kLeanT];  // E (RHO: Er) row r, cells 0-1
+  double2 e1[NSL][kLeanT];  // cells 2-3
+  float edge[NSL][kLeanT];  // u[t-1] row r+1 at z0-1 (lane 0) / z0+128 (lane 31)
+  FaceRingOpt<NSL, RHO> fr; // RHO: fxe row r+1, fz row r
+};
+
+template <int MODE, bool RHO, bool ZD>
 __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, const LaneInfo& L,
-                                              LeanFwdRing<NSL>& ring, int tid, int lane, int z0,
-                                              int x0, int x1, int lu, int txx, int tk,
-                                              double pulse_t, const float* f1, const float* f2,
-                                              const double* Ed, float* fo, float* rec_t,
-                                              float* strip_t, bool has1, bool has2, bool wrx,
-                                              bool wring) {
+                                              LeanFwdRing<kNSL, RHO>& ring, const FaceLane& FL,
+                                              int tid, int lane, int z0, int x0, int x1, int lu,
+                                              int txx, int tk, double pulse_t, const float* f1,
+                                              const float* f2, const double* Ec, float* fo,
+                                              float* rec_t, float* strip_t, bool has1, bool has2,
+                                              bool wrx, bool wring) {
+  constexpr int NSL = kNSL;
   const int nz = g.nz, nx = g.nx;
   const int zc = L.act ? L.z4 : 0;
   const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < g.nz;
@@ -108,7 +186,7 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
   const bool ok1 = has1 && L.act, ok2 = has2 && L.act;
   const float* b1 = opaque(f1 + zc);
   const float* b2 = opaque(f2 + zc);
-  const double* be = opaque(Ed + zc);
+  const double* be = opaque(Ec + zc);
   const float* bl = opaque(f1 + ze);
   float* bo = opaque(fo + zc);
   double Az[4], Bz[4];
@@ -121,7 +199,7 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
       Bz[k] = __ldg(T.Bz + L.z4 + k);
     }
   }
-  // copies of "row r": u[t-1] row r+1 (+ edge), u[t-2] row r, E row r
+  // copies of "row r": u[t-1] row r+1 (+ edge), u[t-2] row r, E row r (+ faces)
   auto issue = [&](int r, int sl) {
     const bool okn = r + 1 < nx;
     const int on = okn ? (r + 1) * nz : 0;
@@ -131,25 +209,31 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
     cp16(&ring.e0[sl][tid], be + orr, L.act);
     cp16(&ring.e1[sl][tid], be + orr + 2, L.act);
     cp4(&ring.edge[sl][tid], bl + on, has_edge && okn);
+    if constexpr (RHO) issue_faces(ring.fr.f, FL, tid, sl, r + 1, true, r, true, L.act, lane == 0, nz);
   };
-  // register window: W[(k) % 3] = row x-1, W[(k+1) % 3] = row x, W[(k+2) % 3] = row x+1
-  double W[3][4];
-  double Eg[3];  // edge value of the row in the same slot of W
+  // register windows: slot (k) % 3 = row x-1, (k+1) % 3 = row x, (k+2) % 3 = row x+1;
+  // FX[s] = x face below the row of slot s (fxe[row])
+  double W[3][4], Eg[3], FX[3][4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) W[0][k] = W[1][k] = W[2][k] = 0.0;
+  for (int k = 0; k < 4; ++k) W[0][k] = W[1][k] = W[2][k] = FX[0][k] = FX[1][k] = FX[2][k] = 0.0;
   Eg[0] = Eg[1] = Eg[2] = 0.0;
   if (has1) {
-    if (x0 >= 1) {
-      if (L.act) {
-        const float4 f = __ldg(reinterpret_cast<const float4*>(b1 + (x0 - 1) * nz));
-        W[0][0] = f.x; W[0][1] = f.y; W[0][2] = f.z; W[0][3] = f.w;
-      }
+    if (x0 >= 1 && L.act) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(b1 + (x0 - 1) * nz));
+      W[0][0] = f.x; W[0][1] = f.y; W[0][2] = f.z; W[0][3] = f.w;
     }
     if (L.act) {
       const float4 f = __ldg(reinterpret_cast<const float4*>(b1 + x0 * nz));
       W[1][0] = f.x; W[1][1] = f.y; W[1][2] = f.z; W[1][3] = f.w;
     }
     if (edge_l || edge_r) Eg[1] = (double)__ldg(bl + x0 * nz);
+  }
+  if constexpr (RHO) {
+    if (L.act) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(FL.fx + x0 * nz));
+      const double2 c = __ldg(reinterpret_cast<const double2*>(FL.fx + x0 * nz + 2));
+      FX[1][0] = a.x; FX[1][1] = a.y; FX[1][2] = c.x; FX[1][3] = c.y;
+    }
   }
 #pragma unroll
   for (int k = 0; k < NSL - 1; ++k) {
@@ -178,25 +262,41 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
       double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1);
       if (lane == 0) zl = Eg[ic];
       if (lane == 31) zr = Eg[ic];
-      double v[4];
-      if (x >= g.x_lo && x <= g.x_hi) {  // undamped row: (A, B) of the lane's z band
+      double lap[4];
+      if constexpr (RHO) {
+        const double2 a = ring.fr.f.fx0[k][tid], c = ring.fr.f.fx1[k][tid];
+        FX[ip][0] = a.x; FX[ip][1] = a.y; FX[ip][2] = c.x; FX[ip][3] = c.y;
+        const double2 z0v = ring.fr.f.fz0[k][tid], z1v = ring.fr.f.fz1[k][tid];
+        const double fzv[4] = {z0v.x, z0v.y, z1v.x, z1v.y};
+        double fzl = __shfl_up_sync(0xffffffffu, fzv[3], 1);
+        if (lane == 0) fzl = ring.fr.f.fze[k][tid];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const double zm = c == 0 ? zl : W[ic][c - 1];
           const double zp = c == 3 ? zr : W[ic][c + 1];
-          const double lap = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
-          v[c] = ZD ? fwd_update(Az[c], Bz[c], W[ic][c], u2v[c], ed[c], lap)
-                    : fwd_update_free(W[ic][c], u2v[c], ed[c], lap);
+          lap[c] = lapf(W[ic][c], W[im][c], W[ip][c], zm, zp, FX[ic][c], FX[ip][c],
+                        c == 0 ? fzl : fzv[c - 1], fzv[c]);
         }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double zm = c == 0 ? zl : W[ic][c - 1];
+          const double zp = c == 3 ? zr : W[ic][c + 1];
+          lap[c] = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
+        }
+      }
+      double v[4];
+      if (x >= g.x_lo && x <= g.x_hi) {  // undamped row: (A, B) of the lane's z band
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          v[c] = ZD ? fwd_update(Az[c], Bz[c], W[ic][c], u2v[c], ed[c], lap[c])
+                    : fwd_update_free(W[ic][c], u2v[c], ed[c], lap[c]);
       } else {  // damped row (x band of the PML)
         const double pxx = __ldg(T.px + x), Axx = __ldg(T.Ax + x), Bxx = __ldg(T.Bx + x);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const double zm = c == 0 ? zl : W[ic][c - 1];
-          const double zp = c == 3 ? zr : W[ic][c + 1];
-          const double lap = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
           const double2 ab = ab_row_damped(T, pxx, Axx, Bxx, min(L.z4 + c, nz - 1));
-          v[c] = fwd_update(ab.x, ab.y, W[ic][c], u2v[c], ed[c], lap);
+          v[c] = fwd_update(ab.x, ab.y, W[ic][c], u2v[c], ed[c], lap[c]);
         }
       }
       if (x == txx) {
@@ -237,13 +337,13 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
   cp_wait<0>();
 }
 
-template <int MODE, int NSL>
-__global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
+template <int MODE, bool RHO>
+__global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
     fwd_lean_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
                     const float* __restrict__ u1, const float* u2, float* uo,
                     float* __restrict__ rec_t, float* __restrict__ strip_t, int has1, int has2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LeanFwdRing<NSL>& ring = *reinterpret_cast<LeanFwdRing<NSL>*>(smem_raw);
+  auto& ring = *reinterpret_cast<LeanFwdRing<kNSL, RHO>*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -266,35 +366,41 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
   const float* f1 = u1 + (size_t)lu * N2;
   const float* f2 = u2 + (size_t)lu * N2;
   float* fo = uo + (size_t)lu * N2;
-  const double* Ed = m.Ed + (size_t)b * N2;
+  const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)b * N2;
+  FaceLane FL{};
+  if constexpr (RHO) FL = face_lane(m, g, b, L.act ? L.z4 : 0, z0);
   if (wzd)
-    fwd_lean_rows<MODE, NSL, true>(g, T, L, ring, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t, f1,
-                                   f2, Ed, fo, rec_t, strip_t, has1, has2, wrx, wring);
+    fwd_lean_rows<MODE, RHO, true>(g, T, L, ring, FL, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t,
+                                   f1, f2, Ec, fo, rec_t, strip_t, has1, has2, wrx, wring);
   else
-    fwd_lean_rows<MODE, NSL, false>(g, T, L, ring, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t, f1,
-                                    f2, Ed, fo, rec_t, strip_t, has1, has2, wrx, wring);
+    fwd_lean_rows<MODE, RHO, false>(g, T, L, ring, FL, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t,
+                                    f1, f2, Ec, fo, rec_t, strip_t, has1, has2, wrx, wring);
 }
 
 // --------------------------------------------------------------- lam update
 // lam[t] = A lam[t+1] + L^T(E lam[t+1]) + B lam[t+2] (+ merged residual at the
-// receiver nodes), in place over lam[t+2] (adjoint.py:119-131).
-template <int NSL>
+// receiver nodes), in place over lam[t+2] (adjoint.py:119-131).  RHO:
+// L^T(E lam) = D(Er lam).
+template <int NSL, bool RHO>
 struct LeanAdjRing {
-  float4 l1[NSL][kLeanWarps * 32];    // lam[t+1] row r+1
-  double2 e0[NSL][kLeanWarps * 32];   // E row r+1, cells 0-1
-  double2 e1[NSL][kLeanWarps * 32];   // E row r+1, cells 2-3
-  float4 l2[NSL][kLeanWarps * 32];    // lam[t+2] row r
-  float edl[NSL][kLeanWarps * 32];    // lam[t+1] row r+1 at the lane's edge column
-  double ede[NSL][kLeanWarps * 32];   // E row r+1 at the lane's edge column
+  float4 l1[NSL][kLeanT];    // lam[t+1] row r+1
+  double2 e0[NSL][kLeanT];   // E (RHO: Er) row r+1, cells 0-1
+  double2 e1[NSL][kLeanT];   // cells 2-3
+  float4 l2[NSL][kLeanT];    // lam[t+2] row r
+  float edl[NSL][kLeanT];    // lam[t+1] row r+1 at the lane's edge column
+  double ede[NSL][kLeanT];   // E row r+1 at the lane's edge column
+  FaceRingOpt<NSL, RHO> fr;  // RHO: fxe row r+1, fz row r
 };
 
-template <int NSL, bool ZD>
+template <bool RHO, bool ZD>
 __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T,
-                                                 const LaneInfo& L, LeanAdjRing<NSL>& ring,
-                                                 int tid, int lane, int z0, int x0, int x1,
-                                                 int lu, const float* L1, float* L2,
-                                                 const double* Ed, const double* rres_t,
-                                                 bool has1, bool has2, bool wrx) {
+                                                 const LaneInfo& L, LeanAdjRing<kNSL, RHO>& ring,
+                                                 const FaceLane& FL, int tid, int lane, int z0,
+                                                 int x0, int x1, int lu, const float* L1,
+                                                 float* L2, const double* Ec,
+                                                 const double* rres_t, bool has1, bool has2,
+                                                 bool wrx) {
+  constexpr int NSL = kNSL;
   const int nz = g.nz, nx = g.nx;
   const int zc = L.act ? L.z4 : 0;
   const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < g.nz;
@@ -303,9 +409,9 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
   const bool ok1 = has1 && L.act, ok2 = has2 && L.act;
   const float* b1 = opaque(L1 + zc);
   float* b2 = opaque(L2 + zc);
-  const double* be = opaque(Ed + zc);
+  const double* be = opaque(Ec + zc);
   const float* bl = opaque(L1 + ze);
-  const double* bel = opaque(Ed + ze);
+  const double* bel = opaque(Ec + ze);
   double Az[4], Bz[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -326,11 +432,15 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
     cp16(&ring.l2[sl][tid], b2 + orr, ok2);
     cp4(&ring.edl[sl][tid], bl + on, has1 && has_edge && okn);
     cp8(&ring.ede[sl][tid], bel + on, has_edge && okn);
+    if constexpr (RHO) issue_faces(ring.fr.f, FL, tid, sl, r + 1, true, r, true, L.act, lane == 0, nz);
   };
-  // window of E*lam1 (EL) and raw lam1 (RL): slot (k)%3 = row x-1, (k+1)%3 = x, (k+2)%3 = x+1
-  double EL[3][4], RL[3][4], EG[3];
+  // windows of E*lam1 (EL) and raw lam1 (RL), slot (k)%3 = row x-1, (k+1)%3 = x,
+  // (k+2)%3 = x+1; FX[s] = x face below the row of slot s
+  double EL[3][4], RL[3][4], EG[3], FX[3][4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) EL[0][k] = EL[1][k] = EL[2][k] = RL[0][k] = RL[1][k] = RL[2][k] = 0.0;
+  for (int k = 0; k < 4; ++k)
+    EL[0][k] = EL[1][k] = EL[2][k] = RL[0][k] = RL[1][k] = RL[2][k] = FX[0][k] = FX[1][k] =
+        FX[2][k] = 0.0;
   EG[0] = EG[1] = EG[2] = 0.0;
   if (has1) {
     auto ld = [&](int x, int w) {
@@ -348,6 +458,13 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
     };
     if (x0 >= 1) ld(x0 - 1, 0);
     ld(x0, 1);
+  }
+  if constexpr (RHO) {
+    if (L.act) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(FL.fx + x0 * nz));
+      const double2 c = __ldg(reinterpret_cast<const double2*>(FL.fx + x0 * nz + 2));
+      FX[1][0] = a.x; FX[1][1] = a.y; FX[1][2] = c.x; FX[1][3] = c.y;
+    }
   }
 #pragma unroll
   for (int k = 0; k < NSL - 1; ++k) {
@@ -379,25 +496,41 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
       double zr = __shfl_down_sync(0xffffffffu, EL[ic][0], 1);
       if (lane == 0) zl = EG[ic];
       if (lane == 31) zr = EG[ic];
+      double adj[4];
+      if constexpr (RHO) {
+        const double2 a = ring.fr.f.fx0[k][tid], c = ring.fr.f.fx1[k][tid];
+        FX[ip][0] = a.x; FX[ip][1] = a.y; FX[ip][2] = c.x; FX[ip][3] = c.y;
+        const double2 z0v = ring.fr.f.fz0[k][tid], z1v = ring.fr.f.fz1[k][tid];
+        const double fzv[4] = {z0v.x, z0v.y, z1v.x, z1v.y};
+        double fzl = __shfl_up_sync(0xffffffffu, fzv[3], 1);
+        if (lane == 0) fzl = ring.fr.f.fze[k][tid];
+#pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2) {
+          const double zm = c2 == 0 ? zl : EL[ic][c2 - 1];
+          const double zp = c2 == 3 ? zr : EL[ic][c2 + 1];
+          adj[c2] = lapf(EL[ic][c2], EL[im][c2], EL[ip][c2], zm, zp, FX[ic][c2], FX[ip][c2],
+                         c2 == 0 ? fzl : fzv[c2 - 1], fzv[c2]);
+        }
+      } else {
+#pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2) {
+          const double zm = c2 == 0 ? zl : EL[ic][c2 - 1];
+          const double zp = c2 == 3 ? zr : EL[ic][c2 + 1];
+          adj[c2] = lap5(EL[ic][c2], EL[im][c2], EL[ip][c2], zm, zp);
+        }
+      }
       double lam[4];
       if (x >= g.x_lo && x <= g.x_hi) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const double zm = c == 0 ? zl : EL[ic][c - 1];
-          const double zp = c == 3 ? zr : EL[ic][c + 1];
-          const double adj = lap5(EL[ic][c], EL[im][c], EL[ip][c], zm, zp);
-          lam[c] = ZD ? adj_update(Az[c], Bz[c], RL[ic][c], l2v[c], adj)
-                      : adj_update_free(RL[ic][c], l2v[c], adj);
-        }
+        for (int c = 0; c < 4; ++c)
+          lam[c] = ZD ? adj_update(Az[c], Bz[c], RL[ic][c], l2v[c], adj[c])
+                      : adj_update_free(RL[ic][c], l2v[c], adj[c]);
       } else {
         const double pxx = __ldg(T.px + x), Axx = __ldg(T.Ax + x), Bxx = __ldg(T.Bx + x);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const double zm = c == 0 ? zl : EL[ic][c - 1];
-          const double zp = c == 3 ? zr : EL[ic][c + 1];
-          const double adj = lap5(EL[ic][c], EL[im][c], EL[ip][c], zm, zp);
           const double2 ab = ab_row_damped(T, pxx, Axx, Bxx, min(L.z4 + c, nz - 1));
-          lam[c] = adj_update(ab.x, ab.y, RL[ic][c], l2v[c], adj);
+          lam[c] = adj_update(ab.x, ab.y, RL[ic][c], l2v[c], adj[c]);
         }
       }
       if (L.act) {
@@ -418,13 +551,13 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
   cp_wait<0>();
 }
 
-template <int NSL>
-__global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
+template <bool RHO>
+__global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
     adjlam_lean_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
                        const float* __restrict__ l1, float* l2o, const double* __restrict__ rres_t,
                        int has1, int has2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LeanAdjRing<NSL>& ring = *reinterpret_cast<LeanAdjRing<NSL>*>(smem_raw);
+  auto& ring = *reinterpret_cast<LeanAdjRing<kNSL, RHO>*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -440,15 +573,16 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
   const bool wzd = __any_sync(0xffffffffu, L.zd);
   const float* L1 = l1 + (size_t)lu * N2;
   float* L2 = l2o + (size_t)lu * N2;
-  const double* Ed = m.Ed + (size_t)b * N2;
+  const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)b * N2;
+  FaceLane FL{};
+  if constexpr (RHO) FL = face_lane(m, g, b, L.act ? L.z4 : 0, z0);
   if (wzd)
-    adjlam_lean_rows<NSL, true>(g, T, L, ring, tid, lane, z0, x0, x1, lu, L1, L2, Ed, rres_t,
+    adjlam_lean_rows<RHO, true>(g, T, L, ring, FL, tid, lane, z0, x0, x1, lu, L1, L2, Ec, rres_t,
                                 has1, has2, wrx);
   else
-    adjlam_lean_rows<NSL, false>(g, T, L, ring, tid, lane, z0, x0, x1, lu, L1, L2, Ed, rres_t,
+    adjlam_lean_rows<RHO, false>(g, T, L, ring, FL, tid, lane, z0, x0, x1, lu, L1, L2, Ec, rres_t,
                                  has1, has2, wrx);
 }
-
 
 // ------------------------------------------------------ imaging + reconstruction
 // sum_t L(u[t-1]) lam[t] over a group of gs shots of one phantom (adjoint.py:128-130)
@@ -457,10 +591,11 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
 //
 // A warp owns a 128-wide z strip x kImgTX box rows and walks the group's shots
 // one after the other as ONE stream of ring items (kImgTX + 2 per shot): item i
-// of a shot carries u[t-1] row x0-1+i (+ the lane's edge value) and, for i >= 2,
-// lam[t], u[t] and E of row x0+i-2, so the pipeline never drains between shots.
-// The imaging sums of the warp's kImgTX x 4 cells per lane stay in registers for
-// the whole group; one f64 read-modify-write of acc_part[group] per cell at the end.
+// of a shot carries u[t-1] row x0-1+i (+ the lane's edge value, + RHO x faces)
+// and, for i >= 2, lam[t], u[t], E and RHO z faces of row x0+i-2, so the
+// pipeline never drains between shots.  The imaging sums of the warp's
+// kImgTX x 4 cells per lane stay in registers for the whole group; one f64
+// read-modify-write of acc_part[group] per cell at the end.
 //
 // MODE 2 keeps u[t-1] complete on the box AND its 1-cell ring in the field
 // buffer: the reconstruction writes the box cells of u[t-2], and the ring cells
@@ -472,27 +607,28 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
 // (+16 B / gs for the accumulator); MODE 1 read u[t-1], lam[t] = 8 B.
 constexpr int kImgTX = 4;
 constexpr int kImgItems = kImgTX + 2;  // ring items per shot (multiple of 3)
-static_assert(kImgItems % 3 == 0, "ring/window rotation needs items % 3 == 0");
+static_assert(kImgItems % 3 == 0 && kImgItems % kNSL == 0, "ring/window rotation");
 
-template <int NSL>  // ring slots: 3 or 6 (divides kImgItems)
+template <bool RHO>
 struct LeanImgRing {
-  float4 u1[NSL][kLeanWarps * 32];    // u[t-1] row x0-1+i
-  float4 lam[NSL][kLeanWarps * 32];   // lam[t] row x0+i-2
-  float4 ut[NSL][kLeanWarps * 32];    // u[t] row x0+i-2 (MODE 2)
-  double2 e0[NSL][kLeanWarps * 32];   // E row x0+i-2, cells 0-1 (MODE 2)
-  double2 e1[NSL][kLeanWarps * 32];   // cells 2-3
-  float edge[NSL][kLeanWarps * 32];   // u[t-1] row x0-1+i at the lane's edge column
+  float4 u1[kNSL][kLeanT];    // u[t-1] row x0-1+i
+  float4 lam[kNSL][kLeanT];   // lam[t] row x0+i-2
+  float4 ut[kNSL][kLeanT];    // u[t] row x0+i-2 (MODE 2)
+  double2 e0[kNSL][kLeanT];   // E (RHO: Er) row x0+i-2, cells 0-1 (MODE 2)
+  double2 e1[kNSL][kLeanT];   // cells 2-3
+  float edge[kNSL][kLeanT];   // u[t-1] row x0-1+i at the lane's edge column
+  FaceRingOpt<kNSL, RHO> fr;  // RHO: fxe row x0-1+i, fz row x0+i-2
 };
 
-template <int MODE, int NSL>
-__global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
+template <int MODE, bool RHO>
+__global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
     img_lean_kernel(Geo g, Model m, int t, int unit_begin, int U, int gs,
                     const float* __restrict__ lam_t, const float* __restrict__ F, float* ut,
                     const float* __restrict__ utm1, const float* __restrict__ strip_tm2,
                     double* __restrict__ acc_part, int do_recon) {
+  constexpr int NSL = kNSL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  static_assert(kImgItems % NSL == 0, "ring slots must divide the items per shot");
-  LeanImgRing<NSL>& ring = *reinterpret_cast<LeanImgRing<NSL>*>(smem_raw);
+  auto& ring = *reinterpret_cast<LeanImgRing<RHO>*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -522,9 +658,10 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
   }
   const bool recon_on = MODE == 2 && do_recon;
   const double pulse_t = __ldg(g.pulse + t);
-  const double* Ed = m.Ed + (size_t)sg.b * N2;
-  const double* be = opaque(Ed + zc);
-  // row r of the u[t-1] field / lam / u[t] of chunk-local unit lu
+  const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)sg.b * N2;
+  const double* be = opaque(Ec + zc);
+  FaceLane FL{};
+  if constexpr (RHO) FL = face_lane(m, g, sg.b, zc, z0);
   const float* U1 = MODE == 1 ? F : utm1;
   auto issue = [&](int k, int i, int sl) {  // item i of the group's k-th shot
     if (k >= sg.n) return;
@@ -534,9 +671,13 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
     const int ou = oku ? ru * nz : 0;
     cp16(&ring.u1[sl][tid], U1 + fo + zc + ou, oku && act);
     cp4(&ring.edge[sl][tid], U1 + fo + ze + ou, oku && has_edge);
+    const int rx = x0 + i - 2;
+    const bool okx = i >= 2 && rx < x1;
+    if constexpr (RHO) {  // fxe has nx + 1 rows (outer faces included)
+      const bool okf = ru >= 0 && ru <= nx;
+      issue_faces(ring.fr.f, FL, tid, sl, okf ? ru : 0, okf, okx ? rx : 0, okx, act, lane == 0, nz);
+    }
     if (i >= 2) {
-      const int rx = x0 + i - 2;
-      const bool okx = rx < x1;
       const int ox = okx ? rx * nz : 0;
       cp16(&ring.lam[sl][tid], lam_t + fo + zc + ox, okx && act);
       if (recon_on) {
@@ -557,7 +698,7 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
     issue(0, i, i);
     cp_commit();
   }
-  double W[3][4], Eg[3];
+  double W[3][4], Eg[3], FX[3][4];
   for (int k = 0; k < sg.n; ++k) {
     const int lu = sg.lu0 + k;
     const int s = (unit_begin + lu) % g.S;
@@ -577,6 +718,10 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
         const float4 f = ring.u1[sl][tid];
         W[wi][0] = f.x; W[wi][1] = f.y; W[wi][2] = f.z; W[wi][3] = f.w;
         Eg[wi] = (double)ring.edge[sl][tid];
+        if constexpr (RHO) {
+          const double2 a = ring.fr.f.fx0[sl][tid], c = ring.fr.f.fx1[sl][tid];
+          FX[wi][0] = a.x; FX[wi][1] = a.y; FX[wi][2] = c.x; FX[wi][3] = c.y;
+        }
       }
       if (i < 2) continue;
       const int r = i - 2;
@@ -586,6 +731,13 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
       double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1);
       if (lane == 0) zl = Eg[ic];
       if (lane == 31) zr = Eg[ic];
+      double fzv[4] = {0.0, 0.0, 0.0, 0.0}, fzl = 0.0;
+      if constexpr (RHO) {
+        const double2 z0v = ring.fr.f.fz0[sl][tid], z1v = ring.fr.f.fz1[sl][tid];
+        fzv[0] = z0v.x; fzv[1] = z0v.y; fzv[2] = z1v.x; fzv[3] = z1v.y;
+        fzl = __shfl_up_sync(0xffffffffu, fzv[3], 1);
+        if (lane == 0) fzl = ring.fr.f.fze[sl][tid];
+      }
       if (x >= x1) continue;  // warp-uniform (last row block)
       const float4 lf = ring.lam[sl][tid];
       const double lam[4] = {lf.x, lf.y, lf.z, lf.w};
@@ -594,7 +746,11 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
       for (int c = 0; c < 4; ++c) {
         const double zm = c == 0 ? zl : W[ic][c - 1];
         const double zp = c == 3 ? zr : W[ic][c + 1];
-        lapu[c] = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
+        if constexpr (RHO)
+          lapu[c] = lapf(W[ic][c], W[im][c], W[ip][c], zm, zp, FX[ic][c], FX[ip][c],
+                         c == 0 ? fzl : fzv[c - 1], fzv[c]);
+        else
+          lapu[c] = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
         if (boxk & (1u << c)) acc[r][c] = __fma_rn(lapu[c], lam[c], acc[r][c]);
       }
       if (recon_on && act) {
@@ -643,4 +799,5 @@ __global__ void __launch_bounds__(kLeanWarps * 32, kLeanMinB)
     }
   }
 }
+
 }  // namespace dufwi
