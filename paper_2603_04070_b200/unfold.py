@@ -120,7 +120,7 @@ def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) ->
     rec = Reconstructor(eng, nets, setup.bounds, rho=rho)
     # ChannelData arrays are read-only views: a writable host copy for torch
     obs = torch.from_numpy(np.require(m_obs.traces, np.float64, ["C", "W"])).to(eng.device)
-    c = torch.as_tensor(c0.values, dtype=torch.float64).to(eng.device)[None]
+    c = torch.from_numpy(np.array(c0.values, dtype=np.float64)).to(eng.device)[None]
     try:
         maps = rec.reconstruct(obs, c)
     except FloatingPointError as exc:
