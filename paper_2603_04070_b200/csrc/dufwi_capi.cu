@@ -65,6 +65,7 @@ struct dufwi_plan {
   std::vector<ClusterCfg> ccands;  // launch shapes that fit, one per cluster size
   ClusterCfg ccfg{};                // the shape for all units at once (plan_info)
   bool cluster_ok = false;
+  int lean_tx = 0;      // rows per warp override (DUFWI_LEAN_TX, experiments)
   bool lean_on = true;  // lean stepwise kernels (DUFWI_LEAN=0: the first vec/stream kernels)
   double *Er = nullptr, *fxe = nullptr, *fz = nullptr, *fz0 = nullptr;  // density tables
 };
@@ -374,16 +375,17 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.row_flag = p->row_flag;
   g.col_flag = p->col_flag;
   if (const char* e = getenv("DUFWI_LEAN")) p->lean_on = atoi(e) != 0;
+  if (const char* e = getenv("DUFWI_LEAN_TX")) p->lean_tx = std::max(0, atoi(e));
   {  // lean rings may exceed the 48 KB default of dynamic shared memory
     auto big = [](const void* f, size_t bytes) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     };
-    big((const void*)fwd_lean_kernel<0, false>, sizeof(LeanFwdRing<kNSL, false>));
-    big((const void*)fwd_lean_kernel<1, false>, sizeof(LeanFwdRing<kNSL, false>));
-    big((const void*)fwd_lean_kernel<2, false>, sizeof(LeanFwdRing<kNSL, false>));
-    big((const void*)fwd_lean_kernel<0, true>, sizeof(LeanFwdRing<kNSL, true>));
-    big((const void*)fwd_lean_kernel<1, true>, sizeof(LeanFwdRing<kNSL, true>));
-    big((const void*)fwd_lean_kernel<2, true>, sizeof(LeanFwdRing<kNSL, true>));
+    big((const void*)fwd_lean_kernel<0, false>, sizeof(LeanFwdRing<kFwdNSL, false>));
+    big((const void*)fwd_lean_kernel<1, false>, sizeof(LeanFwdRing<kFwdNSL, false>));
+    big((const void*)fwd_lean_kernel<2, false>, sizeof(LeanFwdRing<kFwdNSL, false>));
+    big((const void*)fwd_lean_kernel<0, true>, sizeof(LeanFwdRing<kFwdNSL, true>));
+    big((const void*)fwd_lean_kernel<1, true>, sizeof(LeanFwdRing<kFwdNSL, true>));
+    big((const void*)fwd_lean_kernel<2, true>, sizeof(LeanFwdRing<kFwdNSL, true>));
     big((const void*)adjlam_lean_kernel<false>, sizeof(LeanAdjRing<kNSL, false>));
     big((const void*)adjlam_lean_kernel<true>, sizeof(LeanAdjRing<kNSL, true>));
     big((const void*)img_lean_kernel<1, false>, sizeof(LeanImgRing<false>));
@@ -500,6 +502,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
       const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
       if (warps >= 148L * 32) { vtx = c; break; }
     }
+    if (p->lean_tx > 0) vtx = p->lean_tx;
     const dim3 vgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
     const bool lean = use_lean(p);
     const dim3 lgrid((g.nz + 127) / 128, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx), U);
@@ -527,7 +530,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   fwd_vec_kernel<M><<<vgrid, kPipeWarps * 32, sizeof(FwdRing), st>>>(g, m, p->ab, t, unit_begin, \
                                                       vtx, u1, u2, uo, rec_t, st_t, has1, has2)
 #define DUFWI_LEAN(M, R)                                                                        \
-  fwd_lean_kernel<M, R><<<lgrid, kLeanT, sizeof(LeanFwdRing<kNSL, R>), st>>>(                     \
+  fwd_lean_kernel<M, R><<<lgrid, kLeanT, sizeof(LeanFwdRing<kFwdNSL, R>), st>>>(                     \
       g, m, p->ab, t, unit_begin, vtx, u1, u2, uo, rec_t, st_t, has1, has2)
       if (lean) {
         if (p->has_rho) {
@@ -640,6 +643,7 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
       const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
       if (warps >= 148L * 32) { vtx = c; break; }
     }
+    if (p->lean_tx > 0) vtx = p->lean_tx;
     if (use_lean(p)) {
       // split adjoint: lam update (12 B/update) then imaging + reconstruction
       const dim3 lgrid((g.nz + 127) / 128, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx), U);

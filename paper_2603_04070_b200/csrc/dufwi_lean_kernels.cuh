@@ -56,6 +56,10 @@ constexpr int kLeanMinB = DUFWI_LEAN_MINB;        // min resident CTAs per SM (r
 constexpr int kLeanMinBRho = DUFWI_LEAN_MINB_RHO;  // density kernels: more live f64 state
 constexpr int kLeanT = kLeanWarps * 32;
 constexpr int kNSL = 3;                       // ring slots (measured best: 3 > 6)
+#ifndef DUFWI_FWD_NSL
+#define DUFWI_FWD_NSL 3
+#endif
+constexpr int kFwdNSL = DUFWI_FWD_NSL;         // forward ring slots (>3: runtime slot index)
 
 // Per-lane constants of a 4-cell z segment.
 struct LaneInfo {
@@ -171,13 +175,13 @@ struct LeanFwdRing {
 
 template <int MODE, bool RHO, bool ZD>
 __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, const LaneInfo& L,
-                                              LeanFwdRing<kNSL, RHO>& ring, const FaceLane& FL,
+                                              LeanFwdRing<kFwdNSL, RHO>& ring, const FaceLane& FL,
                                               int tid, int lane, int z0, int x0, int x1, int lu,
                                               int txx, int tk, double pulse_t, const float* f1,
                                               const float* f2, const double* Ec, float* fo,
                                               float* rec_t, float* strip_t, bool has1, bool has2,
                                               bool wrx, bool wring) {
-  constexpr int NSL = kNSL;
+  constexpr int NSL = kFwdNSL;
   const int nz = g.nz, nx = g.nx;
   const int zc = L.act ? L.z4 : 0;
   const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < g.nz;
@@ -240,15 +244,24 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
     if (x0 + k < x1) issue(x0 + k, k);
     cp_commit();
   }
-  for (int xb = x0; xb < x1; xb += NSL) {
+  // unrolled by 3 (the register window); with NSL == 3 the ring slot is the
+  // unroll index, deeper rings index their slot at run time
+  constexpr int UNR = 3;
+  int sr = 0, si = NSL - 1;
+  for (int xb = x0; xb < x1; xb += UNR) {
 #pragma unroll
-    for (int k = 0; k < NSL; ++k) {
-      const int x = xb + k;
+    for (int k0 = 0; k0 < UNR; ++k0) {
+      const int x = xb + k0;
       if (x >= x1) break;
-      const int im = k % 3, ic = (k + 1) % 3, ip = (k + 2) % 3;
-      if (x + NSL - 1 < x1) issue(x + NSL - 1, (k + NSL - 1) % NSL);
+      const int k = NSL == 3 ? k0 : sr;
+      const int im = k0 % 3, ic = (k0 + 1) % 3, ip = (k0 + 2) % 3;
+      if (x + NSL - 1 < x1) issue(x + NSL - 1, NSL == 3 ? (k0 + NSL - 1) % NSL : si);
       cp_commit();
       cp_wait<NSL - 1>();  // the group of row x has landed
+      if (NSL != 3) {
+        sr = sr + 1 == NSL ? 0 : sr + 1;
+        si = si + 1 == NSL ? 0 : si + 1;
+      }
       {
         const float4 f = ring.u1[k][tid];
         W[ip][0] = f.x; W[ip][1] = f.y; W[ip][2] = f.z; W[ip][3] = f.w;
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
                     const float* __restrict__ u1, const float* u2, float* uo,
                     float* __restrict__ rec_t, float* __restrict__ strip_t, int has1, int has2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& ring = *reinterpret_cast<LeanFwdRing<kNSL, RHO>*>(smem_raw);
+  auto& ring = *reinterpret_cast<LeanFwdRing<kFwdNSL, RHO>*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;

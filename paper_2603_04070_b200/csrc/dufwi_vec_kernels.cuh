@@ -63,9 +63,15 @@ __device__ __forceinline__ void ab4(const ABTables& T, int x, int z4, int nz, bo
 // zero-fills (rows outside the grid).  Each lane reads back only what it
 // copied, so the pipeline needs no inter-lane synchronisation.
 __device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
+#ifdef DUFWI_CP_L2_256
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)),
+               "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
                "r"(ok ? 16 : 0)
                : "memory");
+#endif
 }
 __device__ __forceinline__ void cp4(void* dst, const void* src, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src),
