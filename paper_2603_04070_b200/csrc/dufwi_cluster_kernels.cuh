@@ -181,6 +181,7 @@ struct IoStage {
   int* ring_b;
   double* srec;
   float* sring;
+  double* spulse;  // pulse samples of the stage's steps (adjoint)
   int maxrec, maxring;
 };
 
@@ -193,7 +194,7 @@ __host__ __device__ inline size_t io_offset(int rows, int rpt, int nz, int nbufs
 
 __host__ __device__ inline size_t io_bytes(int maxrec, int maxring) {
   return 16 + 2 * al16((size_t)maxrec * 4) + 2 * al16((size_t)maxring * 4) +
-         al16((size_t)kStage * maxrec * 8) + al16((size_t)kStage * maxring * 4);
+         al16((size_t)kStage * maxrec * 8) + al16((size_t)kStage * maxring * 4) + kStage * 8;
 }
 
 template <class T>
@@ -217,6 +218,8 @@ __device__ __forceinline__ IoStage io_stage(unsigned char* base, int maxrec, int
   io.srec = reinterpret_cast<double*>(base + o);
   o += al16((size_t)kStage * maxrec * 8);
   io.sring = reinterpret_cast<float*>(base + o);
+  o += al16((size_t)kStage * maxring * 4);
+  io.spulse = reinterpret_cast<double*>(base + o);
   io.maxrec = maxrec;
   io.maxring = maxring;
   return io;
@@ -276,14 +279,33 @@ __device__ __forceinline__ bool in_box(const Geo& g, int x, int z) {
 // columns with no cell in the undamped box (PML, incl. ring columns) first,
 // then columns holding any damped, receiver, ring or source cell, then plain
 // columns (every warp of those runs the fast step).  Sets c.z / c.xo.
-// scratch: 2 * nz ints of shared memory (the exchange buffers, before they
-// are zeroed).
+//
+// Warp placement: a CTA of W warps puts warp w on scheduler (SMSP) w % 4, so
+// with W % 4 != 0 some SMSPs issue for more warps than others (config 1:
+// 10 warps = 3 + 3 + 2 + 2), and the step ends when the busiest SMSP is done.
+// The heavy virtual warps — those holding PML or special columns, which run
+// the slower paths — are placed on the SMSPs with the fewest warps, the plain
+// ones fill the rest (measured per warp with DUFWI_EXP_TIMING: the io and PML
+// warps on a 3-warp SMSP set the step time).  Needs nz % 32 == 0 so that a
+// warp's lanes stay within one row segment.
+// scratch: 2 * nz + 64 + W ints of shared memory (the exchange buffers,
+// before they are zeroed).
+#ifndef DUFWI_PLACE_FWD
+#define DUFWI_PLACE_FWD 1
+#endif
+#ifndef DUFWI_PLACE_ADJ
+#define DUFWI_PLACE_ADJ 0
+#endif
 template <class T>
 __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx, int txz,
-                                              int* scratch) {
+                                              int* scratch, int rpt, int mode) {
   const int nz = g.nz;
   int* cls = scratch;
   int* order = scratch + nz;
+  int* wmap = scratch + 2 * nz;  // physical warp -> virtual warp
+  const int W = blockDim.x >> 5;
+  // mode 0: identity, 1: heavy warps on the SMSPs with fewest warps, 2: one heavy per SMSP
+  const bool place = mode != 0 && (blockDim.x & 31) == 0 && (nz & 31) == 0 && W <= 64;
   for (int z = threadIdx.x; z < nz; z += blockDim.x) {
     int plain = 1, boxed = 0;
     for (int lr = 0; lr < c.nr; ++lr) {
@@ -298,12 +320,40 @@ __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx,
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int k = 0;
+    int k = 0, nheavy = 0;
     for (int q = 0; q < 3; ++q)
       for (int z = 0; z < nz; ++z)
-        if (cls[z] == q) order[k++] = z;
+        if (cls[z] == q) {
+          order[k++] = z;
+          nheavy += q < 2;
+        }
+    if (place) {
+      // physical warps, SMSPs with fewer warps first; virtual warps, heavy first
+      const int bps = nz >> 5, hb = (nheavy + 31) >> 5;
+      int cnt[4] = {0, 0, 0, 0};
+      for (int w = 0; w < W; ++w) ++cnt[w & 3];
+      int n = 0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int v = 0; v < W; ++v)
+          if (((v % bps) < hb) == (pass == 0)) wmap[64 + n++] = v;  // staged virtual order
+      int i = 0;
+      if (mode == 2) {
+        for (int w = 0; w < W; ++w) wmap[w] = wmap[64 + w];  // round robin over SMSPs
+      } else {
+        for (int m = 1; m <= 64 && i < W; ++m)  // SMSPs holding m warps, in SMSP order
+          for (int s = 0; s < 4; ++s)
+            if (cnt[s] == m)
+              for (int w = s; w < W; w += 4) wmap[w] = wmap[64 + i++];
+      }
+    }
   }
   __syncthreads();
+  if (place) {
+    const int vt = wmap[threadIdx.x >> 5] * 32 + (threadIdx.x & 31);
+    c.seg = vt / nz;
+    c.zi = vt - c.seg * nz;
+    c.lrow0 = c.seg * rpt;
+  }
   c.z = order[c.zi];
   c.xo = (c.z + 1) * c.RS + c.lrow0 + 1;
   c.off_dn = (uint32_t)((c.z + 1) * c.RS) * (uint32_t)sizeof(T);        // top halo of rank+1
@@ -581,7 +631,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const uint32_t bar_off = (uint32_t)bar_offset<T>(rows, RPT, g.nz, 2);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
-  order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem));
+  order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem), RPT, DUFWI_PLACE_FWD);
   for (size_t i = threadIdx.x; i < 2 * xe; i += blockDim.x) X[0][i] = T(0);
   const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 2), maxrec, maxring);
   if (threadIdx.x == 0) {
@@ -672,9 +722,8 @@ template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF, bool IO,
 __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
                                          double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
                                          double (&ub)[RPT], double (&acc)[RPT], int i, int U,
-                                         int lu, const AdjBufs<T>& B, double pulse_t,
-                                         const IoStage& io, const float* __restrict__ hist,
-                                         size_t N2) {
+                                         int lu, const AdjBufs<T>& B, const IoStage& io,
+                                         const float* __restrict__ hist, size_t N2) {
   const int RS = c.RS, z = c.z;
   const int t = g.nt - 1 - i;
   const int k = i % kStage;
@@ -757,7 +806,9 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
         acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
         if (T2 || t >= 2) {
           double prev = recon(ub[j], ua[j], s.ed[j], lapu[j]);
-          if ((!PLAIN || IO) && (s.src & (1u << j))) prev = __dadd_rn(prev, pulse_t);
+          // source sample s[t] from the shared-memory stage (a global load here
+          // would sit on the step's critical path)
+          if ((!PLAIN || IO) && (s.src & (1u << j))) prev = __dadd_rn(prev, io.spulse[k]);
           ua[j] = prev;
         }
       } else if ((s.gmask & (1u << j)) && (T2 || t >= 2)) {
@@ -792,6 +843,7 @@ __device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, 
       const int t = g.nt - 1 - (i0 + k);
       io.sring[k * io.maxring + r] = t >= 2 ? strips[((size_t)(t - 2) * U + lu) * g.SL + io.ring_g[r]] : 0.f;
     }
+    if (threadIdx.x < nk) io.spulse[threadIdx.x] = g.pulse[g.nt - 1 - (i0 + threadIdx.x)];
   }
 }
 
@@ -800,7 +852,7 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
                                          double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
                                          double (&ub)[RPT], double (&acc)[RPT], int i, int U,
                                          int lu, const AdjBufs<T>& B, uint32_t tx_bytes,
-                                         double pulse_t, const IoStage& io,
+                                         const IoStage& io,
                                          const float* __restrict__ hist, size_t N2) {
 #ifdef DUFWI_EXP_TIMING
   const long long T0 = clock64();
@@ -811,9 +863,14 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
 #endif
 #define DUFWI_ADJ_BODY(FULL, PLAIN, UNIF, IO, NOIMG)                                           \
   adj_body<RPT, T, MODE, FULL, PLAIN, UNIF, IO, NOIMG, T2>(g, c, s, l1, l2, ua, ub, acc, i, U, lu, \
-                                                           B, pulse_t, io, hist, N2)
+                                                           B, io, hist, N2)
+#ifdef DUFWI_EXP_NOIO
+  if (MODE == 2 && (s.fast || s.plainio))
+    DUFWI_ADJ_BODY(true, true, false, false, false);
+#else
   if (MODE == 2 && s.fast)
     DUFWI_ADJ_BODY(true, true, false, false, false);
+#endif
   else if (MODE == 2 && s.plainio)
     DUFWI_ADJ_BODY(true, true, false, true, false);
   else if (MODE == 2 && s.pml && s.unif)
@@ -856,7 +913,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const uint32_t bar_off = (uint32_t)bar_offset<T>(rows, RPT, g.nz, 4);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
-  order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem));
+  order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem), RPT, DUFWI_PLACE_ADJ);
   for (size_t k = threadIdx.x; k < 4 * xe; k += blockDim.x) base[k] = T(0);
   const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 4), maxrec, maxring);
   if (threadIdx.x == 0) {
@@ -898,7 +955,6 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
       ub[j] = u_prev[cell];
     }
   }
-  const bool owns_src = st.src != 0u;
   cluster_sync_all();
 
   // step i writes XL[i&1], XU[i&1], bar[i&1]; reads XL[(i+1)&1], XU[(i+1)&1], bar[(i+1)&1]
@@ -909,22 +965,19 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   int i = 0;
   for (; i + 1 < nt - 2; i += 2) {
     if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
-    const double p0 = owns_src ? g.pulse[nt - 1 - i] : 0.0;
-    adj_step<RPT, T, MODE, true>(g, c, st, la, lb, ua, ub, acc, i, U, lu, B0, tx_bytes, p0, io,
-                                 hist, N2);
-    const double p1 = owns_src ? g.pulse[nt - 2 - i] : 0.0;
-    adj_step<RPT, T, MODE, true>(g, c, st, lb, la, ub, ua, acc, i + 1, U, lu, B1, tx_bytes, p1, io,
+    adj_step<RPT, T, MODE, true>(g, c, st, la, lb, ua, ub, acc, i, U, lu, B0, tx_bytes, io, hist,
+                                 N2);
+    adj_step<RPT, T, MODE, true>(g, c, st, lb, la, ub, ua, acc, i + 1, U, lu, B1, tx_bytes, io,
                                  hist, N2);
   }
   for (; i < nt; ++i) {
     if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
-    const double p = owns_src ? g.pulse[nt - 1 - i] : 0.0;
     if (i & 1)
-      adj_step<RPT, T, MODE, false>(g, c, st, lb, la, ub, ua, acc, i, U, lu, B1, tx_bytes, p, io,
-                                    hist, N2);
+      adj_step<RPT, T, MODE, false>(g, c, st, lb, la, ub, ua, acc, i, U, lu, B1, tx_bytes, io, hist,
+                                    N2);
     else
-      adj_step<RPT, T, MODE, false>(g, c, st, la, lb, ua, ub, acc, i, U, lu, B0, tx_bytes, p, io,
-                                    hist, N2);
+      adj_step<RPT, T, MODE, false>(g, c, st, la, lb, ua, ub, acc, i, U, lu, B0, tx_bytes, io, hist,
+                                    N2);
   }
   if (c.has_up || c.has_dn) mbar_wait(bar[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
   cluster_sync_all();
