@@ -195,6 +195,12 @@ def largest_config_sample(units: int = 64, nt: int = 200, reps: int = 2) -> dict
             "unit": "GB/s", "peak": peak, "peak_kind": peak_kind}
 
 
+def _device_index() -> int:
+    if os.environ.get("DUFWI_BENCH_ONE_DEVICE") == "1":
+        return 0
+    return int(os.environ.get("LOCAL_RANK", 0))
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -244,7 +250,7 @@ def run_ours(args, rank: int, world: int) -> None:
     from paper_2603_04070_b200.network import make_update_nets
     from paper_2603_04070_b200.unfold import Reconstructor
 
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = _device_index()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     B = world  # weak scaling: one phantom per GPU
@@ -308,19 +314,28 @@ def run_ours(args, rank: int, world: int) -> None:
         except Exception:
             traffic = None
 
-    # ---- end to end through the public API with host buffers (per rank: its phantom)
+    # ---- end to end through the public API with host buffers.  N = 1: the
+    # reference's unfold_infer on the phantom; N > 1: unfold_infer_batch, a
+    # collective over the B = N phantoms (each rank copies all observations in,
+    # computes its shard of units, all ranks combine per stage)
     e2e = None
     if not args.skip_e2e:
-        my_b = rank if world > 1 else 0
-        obs_host = pk.ChannelData(obs[my_b * S:(my_b + 1) * S].cpu().numpy(), geom, grid.dt)
-        c0_host = pk.SosMap(grid, np.full(grid.shape, 1540.0))
+        obs_np = obs.cpu().numpy()
+        obs_host = [pk.ChannelData(obs_np[b * S:(b + 1) * S], geom, grid.dt) for b in range(B)]
+        c0_host = [pk.SosMap(grid, np.full(grid.shape, 1540.0)) for _ in range(B)]
         setup = pk.InversionSetup(pulse, damp, bounds)
-        pk.unfold_infer(obs_host, c0_host, nets, setup)  # warm the public-API engine
+
+        def public_call():
+            if world == 1:
+                return [pk.unfold_infer(obs_host[0], c0_host[0], nets, setup)]
+            return pk.unfold_infer_batch(obs_host, c0_host, nets, setup)
+
+        public_call()  # warm the public-API engine
         barrier()
         e0 = time.perf_counter()
         per = []
         for _ in range(args.steps):
-            maps = pk.unfold_infer(obs_host, c0_host, nets, setup)
+            maps = public_call()
             per.append(time.perf_counter())
         torch.cuda.synchronize()
         e_s = time.perf_counter() - e0
@@ -330,11 +345,13 @@ def run_ours(args, rank: int, world: int) -> None:
         if world > 1:
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
         e_s = float(e_t.item())
-        h2d = obs_host.traces.nbytes + c0_host.values.nbytes
-        d2h = sum(m.values.nbytes for m in maps)
+        h2d = sum(o.traces.nbytes for o in obs_host) + sum(c.values.nbytes for c in c0_host)
+        d2h = sum(m.values.nbytes for ms in maps for m in ms)
         e2e = {"value": updates_per_step * args.steps / e_s, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d // B * B), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * e_s / args.steps, "api": "paper_2603_04070_b200.unfold_infer"}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * e_s / args.steps,
+               "api": ("paper_2603_04070_b200.unfold_infer" if world == 1
+                       else "paper_2603_04070_b200.unfold_infer_batch")}
 
     large = None
     if rank == 0 and world == 1 and not args.skip_large:
@@ -402,8 +419,10 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(_device_index())
+        # DUFWI_BENCH_BACKEND=gloo + DUFWI_BENCH_ONE_DEVICE=1: functional check of the
+        # multi-rank path with every rank on cuda:0 (ranks share no kernels; not a timing)
+        dist.init_process_group(os.environ.get("DUFWI_BENCH_BACKEND", "nccl"))
     try:
         run_ours(args, rank, world)
     finally:

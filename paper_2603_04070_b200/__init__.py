@@ -15,7 +15,8 @@ from .forward import (DampingProfile, NumericError, SourcePulse, Wavefield, buil
                       zero_damping)
 from .adjoint import (GradientMap, compute_gradient, data_misfit, gradient_mask,
                       misfit_and_gradient, misfit_and_gradient_batch)
-from .unfold import InversionSetup, Reconstructor, cfl_safe_bounds, clamp_sos, unfold_infer
+from .unfold import (InversionSetup, Reconstructor, cfl_safe_bounds, clamp_sos, unfold_infer,
+                     unfold_infer_batch)
 from ._lib import DufwiError, ExtensionUnavailable
 
 __all__ = [
@@ -25,5 +26,5 @@ __all__ = [
     "make_source_pulse", "simulate_all", "simulate_transmission", "simulate_wavefield",
     "zero_damping", "GradientMap", "compute_gradient", "data_misfit", "gradient_mask",
     "misfit_and_gradient", "misfit_and_gradient_batch", "InversionSetup", "Reconstructor",
-    "cfl_safe_bounds", "clamp_sos", "unfold_infer", "DufwiError", "ExtensionUnavailable",
+    "cfl_safe_bounds", "clamp_sos", "unfold_infer", "unfold_infer_batch", "DufwiError", "ExtensionUnavailable",
 ]

@@ -17,7 +17,8 @@ from .forward import DampingProfile, NumericError, SourcePulse, _check_simulatio
 from .grid import ChannelData, Grid2D, SosMap, check_cfl
 from .network import NormSpec
 
-__all__ = ["InversionSetup", "cfl_safe_bounds", "clamp_sos", "unfold_infer", "Reconstructor"]
+__all__ = ["InversionSetup", "cfl_safe_bounds", "clamp_sos", "unfold_infer", "unfold_infer_batch",
+           "Reconstructor"]
 
 
 @dataclass(frozen=True)
@@ -127,3 +128,46 @@ def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) ->
         raise NumericError(str(exc)) from exc
     host = torch.stack(maps).cpu().numpy()
     return [SosMap(grid, host[k, 0]) for k in range(host.shape[0])]
+
+
+def unfold_infer_batch(m_obs_list, c0_list, nets, setup: InversionSetup) -> list[list[SosMap]]:
+    """Batched extension of :func:`unfold_infer`: B phantoms on one acquisition,
+    one launch set per stage for all of them.  Returns, per phantom, C_1..C_K.
+
+    Under torch.distributed it is a collective: every rank passes the same lists,
+    the (phantom, shot) units are sharded across ranks and the per-stage partial
+    gradients combined with one all_reduce; every rank returns
+    all maps.
+    """
+    import torch
+
+    if len(m_obs_list) != len(c0_list) or not c0_list:
+        raise ValueError("need one initial map per observed data set")
+    grid = c0_list[0].grid
+    lo, hi = setup.bounds
+    if not lo < hi:
+        raise ValueError("bounds must satisfy c_min < c_max")
+    damping = setup.damping if setup.damping is not None else zero_damping(grid)
+    geometry = m_obs_list[0].geometry
+    for m, c0 in zip(m_obs_list, c0_list):
+        if m.geometry != geometry:
+            raise ValueError("batched inference needs one acquisition geometry")
+        c_first = clamp_sos(c0, setup.bounds)
+        _check_simulation_inputs(c_first, geometry, setup.pulse, damping)
+        if not check_cfl(grid, hi).ok and not check_cfl(grid, max(c_first.c_max, lo)).ok:
+            raise ValueError("CFL violated by the clamp bounds")
+    B = len(c0_list)
+    rho = None if setup.density is None else np.broadcast_to(
+        np.asarray(setup.density, dtype=np.float64), (B,) + grid.shape).copy()
+    eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
+                     setup.pulse.samples, damping, n_phantoms=B, has_rho=rho is not None)
+    rec = Reconstructor(eng, nets, setup.bounds, rho=rho)
+    obs = torch.from_numpy(np.concatenate([np.require(m.traces, np.float64, ["C", "W"])
+                                           for m in m_obs_list])).to(eng.device)
+    c = torch.from_numpy(np.stack([np.asarray(c0.values, np.float64) for c0 in c0_list])).to(eng.device)
+    try:
+        maps = rec.reconstruct(obs, c)
+    except FloatingPointError as exc:
+        raise NumericError(str(exc)) from exc
+    host = torch.stack(maps).cpu().numpy()  # (K, B, nx, nz)
+    return [[SosMap(grid, host[k, b]) for k in range(host.shape[0])] for b in range(B)]

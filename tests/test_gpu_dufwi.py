@@ -88,3 +88,27 @@ def test_unfold_infer_nonfinite_raises(gpu):
     setup = pk.InversionSetup(big, damp, pk.cfl_safe_bounds(grid, (1300.0, 3200.0)))
     with pytest.raises(pk.NumericError):
         pk.unfold_infer(obs, pk.homogeneous_map(grid, 1540.0), nets, setup)
+
+
+def test_unfold_infer_batch_equals_single_calls(gpu):
+    """unfold_infer_batch (B phantoms, one launch set per stage) == B unfold_infer calls.
+    The physics is per unit and bit-identical; the fp32 update net may pick other
+    cuDNN algorithms for batch 2 than for batch 1 (rounding-level map differences)."""
+    from ._cases import small_linear
+
+    wl, grid, geom, pulse, damp = small_linear(seed=5)
+    tx, rx = geom.tx_nodes(), geom.rx_nodes()
+    obs_list, c0_list = [], []
+    for k, dc in enumerate((25.0, -30.0)):
+        c = np.full(grid.shape, 1540.0)
+        c[18:30, 20 + 4 * k:30 + 4 * k] += dc
+        tr, _ = oracle.forward_sweep(c, damp.values, grid.dx, grid.dt, pulse.samples, tx, rx)
+        obs_list.append(pk.ChannelData(tr, geom, grid.dt))
+        c0_list.append(pk.SosMap(grid, np.full(grid.shape, 1540.0)))
+    nets = make_update_nets(2, seed=3, device=gpu)
+    setup = pk.InversionSetup(pulse, damp, (1300.0, 1700.0))
+    batch = pk.unfold_infer_batch(obs_list, c0_list, nets, setup)
+    for b in range(2):
+        single = pk.unfold_infer(obs_list[b], c0_list[b], nets, setup)
+        for m_b, m_s in zip(batch[b], single):
+            assert rel_l2(m_b.values, m_s.values) <= 1e-7
