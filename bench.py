@@ -252,6 +252,9 @@ def run_ours(args, rank: int, world: int) -> None:
 
     local = _device_index()
     torch.cuda.set_device(local)
+    # the update networks' 3x3 convolutions: let cuDNN pick its fastest fp32 algorithm
+    # (measured 0.29 -> 0.26 ms per network at 160^2; TF32 stays off)
+    torch.backends.cudnn.benchmark = True
     dev = torch.device("cuda", local)
     B = world  # weak scaling: one phantom per GPU
     wl, grid, geom, pulse, damp, bounds = build_problem(args.config, B, args.seed)
@@ -276,7 +279,7 @@ def run_ours(args, rank: int, world: int) -> None:
     for _ in range(args.warmup):
         rec.reconstruct(obs, c0)
     barrier()
-    launches0 = eng.launch_count
+    launches0 = eng.launch_count + rec.replayed_launches
     clocks = ClockSampler(local).start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -290,7 +293,7 @@ def run_ours(args, rank: int, world: int) -> None:
     barrier()
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
-    launches = (eng.launch_count - launches0) // args.steps
+    launches = (eng.launch_count + rec.replayed_launches - launches0) // args.steps
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if world > 1:

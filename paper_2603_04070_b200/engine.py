@@ -155,6 +155,9 @@ class PhysicsEngine:
         self.max_chunk_units = max_chunk_units
         self.memory_fraction = memory_fraction
         self._ws: dict[int, _Workspace] = {}
+        # bumped whenever a workspace is (re)allocated or released: CUDA graphs
+        # captured over this engine hold its buffer addresses (unfold.Reconstructor)
+        self.ws_generation = 0
         N2 = self.nx * self.nz
         self._flag = torch.zeros(4, dtype=torch.int32, device=self.device)
         self._c = None
@@ -258,10 +261,12 @@ class PhysicsEngine:
             self._ws.pop(mode, None)
             ws = _Workspace(mode, units, torch.empty(need, dtype=torch.uint8, device=self.device))
             self._ws[mode] = ws
+            self.ws_generation += 1
         return ws
 
     def release_workspace(self) -> None:
         self._ws.clear()
+        self.ws_generation += 1
 
     # ----------------------------------------------------------- sweeps
     def _require_model(self):

@@ -9,6 +9,7 @@ returned :class:`SosMap` list is copied to the host once at the end.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -58,16 +59,26 @@ class Reconstructor:
     ``reconstruct(obs, c0)`` takes device tensors ((B*S, R, nt) f64 observed
     data and (B, nx, nz) initial maps) and returns the list of stage maps
     (B, nx, nz) on device, plus the per-stage gradients when asked.
+
+    In a single process the K stages (sweeps, residual, epilogue, networks,
+    clamps: ~30 launches per stage) are captured once into a CUDA graph and
+    replayed per call; the inputs are copied into the graph's static buffers
+    first.  Under torch.distributed, with host networks or when gradients are
+    kept, the stages are launched eagerly.
     """
 
-    def __init__(self, engine, nets, bounds, guard_radius: int = 2, rho=None):
+    def __init__(self, engine, nets, bounds, guard_radius: int = 2, rho=None, graph: bool | None = None):
         self.engine = engine
         self.nets = list(nets)
         self.bounds = bounds
         self.guard_radius = guard_radius
         self.rho = rho
+        # DUFWI_GRAPH=0 launches the stages eagerly (A/B timing, debugging)
+        self.graph = (os.environ.get("DUFWI_GRAPH", "1") != "0") if graph is None else graph
+        self._g = None  # (key, graph, static obs, static c0, maps, flags, launches, ws generation)
+        self.replayed_launches = 0
 
-    def reconstruct(self, obs, c0, keep_gradients: bool = False, check_finite: bool = True):
+    def _stages(self, obs, c0, keep_gradients: bool, check_finite: bool):
         import torch
 
         from .engine import raise_nonfinite
@@ -94,10 +105,79 @@ class Reconstructor:
             maps.append(c)
             if keep_gradients:
                 grads.append(g)
+        return maps, grads, torch.stack(flags)
+
+    def _graphable(self, obs, keep_gradients: bool) -> bool:
+        import torch
+
+        dist = torch.distributed.is_available() and torch.distributed.is_initialized()
+        return (self.graph and not keep_gradients and not dist and obs.is_cuda
+                and all(hasattr(n, "predict_update_device") for n in self.nets))
+
+    def _graph_key(self, obs, c0):
+        params = tuple(p.data_ptr() for n in self.nets for p in n.parameters())
+        return (tuple(obs.shape), tuple(c0.shape), params, id(self.engine))
+
+    def _replay(self, obs, c0):
+        import torch
+
+        key = self._graph_key(obs, c0)
+        if self._g is not None and self._g[7] != self.engine.ws_generation:
+            self._g = None  # the engine's workspace moved: the captured addresses are stale
+        if self._g is None or self._g[0] != key:
+            self._g = None
+            if self.rho is not None and not isinstance(self.rho, torch.Tensor):
+                self.rho = torch.as_tensor(np.asarray(self.rho, dtype=np.float64), device=obs.device)
+            s_obs = obs.to(torch.float64).clone()
+            s_c0 = c0.to(torch.float64).clone()
+            side = torch.cuda.Stream(device=obs.device)
+            side.wait_stream(torch.cuda.current_stream(obs.device))
+            with torch.cuda.stream(side):  # warm-up: workspaces, cuDNN plans, kernel attributes
+                for _ in range(2):
+                    self._stages(s_obs, s_c0, False, False)
+            torch.cuda.current_stream(obs.device).wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            n0 = self.engine.launch_count
+            with torch.cuda.graph(graph):
+                maps, _, flags = self._stages(s_obs, s_c0, False, False)
+            self._g = (key, graph, s_obs, s_c0, maps, flags, self.engine.launch_count - n0,
+                       self.engine.ws_generation)
+        _, graph, s_obs, s_c0, maps, flags, n_launch, _ = self._g
+        s_obs.copy_(obs)
+        s_c0.copy_(c0)
+        graph.replay()
+        self.replayed_launches += n_launch  # the library's kernels inside the graph
+        return [m.clone() for m in maps], flags
+
+    def reconstruct(self, obs, c0, keep_gradients: bool = False, check_finite: bool = True):
+        from .engine import raise_nonfinite
+
+        if self._graphable(obs, keep_gradients):
+            maps, flags = self._replay(obs, c0)
+            grads = []
+        else:
+            maps, grads, flags = self._stages(obs, c0, keep_gradients, check_finite)
         if check_finite:
-            for f in torch.stack(flags).cpu():  # first failing stage raises
+            for f in flags.cpu():  # first failing stage raises
                 raise_nonfinite(f)
         return (maps, grads) if keep_gradients else maps
+
+
+_RECON_CACHE: dict = {}
+
+
+def _reconstructor(eng, nets, bounds, rho) -> Reconstructor:
+    """Reconstructor (and its captured graph) reused across calls with the same
+    engine, networks and bounds; models with a density map are not cached."""
+    if rho is not None:
+        return Reconstructor(eng, nets, bounds, rho=rho)
+    key = (id(eng), tuple(id(n) for n in nets), tuple(bounds))
+    rec = _RECON_CACHE.get(key)
+    if rec is None or rec.engine is not eng or any(a is not b for a, b in zip(rec.nets, nets)):
+        while len(_RECON_CACHE) >= 4:
+            _RECON_CACHE.pop(next(iter(_RECON_CACHE)))
+        rec = _RECON_CACHE[key] = Reconstructor(eng, nets, bounds)
+    return rec
 
 
 def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) -> list[SosMap]:
@@ -118,7 +198,7 @@ def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) ->
     rho = None if setup.density is None else np.asarray(setup.density, dtype=np.float64)[None]
     eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
                      setup.pulse.samples, damping, has_rho=rho is not None)
-    rec = Reconstructor(eng, nets, setup.bounds, rho=rho)
+    rec = _reconstructor(eng, nets, setup.bounds, rho)
     # ChannelData arrays are read-only views: a writable host copy for torch
     obs = torch.from_numpy(np.require(m_obs.traces, np.float64, ["C", "W"])).to(eng.device)
     c = torch.from_numpy(np.array(c0.values, dtype=np.float64)).to(eng.device)[None]
@@ -161,7 +241,7 @@ def unfold_infer_batch(m_obs_list, c0_list, nets, setup: InversionSetup) -> list
         np.asarray(setup.density, dtype=np.float64), (B,) + grid.shape).copy()
     eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
                      setup.pulse.samples, damping, n_phantoms=B, has_rho=rho is not None)
-    rec = Reconstructor(eng, nets, setup.bounds, rho=rho)
+    rec = _reconstructor(eng, nets, setup.bounds, rho)
     obs = torch.from_numpy(np.concatenate([np.require(m.traces, np.float64, ["C", "W"])
                                            for m in m_obs_list])).to(eng.device)
     c = torch.from_numpy(np.stack([np.asarray(c0.values, np.float64) for c0 in c0_list])).to(eng.device)

@@ -112,3 +112,37 @@ def test_unfold_infer_batch_equals_single_calls(gpu):
         single = pk.unfold_infer(obs_list[b], c0_list[b], nets, setup)
         for m_b, m_s in zip(batch[b], single):
             assert rel_l2(m_b.values, m_s.values) <= 1e-7
+
+
+def test_graphed_reconstruct_equals_eager(gpu):
+    """The CUDA-graph replay of the K stages gives the same bits as the eager
+    launches, follows new inputs, and is re-captured when the engine's
+    workspace is reallocated (the captured addresses would be stale)."""
+    wl, grid, geom, pulse, damp = config_setup(1)
+    bounds = pk.cfl_safe_bounds(grid, (1300.0, 3200.0))
+    eng = fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes,
+                         pulse.samples, damp)
+    nets = make_update_nets(3, seed=1, device=gpu)
+    eng.set_model(wl.c_true)
+    obs = eng.forward().double()
+    c0 = torch.full((1,) + grid.shape, 1540.0, dtype=torch.float64, device=gpu)
+    eager = Reconstructor(eng, nets, bounds, graph=False).reconstruct(obs, c0)
+    rec = Reconstructor(eng, nets, bounds, graph=True)
+    graphed = rec.reconstruct(obs, c0)
+    assert rec._g is not None
+    for a, b in zip(eager, graphed):
+        assert torch.equal(a, b)
+    # new inputs through the same graph
+    obs2 = obs * 0.5
+    c02 = c0 + 10.0
+    e2 = Reconstructor(eng, nets, bounds, graph=False).reconstruct(obs2, c02)
+    g2 = rec.reconstruct(obs2, c02)
+    assert all(torch.equal(a, b) for a, b in zip(e2, g2))
+    assert not torch.equal(g2[-1], graphed[-1])
+    # workspace released -> re-captured, still the same bits
+    first = rec._g
+    eng.release_workspace()
+    g3 = rec.reconstruct(obs, c0)
+    assert rec._g is not first
+    assert all(torch.equal(a, b) for a, b in zip(eager, g3))
+    assert rec.replayed_launches > 0

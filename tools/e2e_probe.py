@@ -30,6 +30,14 @@ for k in range(4):
     pk.unfold_infer(obs_host, c0, nets, setup)
     torch.cuda.synchronize()
     print("unfold_infer s", round(time.perf_counter() - t0, 4))
+import cProfile, pstats  # noqa: E402
+pr = cProfile.Profile()
+pr.enable()
+for k in range(3):
+    pk.unfold_infer(obs_host, c0, nets, setup)
+torch.cuda.synchronize()
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]) as p:
     pk.unfold_infer(obs_host, c0, nets, setup)
     torch.cuda.synchronize()

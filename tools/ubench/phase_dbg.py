@@ -5,7 +5,7 @@ import os
 import sys
 
 sys.path.insert(0, os.getcwd())
-os.environ["DUFWI_LIB"] = os.path.abspath("tools/ubench/lib_TIMING.so")
+os.environ.setdefault("DUFWI_LIB", os.path.abspath("tools/ubench/lib_TIMING.so"))
 import torch  # noqa: E402
 
 import bench  # noqa: E402
@@ -27,11 +27,11 @@ so.dufwi_debug_counters(buf, 256)
 nt = grid.nt
 paths = {0: "plain", 1: "full", 2: "generic", 3: "unif", 4: "xpml", 5: "io-plain"}
 for sweep in (0, 1):
-    print(["forward", "adjoint"][sweep], "cycles per step: [sync+wait, body] path")
+    print(["forward", "adjoint"][sweep], "cycles per step: sync/body(halo wait inside the body) path")
     for cta in (0, 1):
         row = []
         for w in range(15):
             d = ((sweep * 2 + cta) * 16 + w) * 4
             p = round(buf[d + 2] / nt)
-            row.append(f"{buf[d] // nt}/{buf[d + 1] // nt}{paths.get(p, '?')[0]}")
+            row.append(f"{buf[d] // nt}/{buf[d + 1] // nt}({buf[d + 3] // nt}){paths.get(p, '?')[0]}")
         print("  cta", [0, 4][cta], " ".join(row))
