@@ -157,10 +157,12 @@ def cpu_gradient_sample(wl, grid, geom, pulse, damp, workers: int):
     return updates / dt_s, dt_s
 
 
-def largest_config_sample(units: int = 64, nt: int = 200, reps: int = 2) -> dict:
+def largest_config_sample(units: int = 256, nt: int = 200, reps: int = 2) -> dict:
     """Stepwise-engine kernels on the largest config (BASELINE configs[4]: 1088^2
     padded grid, strips), on a bounded sample: the first ``units`` (phantom, shot)
-    units at ``nt`` steps.  Forward / adjoint C-ABI calls timed with CUDA events on
+    units at ``nt`` steps.  256 units: the full gradient runs its 1024 units in
+    chunks of ~650 (profiles/r01_full_configs.jsonl), so a launch this wide is
+    representative where a 64-unit one under-fills the 148 SMs' last wave.  Forward / adjoint C-ABI calls timed with CUDA events on
     the launching stream; algorithmic bytes 16 / 28 per cell update."""
     import dataclasses
 

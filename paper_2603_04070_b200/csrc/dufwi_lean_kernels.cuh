@@ -21,10 +21,9 @@
 // L_rho u = rho_c sum_j f_cj (u_j - u_c) with face factors f_cj = (q_c + q_j)/2,
 // q = 1/rho, outer faces f = q_c and u = 0 outside (oracle rho_face_weights).
 // Writing D u = sum_j f_cj u_j - S_c u_c (S_c = sum of the 4 face factors),
-// L_rho = diag(rho) D with D symmetric, so per phantom only three tables are
-// streamed: Er = rho E / dx^2, fxe (x faces, nx+1 rows incl. the outer ones)
-// and fz (z faces; the outer face of z = nz-1 in the last column, of z = 0 in
-// fz0[x]):
+// L_rho = diag(rho) D with D symmetric, so per phantom two maps are streamed:
+// Er = rho E / dx^2 and q; the face factors of D are formed in registers from
+// the q rows (QRing, rho_row):
 //   forward   u[t]  = A u1 + B u2 + Er * D(u1)
 //   adjoint   lam   = A l1 + B l2 + D(Er * l1)        ((E L_rho)^T = D diag(Er))
 //   imaging   acc  += D(u[t-1]) * lam, scaled by rho once in reduce_groups
@@ -114,52 +113,121 @@ __device__ __forceinline__ double lapf(double c, double xm, double xp, double zm
   return __fma_rn(fzp, zp, __fma_rn(fzm, zm, __fma_rn(fxp, xp, __fma_rn(fxm, xm, __dmul_rn(-S, c)))));
 }
 
-// Face tables of the density operator, streamed alongside the fields.
+// q = 1/rho rows of the density operator, streamed alongside the fields.  The
+// face factors are formed in registers as 0.5 * (q_c + q_j): the expression
+// (hence the bits) of the oracle's rho_face_weights and of rho_faces_kernel's
+// tables; an outer face is 0.5 * (q_c + q_c) == q_c exactly.  One f64 stream
+// (8 B per cell) instead of the two face tables (16 B), and 40 B instead of
+// 72 B of ring per lane and slot.
 template <int NSL>
-struct FaceRing {
-  double2 fx0[NSL][kLeanT], fx1[NSL][kLeanT];  // fxe row (cells 0-1, 2-3)
-  double2 fz0[NSL][kLeanT], fz1[NSL][kLeanT];  // fz row
-  double fze[NSL][kLeanT];                     // z face left of the strip (lane 0)
+struct QRing {
+  double2 q0[NSL][kLeanT], q1[NSL][kLeanT];  // q row (cells 0-1, 2-3)
+  double qe[NSL][kLeanT];                    // q at the lane's edge column
 };
 template <int NSL, bool RHO>
-struct FaceRingOpt {};
+struct QRingOpt {};
 template <int NSL>
-struct FaceRingOpt<NSL, true> {
-  FaceRing<NSL> f;
+struct QRingOpt<NSL, true> {
+  QRing<NSL> r;
 };
 
-// Per-lane view of the face tables of one phantom.
-struct FaceLane {
-  const double* fx;   // fxe + zc (row r at r * nz)
-  const double* fz;   // fz + zc
-  const double* fze;  // lane 0: fz + z0-1 (stride nz) or fz0 (stride 1)
-  int fze_stride;
+// Per-lane view of one phantom's q map.
+struct QLane {
+  const double* q;   // q + zc (row r at r * nz)
+  const double* qe;  // q + edge column (lane 0: z0-1, lane 31: z0+128)
+  bool edge;         // the lane has an edge column inside the grid
+  bool lo, hi;       // the lane's first / last cell is z = 0 / z = nz-1 (outer faces)
 };
 
-__device__ __forceinline__ FaceLane face_lane(const Model& m, const Geo& g, int b, int zc, int z0) {
-  FaceLane F;
-  const size_t N2 = (size_t)g.nx * g.nz;
-  F.fx = opaque(m.fxe + (size_t)b * (N2 + g.nz) + zc);
-  F.fz = opaque(m.fz + (size_t)b * N2 + zc);
-  if (z0 > 0) {
-    F.fze = opaque(m.fz + (size_t)b * N2 + z0 - 1);
-    F.fze_stride = g.nz;
-  } else {
-    F.fze = opaque(m.fz0 + (size_t)b * g.nx);
-    F.fze_stride = 1;
-  }
-  return F;
+__device__ __forceinline__ QLane q_lane(const Model& m, const Geo& g, int b, int zc, int z0,
+                                        int lane, int z4) {
+  QLane Q;
+  const double* qb = m.q + (size_t)b * g.nx * g.nz;
+  const bool el = lane == 0 && z0 > 0, er = lane == 31 && z0 + 128 < g.nz;
+  Q.q = opaque(qb + zc);
+  Q.qe = opaque(qb + (el ? z0 - 1 : er ? z0 + 128 : 0));
+  Q.edge = el || er;
+  Q.lo = z4 == 0;
+  Q.hi = z4 + 4 >= g.nz;
+  return Q;
 }
 
 template <int NSL>
-__device__ __forceinline__ void issue_faces(FaceRing<NSL>& R, const FaceLane& F, int tid, int sl,
-                                            int rfx, bool okfx, int rfz, bool okfz, bool act,
-                                            bool lane0, int nz) {
-  cp16(&R.fx0[sl][tid], F.fx + rfx * nz, okfx && act);
-  cp16(&R.fx1[sl][tid], F.fx + rfx * nz + 2, okfx && act);
-  cp16(&R.fz0[sl][tid], F.fz + rfz * nz, okfz && act);
-  cp16(&R.fz1[sl][tid], F.fz + rfz * nz + 2, okfz && act);
-  cp8(&R.fze[sl][tid], F.fze + rfz * F.fze_stride, okfz && lane0);
+__device__ __forceinline__ void issue_q(QRing<NSL>& R, const QLane& Q, int tid, int sl, int r,
+                                        bool ok, bool act, int nz) {
+  cp16(&R.q0[sl][tid], Q.q + r * nz, ok && act);
+  cp16(&R.q1[sl][tid], Q.q + r * nz + 2, ok && act);
+  cp8(&R.qe[sl][tid], Q.qe + r * nz, ok && Q.edge);
+}
+
+template <int NSL>
+__device__ __forceinline__ void read_q(const QRing<NSL>& R, int tid, int sl, double (&q)[4],
+                                       double& qe) {
+  const double2 a = R.q0[sl][tid], c = R.q1[sl][tid];
+  q[0] = a.x; q[1] = a.y; q[2] = c.x; q[3] = c.y;
+  qe = R.qe[sl][tid];
+}
+
+__device__ __forceinline__ double face(double a, double b) {
+  return __dmul_rn(0.5, __dadd_rn(a, b));
+}
+
+// z faces of a lane's 4 cells in one row: fz[k] lies between cells k-1 and k
+// (fz[0] / fz[4]: the neighbours in lanes -1 / +1, the edge column, or outer).
+__device__ __forceinline__ void zfaces(const QLane& Q, int lane, const double (&q)[4], double qe,
+                                       double (&fz)[5]) {
+  double ql = __shfl_up_sync(0xffffffffu, q[3], 1);
+  double qr = __shfl_down_sync(0xffffffffu, q[0], 1);
+  if (lane == 0) ql = qe;
+  if (lane == 31) qr = qe;
+  if (Q.lo) ql = q[0];
+  if (Q.hi) qr = q[3];
+  fz[0] = face(ql, q[0]);
+#pragma unroll
+  for (int k = 1; k < 4; ++k) fz[k] = face(q[k - 1], q[k]);
+  fz[4] = face(q[3], qr);
+}
+
+// Row-walk state at the first row x0: q of row x0 (+ edge column) and the
+// x face above it, fxe[x0] = face(q[x0-1], q[x0]) (outer at x0 = 0: q[0]).
+__device__ __forceinline__ void rho_prologue(const QLane& Q, bool act, int x0, int nz,
+                                             double (&qc)[4], double& qce, double (&fx)[4]) {
+  if (act) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(Q.q + x0 * nz));
+    const double2 c = __ldg(reinterpret_cast<const double2*>(Q.q + x0 * nz + 2));
+    qc[0] = a.x; qc[1] = a.y; qc[2] = c.x; qc[3] = c.y;
+  }
+  if (Q.edge) qce = __ldg(Q.qe + x0 * nz);
+  double qm[4] = {qc[0], qc[1], qc[2], qc[3]};
+  if (act && x0 >= 1) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(Q.q + (x0 - 1) * nz));
+    const double2 c = __ldg(reinterpret_cast<const double2*>(Q.q + (x0 - 1) * nz + 2));
+    qm[0] = a.x; qm[1] = a.y; qm[2] = c.x; qm[3] = c.y;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) fx[k] = face(qm[k], qc[k]);
+}
+
+// One row x of the walk: q of row x+1 from ring slot sl (outer below the last
+// row: q of row x again) gives the x face below row x; the z faces of row x come
+// from the carried q of row x, which then advances to row x+1.
+template <int NSL>
+__device__ __forceinline__ void rho_row(const QRing<NSL>& R, const QLane& Q, int tid, int sl,
+                                        int lane, bool has_next, double (&qc)[4], double& qce,
+                                        double (&fxp)[4], double (&fz)[5]) {
+  double qn[4], qen;
+  read_q(R, tid, sl, qn, qen);
+  if (!has_next) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qn[k] = qc[k];
+    qen = qce;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) fxp[k] = face(qc[k], qn[k]);
+  zfaces(Q, lane, qc, qce, fz);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) qc[k] = qn[k];
+  qce = qen;
 }
 
 // ----------------------------------------------------------------- forward
@@ -170,12 +238,12 @@ struct LeanFwdRing {
   double2 e0[NSL][kLeanT];  // E (RHO: Er) row r, cells 0-1
   double2 e1[NSL][kLeanT];  // cells 2-3
   float edge[NSL][kLeanT];  // u[t-1] row r+1 at z0-1 (lane 0) / z0+128 (lane 31)
-  FaceRingOpt<NSL, RHO> fr; // RHO: fxe row r+1, fz row r
+  QRingOpt<NSL, RHO> fr;    // RHO: q row r+1
 };
 
 template <int MODE, bool RHO, bool ZD>
 __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, const LaneInfo& L,
-                                              LeanFwdRing<kFwdNSL, RHO>& ring, const FaceLane& FL,
+                                              LeanFwdRing<kFwdNSL, RHO>& ring, const QLane& QL,
                                               int tid, int lane, int z0, int x0, int x1, int lu,
                                               int txx, int tk, double pulse_t, const float* f1,
                                               const float* f2, const double* Ec, float* fo,
@@ -213,11 +281,11 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
     cp16(&ring.e0[sl][tid], be + orr, L.act);
     cp16(&ring.e1[sl][tid], be + orr + 2, L.act);
     cp4(&ring.edge[sl][tid], bl + on, has_edge && okn);
-    if constexpr (RHO) issue_faces(ring.fr.f, FL, tid, sl, r + 1, true, r, true, L.act, lane == 0, nz);
+    if constexpr (RHO) issue_q(ring.fr.r, QL, tid, sl, r + 1, okn, L.act, nz);
   };
   // register windows: slot (k) % 3 = row x-1, (k+1) % 3 = row x, (k+2) % 3 = row x+1;
-  // FX[s] = x face below the row of slot s (fxe[row])
-  double W[3][4], Eg[3], FX[3][4];
+  // FX[s] = x face above the row of slot s (fxe[row]); qc / qce: q of row x
+  double W[3][4], Eg[3], FX[3][4], qc[4] = {0.0, 0.0, 0.0, 0.0}, qce = 0.0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) W[0][k] = W[1][k] = W[2][k] = FX[0][k] = FX[1][k] = FX[2][k] = 0.0;
   Eg[0] = Eg[1] = Eg[2] = 0.0;
@@ -232,13 +300,7 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
     }
     if (edge_l || edge_r) Eg[1] = (double)__ldg(bl + x0 * nz);
   }
-  if constexpr (RHO) {
-    if (L.act) {
-      const double2 a = __ldg(reinterpret_cast<const double2*>(FL.fx + x0 * nz));
-      const double2 c = __ldg(reinterpret_cast<const double2*>(FL.fx + x0 * nz + 2));
-      FX[1][0] = a.x; FX[1][1] = a.y; FX[1][2] = c.x; FX[1][3] = c.y;
-    }
-  }
+  if constexpr (RHO) rho_prologue(QL, L.act, x0, nz, qc, qce, FX[1]);
 #pragma unroll
   for (int k = 0; k < NSL - 1; ++k) {
     if (x0 + k < x1) issue(x0 + k, k);
@@ -277,18 +339,13 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
       if (lane == 31) zr = Eg[ic];
       double lap[4];
       if constexpr (RHO) {
-        const double2 a = ring.fr.f.fx0[k][tid], c = ring.fr.f.fx1[k][tid];
-        FX[ip][0] = a.x; FX[ip][1] = a.y; FX[ip][2] = c.x; FX[ip][3] = c.y;
-        const double2 z0v = ring.fr.f.fz0[k][tid], z1v = ring.fr.f.fz1[k][tid];
-        const double fzv[4] = {z0v.x, z0v.y, z1v.x, z1v.y};
-        double fzl = __shfl_up_sync(0xffffffffu, fzv[3], 1);
-        if (lane == 0) fzl = ring.fr.f.fze[k][tid];
+        double fz[5];
+        rho_row(ring.fr.r, QL, tid, k, lane, x + 1 < nx, qc, qce, FX[ip], fz);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const double zm = c == 0 ? zl : W[ic][c - 1];
           const double zp = c == 3 ? zr : W[ic][c + 1];
-          lap[c] = lapf(W[ic][c], W[im][c], W[ip][c], zm, zp, FX[ic][c], FX[ip][c],
-                        c == 0 ? fzl : fzv[c - 1], fzv[c]);
+          lap[c] = lapf(W[ic][c], W[im][c], W[ip][c], zm, zp, FX[ic][c], FX[ip][c], fz[c], fz[c + 1]);
         }
       } else {
 #pragma unroll
@@ -380,13 +437,13 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const float* f2 = u2 + (size_t)lu * N2;
   float* fo = uo + (size_t)lu * N2;
   const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)b * N2;
-  FaceLane FL{};
-  if constexpr (RHO) FL = face_lane(m, g, b, L.act ? L.z4 : 0, z0);
+  QLane QL{};
+  if constexpr (RHO) QL = q_lane(m, g, b, L.act ? L.z4 : 0, z0, lane, L.z4);
   if (wzd)
-    fwd_lean_rows<MODE, RHO, true>(g, T, L, ring, FL, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t,
+    fwd_lean_rows<MODE, RHO, true>(g, T, L, ring, QL, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t,
                                    f1, f2, Ec, fo, rec_t, strip_t, has1, has2, wrx, wring);
   else
-    fwd_lean_rows<MODE, RHO, false>(g, T, L, ring, FL, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t,
+    fwd_lean_rows<MODE, RHO, false>(g, T, L, ring, QL, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t,
                                     f1, f2, Ec, fo, rec_t, strip_t, has1, has2, wrx, wring);
 }
 
@@ -402,13 +459,13 @@ struct LeanAdjRing {
   float4 l2[NSL][kLeanT];    // lam[t+2] row r
   float edl[NSL][kLeanT];    // lam[t+1] row r+1 at the lane's edge column
   double ede[NSL][kLeanT];   // E row r+1 at the lane's edge column
-  FaceRingOpt<NSL, RHO> fr;  // RHO: fxe row r+1, fz row r
+  QRingOpt<NSL, RHO> fr;     // RHO: q row r+1
 };
 
 template <bool RHO, bool ZD>
 __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T,
                                                  const LaneInfo& L, LeanAdjRing<kNSL, RHO>& ring,
-                                                 const FaceLane& FL, int tid, int lane, int z0,
+                                                 const QLane& QL, int tid, int lane, int z0,
                                                  int x0, int x1, int lu, const float* L1,
                                                  float* L2, const double* Ec,
                                                  const double* rres_t, bool has1, bool has2,
@@ -445,11 +502,11 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
     cp16(&ring.l2[sl][tid], b2 + orr, ok2);
     cp4(&ring.edl[sl][tid], bl + on, has1 && has_edge && okn);
     cp8(&ring.ede[sl][tid], bel + on, has_edge && okn);
-    if constexpr (RHO) issue_faces(ring.fr.f, FL, tid, sl, r + 1, true, r, true, L.act, lane == 0, nz);
+    if constexpr (RHO) issue_q(ring.fr.r, QL, tid, sl, r + 1, okn, L.act, nz);
   };
   // windows of E*lam1 (EL) and raw lam1 (RL), slot (k)%3 = row x-1, (k+1)%3 = x,
-  // (k+2)%3 = x+1; FX[s] = x face below the row of slot s
-  double EL[3][4], RL[3][4], EG[3], FX[3][4];
+  // (k+2)%3 = x+1; FX[s] = x face above the row of slot s; qc / qce: q of row x
+  double EL[3][4], RL[3][4], EG[3], FX[3][4], qc[4] = {0.0, 0.0, 0.0, 0.0}, qce = 0.0;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     EL[0][k] = EL[1][k] = EL[2][k] = RL[0][k] = RL[1][k] = RL[2][k] = FX[0][k] = FX[1][k] =
@@ -472,13 +529,7 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
     if (x0 >= 1) ld(x0 - 1, 0);
     ld(x0, 1);
   }
-  if constexpr (RHO) {
-    if (L.act) {
-      const double2 a = __ldg(reinterpret_cast<const double2*>(FL.fx + x0 * nz));
-      const double2 c = __ldg(reinterpret_cast<const double2*>(FL.fx + x0 * nz + 2));
-      FX[1][0] = a.x; FX[1][1] = a.y; FX[1][2] = c.x; FX[1][3] = c.y;
-    }
-  }
+  if constexpr (RHO) rho_prologue(QL, L.act, x0, nz, qc, qce, FX[1]);
 #pragma unroll
   for (int k = 0; k < NSL - 1; ++k) {
     if (x0 + k < x1) issue(x0 + k, k);
@@ -511,18 +562,14 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
       if (lane == 31) zr = EG[ic];
       double adj[4];
       if constexpr (RHO) {
-        const double2 a = ring.fr.f.fx0[k][tid], c = ring.fr.f.fx1[k][tid];
-        FX[ip][0] = a.x; FX[ip][1] = a.y; FX[ip][2] = c.x; FX[ip][3] = c.y;
-        const double2 z0v = ring.fr.f.fz0[k][tid], z1v = ring.fr.f.fz1[k][tid];
-        const double fzv[4] = {z0v.x, z0v.y, z1v.x, z1v.y};
-        double fzl = __shfl_up_sync(0xffffffffu, fzv[3], 1);
-        if (lane == 0) fzl = ring.fr.f.fze[k][tid];
+        double fz[5];
+        rho_row(ring.fr.r, QL, tid, k, lane, x + 1 < nx, qc, qce, FX[ip], fz);
 #pragma unroll
         for (int c2 = 0; c2 < 4; ++c2) {
           const double zm = c2 == 0 ? zl : EL[ic][c2 - 1];
           const double zp = c2 == 3 ? zr : EL[ic][c2 + 1];
-          adj[c2] = lapf(EL[ic][c2], EL[im][c2], EL[ip][c2], zm, zp, FX[ic][c2], FX[ip][c2],
-                         c2 == 0 ? fzl : fzv[c2 - 1], fzv[c2]);
+          adj[c2] = lapf(EL[ic][c2], EL[im][c2], EL[ip][c2], zm, zp, FX[ic][c2], FX[ip][c2], fz[c2],
+                         fz[c2 + 1]);
         }
       } else {
 #pragma unroll
@@ -587,13 +634,13 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const float* L1 = l1 + (size_t)lu * N2;
   float* L2 = l2o + (size_t)lu * N2;
   const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)b * N2;
-  FaceLane FL{};
-  if constexpr (RHO) FL = face_lane(m, g, b, L.act ? L.z4 : 0, z0);
+  QLane QL{};
+  if constexpr (RHO) QL = q_lane(m, g, b, L.act ? L.z4 : 0, z0, lane, L.z4);
   if (wzd)
-    adjlam_lean_rows<RHO, true>(g, T, L, ring, FL, tid, lane, z0, x0, x1, lu, L1, L2, Ec, rres_t,
+    adjlam_lean_rows<RHO, true>(g, T, L, ring, QL, tid, lane, z0, x0, x1, lu, L1, L2, Ec, rres_t,
                                 has1, has2, wrx);
   else
-    adjlam_lean_rows<RHO, false>(g, T, L, ring, FL, tid, lane, z0, x0, x1, lu, L1, L2, Ec, rres_t,
+    adjlam_lean_rows<RHO, false>(g, T, L, ring, QL, tid, lane, z0, x0, x1, lu, L1, L2, Ec, rres_t,
                                  has1, has2, wrx);
 }
 
@@ -630,7 +677,7 @@ struct LeanImgRing {
   double2 e0[kNSL][kLeanT];   // E (RHO: Er) row x0+i-2, cells 0-1 (MODE 2)
   double2 e1[kNSL][kLeanT];   // cells 2-3
   float edge[kNSL][kLeanT];   // u[t-1] row x0-1+i at the lane's edge column
-  FaceRingOpt<kNSL, RHO> fr;  // RHO: fxe row x0-1+i, fz row x0+i-2
+  QRingOpt<kNSL, RHO> fr;     // RHO: q row x0-1+i
 };
 
 template <int MODE, bool RHO>
@@ -673,8 +720,8 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const double pulse_t = __ldg(g.pulse + t);
   const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)sg.b * N2;
   const double* be = opaque(Ec + zc);
-  FaceLane FL{};
-  if constexpr (RHO) FL = face_lane(m, g, sg.b, zc, z0);
+  QLane QL{};
+  if constexpr (RHO) QL = q_lane(m, g, sg.b, zc, z0, lane, z4);
   const float* U1 = MODE == 1 ? F : utm1;
   auto issue = [&](int k, int i, int sl) {  // item i of the group's k-th shot
     if (k >= sg.n) return;
@@ -686,9 +733,9 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
     cp4(&ring.edge[sl][tid], U1 + fo + ze + ou, oku && has_edge);
     const int rx = x0 + i - 2;
     const bool okx = i >= 2 && rx < x1;
-    if constexpr (RHO) {  // fxe has nx + 1 rows (outer faces included)
-      const bool okf = ru >= 0 && ru <= nx;
-      issue_faces(ring.fr.f, FL, tid, sl, okf ? ru : 0, okf, okx ? rx : 0, okx, act, lane == 0, nz);
+    if constexpr (RHO) {
+      const bool okq = ru >= 0 && ru < nx;
+      issue_q(ring.fr.r, QL, tid, sl, okq ? ru : 0, okq, act, nz);
     }
     if (i >= 2) {
       const int ox = okx ? rx * nz : 0;
@@ -711,7 +758,8 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
     issue(0, i, i);
     cp_commit();
   }
-  double W[3][4], Eg[3], FX[3][4];
+  // FX[s]: x face above the u[t-1] row of slot s; qp / qpe: q of the previous item's row
+  double W[3][4], Eg[3], FX[3][4], qp[4] = {0.0, 0.0, 0.0, 0.0}, qpe = 0.0;
   for (int k = 0; k < sg.n; ++k) {
     const int lu = sg.lu0 + k;
     const int s = (unit_begin + lu) % g.S;
@@ -731,10 +779,28 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
         const float4 f = ring.u1[sl][tid];
         W[wi][0] = f.x; W[wi][1] = f.y; W[wi][2] = f.z; W[wi][3] = f.w;
         Eg[wi] = (double)ring.edge[sl][tid];
-        if constexpr (RHO) {
-          const double2 a = ring.fr.f.fx0[sl][tid], c = ring.fr.f.fx1[sl][tid];
-          FX[wi][0] = a.x; FX[wi][1] = a.y; FX[wi][2] = c.x; FX[wi][3] = c.y;
+      }
+      double fz[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // z faces of row x0+i-2
+      if constexpr (RHO) {
+        const int ru = x0 - 1 + i;
+        double qn[4], qen;
+        read_q(ring.fr.r, tid, sl, qn, qen);
+        if (ru == 0) {  // outer face above row 0
+#pragma unroll
+          for (int c = 0; c < 4; ++c) qp[c] = qn[c];
+          qpe = qen;
         }
+        if (ru >= nx) {  // outer face below row nx-1
+#pragma unroll
+          for (int c = 0; c < 4; ++c) qn[c] = qp[c];
+          qen = qpe;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) FX[wi][c] = face(qp[c], qn[c]);
+        if (i >= 2) zfaces(QL, lane, qp, qpe, fz);  // warp-uniform
+#pragma unroll
+        for (int c = 0; c < 4; ++c) qp[c] = qn[c];
+        qpe = qen;
       }
       if (i < 2) continue;
       const int r = i - 2;
@@ -744,13 +810,6 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
       double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1);
       if (lane == 0) zl = Eg[ic];
       if (lane == 31) zr = Eg[ic];
-      double fzv[4] = {0.0, 0.0, 0.0, 0.0}, fzl = 0.0;
-      if constexpr (RHO) {
-        const double2 z0v = ring.fr.f.fz0[sl][tid], z1v = ring.fr.f.fz1[sl][tid];
-        fzv[0] = z0v.x; fzv[1] = z0v.y; fzv[2] = z1v.x; fzv[3] = z1v.y;
-        fzl = __shfl_up_sync(0xffffffffu, fzv[3], 1);
-        if (lane == 0) fzl = ring.fr.f.fze[sl][tid];
-      }
       if (x >= x1) continue;  // warp-uniform (last row block)
       const float4 lf = ring.lam[sl][tid];
       const double lam[4] = {lf.x, lf.y, lf.z, lf.w};
@@ -760,8 +819,8 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
         const double zm = c == 0 ? zl : W[ic][c - 1];
         const double zp = c == 3 ? zr : W[ic][c + 1];
         if constexpr (RHO)
-          lapu[c] = lapf(W[ic][c], W[im][c], W[ip][c], zm, zp, FX[ic][c], FX[ip][c],
-                         c == 0 ? fzl : fzv[c - 1], fzv[c]);
+          lapu[c] = lapf(W[ic][c], W[im][c], W[ip][c], zm, zp, FX[ic][c], FX[ip][c], fz[c],
+                         fz[c + 1]);
         else
           lapu[c] = lap5(W[ic][c], W[im][c], W[ip][c], zm, zp);
         if (boxk & (1u << c)) acc[r][c] = __fma_rn(lapu[c], lam[c], acc[r][c]);
