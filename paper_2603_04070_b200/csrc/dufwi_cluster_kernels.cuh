@@ -68,7 +68,10 @@ struct ClusterCfg {
 // through shared-memory stages of kStage steps: written (forward) or read
 // (adjoint) with one coalesced pass per kStage steps instead of scattered
 // global accesses inside every step.
-constexpr int kStage = 16;
+#ifndef DUFWI_KSTAGE
+#define DUFWI_KSTAGE 32
+#endif
+constexpr int kStage = DUFWI_KSTAGE;
 
 // Threads per CTA the sweep kernels are compiled for: the register budget per
 // thread (65536 / threads) must hold RPT rows of f64 state (6 per row in the
@@ -843,7 +846,8 @@ __device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, 
       const int t = g.nt - 1 - (i0 + k);
       io.sring[k * io.maxring + r] = t >= 2 ? strips[((size_t)(t - 2) * U + lu) * g.SL + io.ring_g[r]] : 0.f;
     }
-    if (threadIdx.x < nk) io.spulse[threadIdx.x] = g.pulse[g.nt - 1 - (i0 + threadIdx.x)];
+    // (a strided loop: a small grid's CTA can have fewer threads than kStage)
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) io.spulse[k] = g.pulse[g.nt - 1 - (i0 + k)];
   }
 }
 

@@ -19,6 +19,7 @@ ap.add_argument("--engine", default="stepwise")
 ap.add_argument("--store", default="auto")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--nt", type=int, default=0, help="override nt (shorter runs)")
+ap.add_argument("--no-rho", action="store_true", help="drop the density map (constant-density kernels)")
 args = ap.parse_args()
 torch.cuda.set_device(0)
 from paper_2603_04070_b200 import configs
@@ -30,6 +31,9 @@ if args.nt:
 S = spec.n_tx
 B = max(1, -(-args.units // S))
 wl = configs.make_workload(spec, seed=0, n_phantoms=B)
+if args.no_rho:
+    import dataclasses as _dc
+    wl = _dc.replace(wl, rho=None)
 grid = pk.Grid2D(spec.n, spec.n, spec.dx, spec.dt, spec.nt)
 geom = pk.AcquisitionGeometry(grid, wl.nodes, wl.rx, 0.0, tx_elements=wl.tx)
 damp = pk.build_pml(grid, spec.pml)
