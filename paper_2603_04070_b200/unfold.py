@@ -164,6 +164,52 @@ class Reconstructor:
 
 
 _RECON_CACHE: dict = {}
+_PINNED: dict = {}
+
+
+def _pinned(shape, device) -> "torch.Tensor":
+    """Page-locked f64 host buffer of ``shape``, reused across calls (staging of
+    the public API's host arrays: one memcpy in, one DMA to the device)."""
+    import torch
+
+    key = (tuple(shape), str(device))
+    buf = _PINNED.get(key)
+    if buf is None:
+        if len(_PINNED) >= 8:
+            _PINNED.pop(next(iter(_PINNED)))
+        buf = _PINNED[key] = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+    return buf
+
+
+def _upload(arrays, device) -> "torch.Tensor":
+    """Host f64 arrays (stacked along axis 0) -> one device tensor through a
+    pinned staging buffer.  Read-only ChannelData arrays are copied, never aliased."""
+    import torch
+
+    arrays = [np.asarray(a) for a in arrays]
+    n = sum(a.shape[0] for a in arrays)
+    stage = _pinned((n,) + arrays[0].shape[1:], device)
+    host = stage.numpy()
+    o = 0
+    for a in arrays:
+        host[o:o + a.shape[0]] = a
+        o += a.shape[0]
+    out = torch.empty(stage.shape, dtype=torch.float64, device=device)
+    out.copy_(stage, non_blocking=True)
+    # the staging buffer is reused by the next call: order its reuse after this copy
+    torch.cuda.current_stream(device).synchronize()
+    return out
+
+
+def _download(maps) -> np.ndarray:
+    """Stage maps (K tensors (B, nx, nz) on device) -> host (K, B, nx, nz) f64."""
+    import torch
+
+    dev = torch.stack(maps)
+    stage = _pinned(tuple(dev.shape), dev.device)
+    stage.copy_(dev, non_blocking=True)
+    torch.cuda.current_stream(dev.device).synchronize()
+    return stage.numpy().copy()
 
 
 def _reconstructor(eng, nets, bounds, rho) -> Reconstructor:
@@ -200,13 +246,13 @@ def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) ->
                      setup.pulse.samples, damping, has_rho=rho is not None)
     rec = _reconstructor(eng, nets, setup.bounds, rho)
     # ChannelData arrays are read-only views: a writable host copy for torch
-    obs = torch.from_numpy(np.require(m_obs.traces, np.float64, ["C", "W"])).to(eng.device)
-    c = torch.from_numpy(np.array(c0.values, dtype=np.float64)).to(eng.device)[None]
+    obs = _upload([m_obs.traces], eng.device)
+    c = _upload([np.asarray(c0.values, dtype=np.float64)[None]], eng.device)
     try:
         maps = rec.reconstruct(obs, c)
     except FloatingPointError as exc:
         raise NumericError(str(exc)) from exc
-    host = torch.stack(maps).cpu().numpy()
+    host = _download(maps)
     return [SosMap(grid, host[k, 0]) for k in range(host.shape[0])]
 
 
@@ -242,12 +288,11 @@ def unfold_infer_batch(m_obs_list, c0_list, nets, setup: InversionSetup) -> list
     eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
                      setup.pulse.samples, damping, n_phantoms=B, has_rho=rho is not None)
     rec = _reconstructor(eng, nets, setup.bounds, rho)
-    obs = torch.from_numpy(np.concatenate([np.require(m.traces, np.float64, ["C", "W"])
-                                           for m in m_obs_list])).to(eng.device)
-    c = torch.from_numpy(np.stack([np.asarray(c0.values, np.float64) for c0 in c0_list])).to(eng.device)
+    obs = _upload([m.traces for m in m_obs_list], eng.device)
+    c = _upload([np.asarray(c0.values, np.float64)[None] for c0 in c0_list], eng.device)
     try:
         maps = rec.reconstruct(obs, c)
     except FloatingPointError as exc:
         raise NumericError(str(exc)) from exc
-    host = torch.stack(maps).cpu().numpy()  # (K, B, nx, nz)
+    host = _download(maps)  # (K, B, nx, nz)
     return [[SosMap(grid, host[k, b]) for k in range(host.shape[0])] for b in range(B)]
