@@ -616,7 +616,7 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     p->last_engine = DUFWI_ENGINE_CLUSTER;
     // per-unit accumulators: with one shot per group, group index == chunk-local unit
     const int acc_off = 0;
-    rc = cluster_adjoint(g, m, pick_cluster(p->ccands, U), mode, unit_begin, U, rres,
+    rc = cluster_adjoint(g, m, pick_cluster(p->ccands, U, true), mode, unit_begin, U, rres,
                          mode == DUFWI_STORE_FULL ? hist : nullptr,
                          mode == DUFWI_STORE_STRIPS ? strips : nullptr, ubuf, acc_part, acc_off,
                          st);

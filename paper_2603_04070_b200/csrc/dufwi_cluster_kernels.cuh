@@ -76,8 +76,9 @@ constexpr int kStage = DUFWI_KSTAGE;
 // Threads per CTA the sweep kernels are compiled for: the register budget per
 // thread (65536 / threads) must hold RPT rows of f64 state (6 per row in the
 // adjoint) without spilling.
+// (<= 5 rows: up to 20 warps, e.g. config 1's 4 x 4 adjoint shape at 96 registers)
 __host__ __device__ constexpr int cluster_max_threads(int rpt) {
-  return rpt >= 7 ? 384 : 512;
+  return rpt >= 7 ? 384 : rpt >= 6 ? 512 : 640;
 }
 // registers per thread for that budget (one CTA per SM, multiples of 8; a warp's
 // registers come from one SM sub-partition, 16384 each, so 15 warps cap at 128)
@@ -1160,13 +1161,28 @@ inline double cluster_cost(const ClusterCfg& c) {
 // Launch shape for U units: the fewest waves of co-resident clusters (a unit's
 // time loop cannot be split, so a second wave doubles the sweep), then the
 // cheapest step.
-inline const ClusterCfg& pick_cluster(const std::vector<ClusterCfg>& c, int U) {
+//
+// The adjoint step is issue / FP64-pipe bound on each SM sub-partition: a CTA of
+// W warps puts ceil(W/4) of them on its busiest SMSP, so its cost is scaled by
+// ceil(W/4) / (W/4) (config 1: 10 warps = 3+3+2+2 -> x1.2; 20 warps -> x1).
+// Measured (fwd / adj ms): 2 x 8 rows, 10 warps 0.839 / 1.327; 4 x 4, 20 warps
+// 0.848 / 1.289.  The forward keeps the <= 512-thread shapes and the plain cost.
+inline const ClusterCfg& pick_cluster(const std::vector<ClusterCfg>& c, int U,
+                                      bool adjoint = false) {
   size_t best = 0;
   long best_w = -1;
   double best_c = 0.0;
+  bool any = false;
+  for (size_t i = 0; i < c.size(); ++i)
+    if (adjoint || c[i].threads <= 512) any = true;
   for (size_t i = 0; i < c.size(); ++i) {
+    if (any && !adjoint && c[i].threads > 512) continue;
     const long w = (U + c[i].maxc - 1) / c[i].maxc;
-    const double k = cluster_cost(c[i]);
+    double k = cluster_cost(c[i]);
+    if (adjoint) {
+      const int W = (c[i].threads + 31) / 32;
+      k *= (double)((W + 3) / 4) / (W / 4.0);
+    }
     if (best_w < 0 || w < best_w || (w == best_w && k < best_c)) {
       best = i;
       best_w = w;

@@ -1,7 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for L in paper_2603_04070_b200/libdufwi.so tools/ubench/lib_RB2.so tools/ubench/lib_RB4.so; do
-  for c in 2 3; do
-    echo "$L $c $(DUFWI_LIB=$PWD/$L timeout 200 python tools/time_config.py --config $c --units 128 --nt 200 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.3g %.3g' % (d['fwd_updates_per_s'], d['adj_updates_per_s']))")"
-  done
+L=tools/ubench/lib_T640.so
+for cfg in "10 4" "8 5" "10 5" "16 5" "12 4"; do
+  set -- $cfg
+  echo "cs=$1 rpt=$2 $(DUFWI_CLUSTER_CS=$1 DUFWI_CLUSTER_RPT=$2 DUFWI_LIB=$PWD/$L timeout 120 python tools/sweep_ms.py 2>&1 | tail -1 | cut -c1-250)"
 done
