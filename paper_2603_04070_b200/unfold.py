@@ -61,10 +61,11 @@ class Reconstructor:
     (B, nx, nz) on device, plus the per-stage gradients when asked.
 
     In a single process the K stages (sweeps, residual, epilogue, networks,
-    clamps: ~30 launches per stage) are captured once into a CUDA graph and
-    replayed per call; the inputs are copied into the graph's static buffers
-    first.  Under torch.distributed, with host networks or when gradients are
-    kept, the stages are launched eagerly.
+    clamps: ~30 launches per stage) are captured into a CUDA graph on the
+    second call with the same shapes and replayed from then on; the inputs are
+    copied into the graph's static buffers first.  The first call, calls under
+    torch.distributed, with host networks or when gradients are kept launch the
+    stages eagerly.
     """
 
     def __init__(self, engine, nets, bounds, guard_radius: int = 2, rho=None, graph: bool | None = None):
@@ -76,6 +77,7 @@ class Reconstructor:
         # DUFWI_GRAPH=0 launches the stages eagerly (A/B timing, debugging)
         self.graph = (os.environ.get("DUFWI_GRAPH", "1") != "0") if graph is None else graph
         self._g = None  # (key, graph, static obs, static c0, maps, flags, launches, ws generation)
+        self._seen = None  # key of the last eager call (capture on the next one)
         self.replayed_launches = 0
 
     def _stages(self, obs, c0, keep_gradients: bool, check_finite: bool):
@@ -152,10 +154,13 @@ class Reconstructor:
     def reconstruct(self, obs, c0, keep_gradients: bool = False, check_finite: bool = True):
         from .engine import raise_nonfinite
 
-        if self._graphable(obs, keep_gradients):
+        graphable = self._graphable(obs, keep_gradients)
+        key = self._graph_key(obs, c0) if graphable else None
+        if graphable and (self._g is not None and self._g[0] == key or self._seen == key):
             maps, flags = self._replay(obs, c0)
             grads = []
         else:
+            self._seen = key
             maps, grads, flags = self._stages(obs, c0, keep_gradients, check_finite)
         if check_finite:
             for f in flags.cpu():  # first failing stage raises

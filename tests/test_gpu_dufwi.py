@@ -128,6 +128,9 @@ def test_graphed_reconstruct_equals_eager(gpu):
     c0 = torch.full((1,) + grid.shape, 1540.0, dtype=torch.float64, device=gpu)
     eager = Reconstructor(eng, nets, bounds, graph=False).reconstruct(obs, c0)
     rec = Reconstructor(eng, nets, bounds, graph=True)
+    first = rec.reconstruct(obs, c0)  # eager; the graph is captured on the next call
+    assert rec._g is None
+    assert all(torch.equal(a, b) for a, b in zip(eager, first))
     graphed = rec.reconstruct(obs, c0)
     assert rec._g is not None
     for a, b in zip(eager, graphed):
