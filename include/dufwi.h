@@ -132,9 +132,10 @@ int64_t dufwi_plan_launch_count(const dufwi_plan_t* plan);
 /* Engine actually used for the last forward/adjoint call (DUFWI_ENGINE_*). */
 int32_t dufwi_plan_last_engine(const dufwi_plan_t* plan);
 
-/* Engine diagnostics: out[0..8] = cluster_ok, cluster CTAs, rows per CTA,
+/* Engine diagnostics: out[0..11] = cluster_ok, cluster CTAs, rows per CTA,
  * rows per thread, threads per CTA, f64 exchange, smem forward, smem adjoint,
- * co-resident clusters — for the launch shape of all units at once.
+ * co-resident clusters (the forward's shape), then the adjoint's cluster CTAs,
+ * rows per thread and threads per CTA — for all units at once.
  * Returns the number of values written (<= n). */
 int32_t dufwi_plan_info(const dufwi_plan_t* plan, int64_t* out, int32_t n);
 

@@ -63,7 +63,8 @@ struct dufwi_plan {
   ABTables ab{};  // (A, B) tables of the damped update for the stepwise kernels
   // cluster engine
   std::vector<ClusterCfg> ccands;  // launch shapes that fit, one per cluster size
-  ClusterCfg ccfg{};                // the shape for all units at once (plan_info)
+  ClusterCfg ccfg{};                // the forward's shape for all units at once (plan_info)
+  ClusterCfg ccfg_adj{};            // the adjoint's
   bool cluster_ok = false;
   int lean_tx = 0;      // rows per warp override (DUFWI_LEAN_TX, experiments)
   bool lean_on = true;  // lean stepwise kernels (DUFWI_LEAN=0: the first vec/stream kernels)
@@ -394,7 +395,10 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
     big((const void*)img_lean_kernel<2, true>, sizeof(LeanImgRing<true>));
   }
   p->cluster_ok = cluster_candidates(g, p->has_rho != 0, rx_nodes, p->ccands);
-  if (p->cluster_ok) p->ccfg = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots);
+  if (p->cluster_ok) {
+    p->ccfg = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots);
+    p->ccfg_adj = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots, true);
+  }
   *plan_out = p;
   return DUFWI_OK;
 }
@@ -732,10 +736,11 @@ extern "C" int64_t dufwi_plan_launch_count(const dufwi_plan_t* p) { return p ? p
 extern "C" int32_t dufwi_plan_last_engine(const dufwi_plan_t* p) { return p ? p->last_engine : -1; }
 extern "C" int32_t dufwi_plan_info(const dufwi_plan_t* p, int64_t* out, int32_t n) {
   if (!p || !out) return 0;
-  const int64_t v[9] = {p->cluster_ok ? 1 : 0, p->ccfg.cs, p->ccfg.rows, p->ccfg.rpt,
-                        p->ccfg.threads, p->ccfg.dbl, (int64_t)p->ccfg.smem_fwd,
-                        (int64_t)p->ccfg.smem_adj, p->ccfg.maxc};
-  const int k = n < 9 ? n : 9;
+  const int64_t v[12] = {p->cluster_ok ? 1 : 0, p->ccfg.cs, p->ccfg.rows, p->ccfg.rpt,
+                         p->ccfg.threads, p->ccfg.dbl, (int64_t)p->ccfg.smem_fwd,
+                         (int64_t)p->ccfg_adj.smem_adj, p->ccfg.maxc, p->ccfg_adj.cs,
+                         p->ccfg_adj.rpt, p->ccfg_adj.threads};
+  const int k = n < 12 ? n : 12;
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }

@@ -190,11 +190,12 @@ class PhysicsEngine:
 
     def info(self) -> dict:
         """Engine configuration chosen by the plan (cluster shape, shared memory)."""
-        buf = (ctypes.c_int64 * 9)()
-        n = self._so.dufwi_plan_info(self._plan, buf, 9)
+        buf = (ctypes.c_int64 * 12)()
+        n = self._so.dufwi_plan_info(self._plan, buf, 12)
         keys = ("cluster_ok", "cluster_ctas", "rows_per_cta", "rows_per_thread",
                 "threads_per_cta", "f64_exchange", "smem_forward", "smem_adjoint",
-                "clusters_resident")
+                "clusters_resident", "adjoint_cluster_ctas", "adjoint_rows_per_thread",
+                "adjoint_threads_per_cta")
         return {k: int(buf[i]) for i, k in enumerate(keys[:n])}
 
     def _stream(self) -> int:
