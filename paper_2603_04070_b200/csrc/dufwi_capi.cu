@@ -509,7 +509,8 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     if (p->lean_tx > 0) vtx = p->lean_tx;
     const dim3 vgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
     const bool lean = use_lean(p);
-    const dim3 lgrid((g.nz + 127) / 128, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx), U);
+    const dim3 lgrid((g.nz + kSW - 1) / kSW, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx),
+                     (U + kSPW - 1) / kSPW);
     dim3 block(kWarpsX * 32);
     dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXF - 1) / (kWarpsX * kRXF), G.ngroups);
     for (int t = 0; t < g.nt; ++t) {
@@ -535,7 +536,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
                                                       vtx, u1, u2, uo, rec_t, st_t, has1, has2)
 #define DUFWI_LEAN(M, R)                                                                        \
   fwd_lean_kernel<M, R><<<lgrid, kLeanT, sizeof(LeanFwdRing<kFwdNSL, R>), st>>>(                     \
-      g, m, p->ab, t, unit_begin, vtx, u1, u2, uo, rec_t, st_t, has1, has2)
+      g, m, p->ab, t, unit_begin, U, vtx, u1, u2, uo, rec_t, st_t, has1, has2)
       if (lean) {
         if (p->has_rho) {
           if (mode == 0) DUFWI_LEAN(0, true); else if (mode == 1) DUFWI_LEAN(1, true); else DUFWI_LEAN(2, true);
@@ -650,17 +651,19 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     if (p->lean_tx > 0) vtx = p->lean_tx;
     if (use_lean(p)) {
       // split adjoint: lam update (12 B/update) then imaging + reconstruction
-      const dim3 lgrid((g.nz + 127) / 128, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx), U);
+      const dim3 lgrid((g.nz + kSW - 1) / kSW, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx),
+                       (U + kSPW - 1) / kSPW);
       if (p->has_rho)
         adjlam_lean_kernel<true><<<lgrid, kLeanT, sizeof(LeanAdjRing<kNSL, true>), st>>>(
-            g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
+            g, m, p->ab, t, unit_begin, U, vtx, l1, l2o, rres_t, has1, has2);
       else
         adjlam_lean_kernel<false><<<lgrid, kLeanT, sizeof(LeanAdjRing<kNSL, false>), st>>>(
-            g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
+            g, m, p->ab, t, unit_begin, U, vtx, l1, l2o, rres_t, has1, has2);
       LAUNCH_CHECK(p);
       if (do_img) {
         const int rows = mode == DUFWI_STORE_STRIPS ? g.Lx : g.nx;
-        const dim3 igrid((g.nz + 127) / 128, (rows + kLeanWarps * kImgTX - 1) / (kLeanWarps * kImgTX),
+        const dim3 igrid((g.nz + kSW - 1) / kSW,
+                         (rows + kLeanWarps * kImgTX * kSPW - 1) / (kLeanWarps * kImgTX * kSPW),
                          G.ngroups);
         const float* st_tm2 = (mode == DUFWI_STORE_STRIPS && do_recon) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
 #define DUFWI_IMG(M, R)                                                                         \

@@ -54,6 +54,19 @@ constexpr int kLeanWarps = DUFWI_LEAN_WARPS;  // warps per CTA
 constexpr int kLeanMinB = DUFWI_LEAN_MINB;        // min resident CTAs per SM (register cap)
 constexpr int kLeanMinBRho = DUFWI_LEAN_MINB_RHO;  // density kernels: more live f64 state
 constexpr int kLeanT = kLeanWarps * 32;
+// Lane groups: a warp is kSPW groups of kLS lanes, each group on a kSW-wide z
+// strip (4 cells per lane).  kSW = 64: two groups per warp, so a grid whose
+// last strip is partial idles at most 15 lanes per group (560 columns: 97% of
+// the lanes busy instead of 87.5% with 128-wide strips; 296: 92.5% vs 77%;
+// 1088: 100% vs 94%).  The forward and lam update put two units in a warp,
+// the imaging kernel two row blocks of the same shot group.
+#ifndef DUFWI_LEAN_SW
+#define DUFWI_LEAN_SW 64
+#endif
+constexpr int kSW = DUFWI_LEAN_SW;
+constexpr int kLS = kSW / 4;    // lanes per group (the shuffle width)
+constexpr int kSPW = 32 / kLS;  // groups per warp
+static_assert(kSW == 64 || kSW == 128, "lane-group strip width");
 constexpr int kNSL = 3;                       // ring slots (measured best: 3 > 6)
 #ifndef DUFWI_FWD_NSL
 #define DUFWI_FWD_NSL 3
@@ -63,17 +76,19 @@ constexpr int kFwdNSL = DUFWI_FWD_NSL;         // forward ring slots (>3: runtim
 // Per-lane constants of a 4-cell z segment.
 struct LaneInfo {
   int z4;
-  bool act;
+  bool on;           // the lane group has work (a unit / row block)
+  bool act;          // on, and the lane's cells lie in the grid
   unsigned rxk;      // cells on a receiver column
   unsigned boxk;     // cells with z in [z_lo, z_hi]
   int ringl, ringr;  // cell index on ring column z_lo-1 / z_hi+1, or -1
   bool zd;           // any cell in the z damping band
 };
 
-__device__ __forceinline__ LaneInfo lane_info(const Geo& g, const ABTables& T, int z4) {
+__device__ __forceinline__ LaneInfo lane_info(const Geo& g, const ABTables& T, int z4, bool on) {
   LaneInfo L;
   L.z4 = z4;
-  L.act = z4 < g.nz;
+  L.on = on;
+  L.act = on && z4 < g.nz;
   L.rxk = L.boxk = 0u;
   L.ringl = L.ringr = -1;
   L.zd = false;
@@ -134,18 +149,18 @@ struct QRingOpt<NSL, true> {
 // Per-lane view of one phantom's q map.
 struct QLane {
   const double* q;   // q + zc (row r at r * nz)
-  const double* qe;  // q + edge column (lane 0: z0-1, lane 31: z0+128)
+  const double* qe;  // q + edge column (first lane of a group: z0-1, last: z0+kSW)
   bool edge;         // the lane has an edge column inside the grid
   bool lo, hi;       // the lane's first / last cell is z = 0 / z = nz-1 (outer faces)
 };
 
 __device__ __forceinline__ QLane q_lane(const Model& m, const Geo& g, int b, int zc, int z0,
-                                        int lane, int z4) {
+                                        int l, int z4, bool on) {
   QLane Q;
   const double* qb = m.q + (size_t)b * g.nx * g.nz;
-  const bool el = lane == 0 && z0 > 0, er = lane == 31 && z0 + 128 < g.nz;
+  const bool el = on && l == 0 && z0 > 0, er = on && l == kLS - 1 && z0 + kSW < g.nz;
   Q.q = opaque(qb + zc);
-  Q.qe = opaque(qb + (el ? z0 - 1 : er ? z0 + 128 : 0));
+  Q.qe = opaque(qb + (el ? z0 - 1 : er ? z0 + kSW : 0));
   Q.edge = el || er;
   Q.lo = z4 == 0;
   Q.hi = z4 + 4 >= g.nz;
@@ -174,12 +189,12 @@ __device__ __forceinline__ double face(double a, double b) {
 
 // z faces of a lane's 4 cells in one row: fz[k] lies between cells k-1 and k
 // (fz[0] / fz[4]: the neighbours in lanes -1 / +1, the edge column, or outer).
-__device__ __forceinline__ void zfaces(const QLane& Q, int lane, const double (&q)[4], double qe,
+__device__ __forceinline__ void zfaces(const QLane& Q, int l, const double (&q)[4], double qe,
                                        double (&fz)[5]) {
-  double ql = __shfl_up_sync(0xffffffffu, q[3], 1);
-  double qr = __shfl_down_sync(0xffffffffu, q[0], 1);
-  if (lane == 0) ql = qe;
-  if (lane == 31) qr = qe;
+  double ql = __shfl_up_sync(0xffffffffu, q[3], 1, kLS);
+  double qr = __shfl_down_sync(0xffffffffu, q[0], 1, kLS);
+  if (l == 0) ql = qe;
+  if (l == kLS - 1) qr = qe;
   if (Q.lo) ql = q[0];
   if (Q.hi) qr = q[3];
   fz[0] = face(ql, q[0]);
@@ -213,7 +228,7 @@ __device__ __forceinline__ void rho_prologue(const QLane& Q, bool act, int x0, i
 // from the carried q of row x, which then advances to row x+1.
 template <int NSL>
 __device__ __forceinline__ void rho_row(const QRing<NSL>& R, const QLane& Q, int tid, int sl,
-                                        int lane, bool has_next, double (&qc)[4], double& qce,
+                                        int l, bool has_next, double (&qc)[4], double& qce,
                                         double (&fxp)[4], double (&fz)[5]) {
   double qn[4], qen;
   read_q(R, tid, sl, qn, qen);
@@ -224,7 +239,7 @@ __device__ __forceinline__ void rho_row(const QRing<NSL>& R, const QLane& Q, int
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) fxp[k] = face(qc[k], qn[k]);
-  zfaces(Q, lane, qc, qce, fz);
+  zfaces(Q, l, qc, qce, fz);
 #pragma unroll
   for (int k = 0; k < 4; ++k) qc[k] = qn[k];
   qce = qen;
@@ -237,7 +252,7 @@ struct LeanFwdRing {
   float4 u2[NSL][kLeanT];   // u[t-2] row r
   double2 e0[NSL][kLeanT];  // E (RHO: Er) row r, cells 0-1
   double2 e1[NSL][kLeanT];  // cells 2-3
-  float edge[NSL][kLeanT];  // u[t-1] row r+1 at z0-1 (lane 0) / z0+128 (lane 31)
+  float edge[NSL][kLeanT];  // u[t-1] row r+1 at the group's edge column (z0-1 / z0+kSW)
   QRingOpt<NSL, RHO> fr;    // RHO: q row r+1
 };
 
@@ -252,8 +267,9 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
   constexpr int NSL = kFwdNSL;
   const int nz = g.nz, nx = g.nx;
   const int zc = L.act ? L.z4 : 0;
-  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < g.nz;
-  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + 128 : 0;
+  const bool edge_l = L.on && lane == 0 && z0 > 0;
+  const bool edge_r = L.on && lane == kLS - 1 && z0 + kSW < g.nz;
+  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + kSW : 0;
   const bool has_edge = has1 && (edge_l || edge_r);
   const bool ok1 = has1 && L.act, ok2 = has2 && L.act;
   const float* b1 = opaque(f1 + zc);
@@ -333,10 +349,10 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
       const double2 e0 = ring.e0[k][tid], e1 = ring.e1[k][tid];
       const double u2v[4] = {w2.x, w2.y, w2.z, w2.w};
       const double ed[4] = {e0.x, e0.y, e1.x, e1.y};
-      double zl = __shfl_up_sync(0xffffffffu, W[ic][3], 1);
-      double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1);
+      double zl = __shfl_up_sync(0xffffffffu, W[ic][3], 1, kLS);
+      double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1, kLS);
       if (lane == 0) zl = Eg[ic];
-      if (lane == 31) zr = Eg[ic];
+      if (lane == kLS - 1) zr = Eg[ic];
       double lap[4];
       if constexpr (RHO) {
         double fz[5];
@@ -409,7 +425,7 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
 
 template <int MODE, bool RHO>
 __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
-    fwd_lean_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
+    fwd_lean_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int U, int TX,
                     const float* __restrict__ u1, const float* u2, float* uo,
                     float* __restrict__ rec_t, float* __restrict__ strip_t, int has1, int has2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -417,16 +433,19 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int z0 = blockIdx.x * 128;
+  const int l = lane % kLS;  // lane within its group; group lane / kLS works on its own unit
+  const int z0 = blockIdx.x * kSW;
   const int x0 = (blockIdx.y * kLeanWarps + warp) * TX;
   if (x0 >= g.nx) return;  // warp-uniform
   const int x1 = min(g.nx, x0 + TX);
-  const int lu = blockIdx.z;
+  const int lu0 = blockIdx.z * kSPW + lane / kLS;
+  const bool on = lu0 < U;
+  const int lu = on ? lu0 : U - 1;
   const int u = unit_begin + lu;
   const int b = u / g.S;
   const int s = u - b * g.S;
   const size_t N2 = (size_t)g.nx * g.nz;
-  const LaneInfo L = lane_info(g, T, z0 + 4 * lane);
+  const LaneInfo L = lane_info(g, T, z0 + 4 * l, on);
   const int txx = __ldg(g.tx + 2 * s), txz = __ldg(g.tx + 2 * s + 1);
   const int tk = (L.act && txz >= L.z4 && txz < L.z4 + 4) ? txz - L.z4 : -1;
   const double pulse_t = __ldg(g.pulse + t);
@@ -438,12 +457,12 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   float* fo = uo + (size_t)lu * N2;
   const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)b * N2;
   QLane QL{};
-  if constexpr (RHO) QL = q_lane(m, g, b, L.act ? L.z4 : 0, z0, lane, L.z4);
+  if constexpr (RHO) QL = q_lane(m, g, b, L.act ? L.z4 : 0, z0, l, L.z4, on);
   if (wzd)
-    fwd_lean_rows<MODE, RHO, true>(g, T, L, ring, QL, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t,
+    fwd_lean_rows<MODE, RHO, true>(g, T, L, ring, QL, tid, l, z0, x0, x1, lu, txx, tk, pulse_t,
                                    f1, f2, Ec, fo, rec_t, strip_t, has1, has2, wrx, wring);
   else
-    fwd_lean_rows<MODE, RHO, false>(g, T, L, ring, QL, tid, lane, z0, x0, x1, lu, txx, tk, pulse_t,
+    fwd_lean_rows<MODE, RHO, false>(g, T, L, ring, QL, tid, l, z0, x0, x1, lu, txx, tk, pulse_t,
                                     f1, f2, Ec, fo, rec_t, strip_t, has1, has2, wrx, wring);
 }
 
@@ -473,9 +492,10 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
   constexpr int NSL = kNSL;
   const int nz = g.nz, nx = g.nx;
   const int zc = L.act ? L.z4 : 0;
-  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < g.nz;
+  const bool edge_l = L.on && lane == 0 && z0 > 0;
+  const bool edge_r = L.on && lane == kLS - 1 && z0 + kSW < g.nz;
   const bool has_edge = edge_l || edge_r;
-  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + 128 : 0;
+  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + kSW : 0;
   const bool ok1 = has1 && L.act, ok2 = has2 && L.act;
   const float* b1 = opaque(L1 + zc);
   float* b2 = opaque(L2 + zc);
@@ -556,10 +576,10 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
       }
       const float4 w2 = ring.l2[k][tid];
       const double l2v[4] = {w2.x, w2.y, w2.z, w2.w};
-      double zl = __shfl_up_sync(0xffffffffu, EL[ic][3], 1);
-      double zr = __shfl_down_sync(0xffffffffu, EL[ic][0], 1);
+      double zl = __shfl_up_sync(0xffffffffu, EL[ic][3], 1, kLS);
+      double zr = __shfl_down_sync(0xffffffffu, EL[ic][0], 1, kLS);
       if (lane == 0) zl = EG[ic];
-      if (lane == 31) zr = EG[ic];
+      if (lane == kLS - 1) zr = EG[ic];
       double adj[4];
       if constexpr (RHO) {
         double fz[5];
@@ -613,7 +633,7 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
 
 template <bool RHO>
 __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
-    adjlam_lean_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int TX,
+    adjlam_lean_kernel(Geo g, Model m, ABTables T, int t, int unit_begin, int U, int TX,
                        const float* __restrict__ l1, float* l2o, const double* __restrict__ rres_t,
                        int has1, int has2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -621,26 +641,29 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int z0 = blockIdx.x * 128;
+  const int l = lane % kLS;  // lane within its group; group lane / kLS works on its own unit
+  const int z0 = blockIdx.x * kSW;
   const int x0 = (blockIdx.y * kLeanWarps + warp) * TX;
   if (x0 >= g.nx) return;  // warp-uniform
   const int x1 = min(g.nx, x0 + TX);
-  const int lu = blockIdx.z;
+  const int lu0 = blockIdx.z * kSPW + lane / kLS;
+  const bool on = lu0 < U;
+  const int lu = on ? lu0 : U - 1;
   const int b = (unit_begin + lu) / g.S;
   const size_t N2 = (size_t)g.nx * g.nz;
-  const LaneInfo L = lane_info(g, T, z0 + 4 * lane);
+  const LaneInfo L = lane_info(g, T, z0 + 4 * l, on);
   const bool wrx = __any_sync(0xffffffffu, L.rxk != 0u);
   const bool wzd = __any_sync(0xffffffffu, L.zd);
   const float* L1 = l1 + (size_t)lu * N2;
   float* L2 = l2o + (size_t)lu * N2;
   const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)b * N2;
   QLane QL{};
-  if constexpr (RHO) QL = q_lane(m, g, b, L.act ? L.z4 : 0, z0, lane, L.z4);
+  if constexpr (RHO) QL = q_lane(m, g, b, L.act ? L.z4 : 0, z0, l, L.z4, on);
   if (wzd)
-    adjlam_lean_rows<RHO, true>(g, T, L, ring, QL, tid, lane, z0, x0, x1, lu, L1, L2, Ec, rres_t,
+    adjlam_lean_rows<RHO, true>(g, T, L, ring, QL, tid, l, z0, x0, x1, lu, L1, L2, Ec, rres_t,
                                 has1, has2, wrx);
   else
-    adjlam_lean_rows<RHO, false>(g, T, L, ring, QL, tid, lane, z0, x0, x1, lu, L1, L2, Ec, rres_t,
+    adjlam_lean_rows<RHO, false>(g, T, L, ring, QL, tid, l, z0, x0, x1, lu, L1, L2, Ec, rres_t,
                                  has1, has2, wrx);
 }
 
@@ -693,20 +716,22 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int nz = g.nz, nx = g.nx;
-  const int z0 = blockIdx.x * 128;
+  const int l = lane % kLS;  // lane within its group; group lane / kLS takes its own row block
+  const int z0 = blockIdx.x * kSW;
   const int rlo = MODE == 2 ? g.x_lo : 0, rhi = MODE == 2 ? g.x_hi + 1 : nx;  // rows [rlo, rhi)
-  const int x0 = rlo + (blockIdx.y * kLeanWarps + warp) * kImgTX;
-  if (x0 >= rhi) return;  // warp-uniform
-  const int x1 = min(rhi, x0 + kImgTX);
+  const int x0 = rlo + ((blockIdx.y * kLeanWarps + warp) * kSPW + lane / kLS) * kImgTX;
+  const bool on = x0 < rhi;
+  if (!__any_sync(0xffffffffu, on)) return;  // warp-uniform
+  const int x1 = on ? min(rhi, x0 + kImgTX) : x0;  // an idle group walks no rows
   const ShotGroup sg = shot_group(g, blockIdx.z, unit_begin, U, gs);
   if (sg.n == 0) return;
   const size_t N2 = (size_t)nx * nz;
-  const int z4 = z0 + 4 * lane;
-  const bool act = z4 < nz;
+  const int z4 = z0 + 4 * l;
+  const bool act = on && z4 < nz;
   const int zc = act ? z4 : 0;
-  const bool edge_l = lane == 0 && z0 > 0, edge_r = lane == 31 && z0 + 128 < nz;
+  const bool edge_l = on && l == 0 && z0 > 0, edge_r = on && l == kLS - 1 && z0 + kSW < nz;
   const bool has_edge = edge_l || edge_r;
-  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + 128 : 0;
+  const int ze = edge_l ? z0 - 1 : edge_r ? z0 + kSW : 0;
   unsigned boxk = 0u;
   int ringl = -1, ringr = -1;
 #pragma unroll
@@ -721,7 +746,7 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)sg.b * N2;
   const double* be = opaque(Ec + zc);
   QLane QL{};
-  if constexpr (RHO) QL = q_lane(m, g, sg.b, zc, z0, lane, z4);
+  if constexpr (RHO) QL = q_lane(m, g, sg.b, zc, z0, l, z4, on);
   const float* U1 = MODE == 1 ? F : utm1;
   auto issue = [&](int k, int i, int sl) {  // item i of the group's k-th shot
     if (k >= sg.n) return;
@@ -797,7 +822,7 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) FX[wi][c] = face(qp[c], qn[c]);
-        if (i >= 2) zfaces(QL, lane, qp, qpe, fz);  // warp-uniform
+        if (i >= 2) zfaces(QL, l, qp, qpe, fz);  // warp-uniform
 #pragma unroll
         for (int c = 0; c < 4; ++c) qp[c] = qn[c];
         qpe = qen;
@@ -806,10 +831,10 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
       const int r = i - 2;
       const int x = x0 + r;
       const int im = (i + 1) % 3, ic = (i + 2) % 3, ip = i % 3;  // rows x-1, x, x+1
-      double zl = __shfl_up_sync(0xffffffffu, W[ic][3], 1);
-      double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1);
-      if (lane == 0) zl = Eg[ic];
-      if (lane == 31) zr = Eg[ic];
+      double zl = __shfl_up_sync(0xffffffffu, W[ic][3], 1, kLS);
+      double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1, kLS);
+      if (l == 0) zl = Eg[ic];
+      if (l == kLS - 1) zr = Eg[ic];
       if (x >= x1) continue;  // warp-uniform (last row block)
       const float4 lf = ring.lam[sl][tid];
       const double lam[4] = {lf.x, lf.y, lf.z, lf.w};
