@@ -551,10 +551,26 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
 // Receiver samples / ring cells of step t, read back from the exchange buffer
 // written at step t (complete after the following __syncthreads) into stage
 // slot t % kStage: one cell per thread, no per-row branches in the step bodies.
+//
+// gather_rank(): the order in which threads take the cells — warps on the SM
+// sub-partitions that hold fewer warps first (a CTA of W warps puts warp w on
+// SMSP w % 4, so with W % 4 != 0 the SMSPs >= W % 4 hold one warp less and
+// finish their step bodies earlier).
+__device__ __forceinline__ int gather_rank() {
+  const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = W & 3;
+  if (r == 0 || (blockDim.x & 31)) return threadIdx.x;
+  const int nl = W / 4 * (4 - r);  // warps on the lighter SMSPs
+  const bool light = (w & 3) >= r;
+  const int idx = light ? (w >> 2) * (4 - r) + (w & 3) - r : (w >> 2) * r + (w & 3);
+  return (light ? idx : nl + idx) * 32 + lane;
+}
+
 template <class T, int MODE>
-__device__ __forceinline__ void io_gather(const IoStage& io, int nrec, int nio, const T* X, int t) {
+__device__ __forceinline__ void io_gather(const IoStage& io, int nrec, int nio, const T* X, int t,
+                                          int rank) {
   const int k = t % kStage;
-  for (int i = threadIdx.x; i < nio; i += blockDim.x) {
+  for (int i = rank; i < nio; i += blockDim.x) {
     if (i < nrec) {
       io.srec[k * io.maxrec + i] = (double)(float)X[io.rec_b[i]];
     } else if (MODE == 2) {
@@ -590,13 +606,13 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
                                          int lu, const StepBufs<T>& B, uint32_t tx_bytes,
                                          double pulse_t, const IoStage& io, int nrec, int nio,
                                          float* __restrict__ rec, float* __restrict__ strips,
-                                         float* __restrict__ hist, size_t N2) {
+                                         float* __restrict__ hist, size_t N2, int grank) {
 #ifdef DUFWI_EXP_TIMING
   const long long T0 = clock64();
 #endif
   step_sync(c, t, B.bar_r, B.bar_w, tx_bytes);
   if (t >= 1) {
-    io_gather<T, MODE>(io, nrec, nio, B.r, t - 1);
+    io_gather<T, MODE>(io, nrec, nio, B.r, t - 1, grank);
     if (t % kStage == 0) flush_stage<MODE>(g, io, t - kStage, kStage, U, lu, rec, strips);
   }
 #ifdef DUFWI_EXP_TIMING
@@ -660,6 +676,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   cluster_sync_all();  // barriers initialised, buffers zeroed, IO lists complete cluster-wide
   const int nrec = io.counts[0];
   const int nio = nrec + (MODE == 2 ? io.counts[1] : 0);
+  const int grank = gather_rank();
 
   // step t writes X[t & 1] / bar[t & 1]; ub receives u[t] at even t, ua at odd t
   const uint32_t xb1 = (uint32_t)(xe * sizeof(T));
@@ -670,18 +687,18 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
     double p = p_next;
     if (owns_src) p_next = g.pulse[t + 1];
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p, io, nrec, nio, rec,
-                           strips, hist, N2);
+                           strips, hist, N2, grank);
     p = p_next;
     if (owns_src && t + 2 < g.nt) p_next = g.pulse[t + 2];
     fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, B1, tx_bytes, p, io, nrec, nio, rec,
-                           strips, hist, N2);
+                           strips, hist, N2, grank);
   }
   if (t < g.nt)
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p_next, io, nrec, nio, rec,
-                           strips, hist, N2);
+                           strips, hist, N2, grank);
   // the last step's samples, then the partial stage
   __syncthreads();
-  io_gather<T, MODE>(io, nrec, nio, X[(g.nt - 1) & 1], g.nt - 1);
+  io_gather<T, MODE>(io, nrec, nio, X[(g.nt - 1) & 1], g.nt - 1, gather_rank());
   {
     const int t0 = (g.nt - 1) / kStage * kStage;
     flush_stage<MODE>(g, io, t0, g.nt - t0, U, lu, rec, strips);
