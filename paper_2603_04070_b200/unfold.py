@@ -191,13 +191,17 @@ def _upload(arrays, device) -> "torch.Tensor":
     pinned staging buffer.  Read-only ChannelData arrays are copied, never aliased."""
     import torch
 
+    import warnings
+
     arrays = [np.asarray(a) for a in arrays]
     n = sum(a.shape[0] for a in arrays)
     stage = _pinned((n,) + arrays[0].shape[1:], device)
-    host = stage.numpy()
     o = 0
     for a in arrays:
-        host[o:o + a.shape[0]] = a
+        with warnings.catch_warnings():  # read-only ChannelData arrays: only read here
+            warnings.simplefilter("ignore", UserWarning)
+            src = torch.from_numpy(a) if a.dtype == np.float64 else torch.from_numpy(a.astype(np.float64))
+        stage[o:o + a.shape[0]].copy_(src)  # torch's multi-threaded host copy
         o += a.shape[0]
     out = torch.empty(stage.shape, dtype=torch.float64, device=device)
     out.copy_(stage, non_blocking=True)

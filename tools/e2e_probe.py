@@ -37,7 +37,7 @@ for k in range(3):
     pk.unfold_infer(obs_host, c0, nets, setup)
 torch.cuda.synchronize()
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(20)
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]) as p:
     pk.unfold_infer(obs_host, c0, nets, setup)
     torch.cuda.synchronize()
