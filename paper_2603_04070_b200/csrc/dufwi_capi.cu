@@ -750,8 +750,8 @@ extern "C" int32_t dufwi_plan_info(const dufwi_plan_t* p, int64_t* out, int32_t 
 #ifdef DUFWI_EXP_TIMING
 extern "C" int dufwi_debug_counters(unsigned long long* out, int n) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * (n < 256 ? n : 256));
-  unsigned long long z[256] = {0};  // g_dbg holds 256 counters
+  cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * (n < 512 ? n : 512));
+  unsigned long long z[512] = {0};  // g_dbg holds 512 counters
   cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
   return 0;
 }

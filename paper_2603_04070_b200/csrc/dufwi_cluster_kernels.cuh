@@ -38,12 +38,12 @@ namespace dufwi {
 
 namespace cg = cooperative_groups;
 #ifdef DUFWI_EXP_TIMING
-// per-warp step timing of CTA ranks 0 and 4 of cluster 0: [sweep][cta][warp][sync, body, path]
-__device__ unsigned long long g_dbg[2 * 2 * 16 * 4];
+// per-warp step timing of CTA ranks 0 and 4 of cluster 0: [sweep][cta][warp < 32][sync, body, path, -]
+__device__ unsigned long long g_dbg[2 * 2 * 32 * 4];
 __device__ __forceinline__ void dbg_step(int sweep, long long T0, long long T1, int path) {
   if ((blockIdx.x == 0 || blockIdx.x == 4) && (threadIdx.x & 31) == 0) {
     const int w = threadIdx.x >> 5;
-    unsigned long long* d = g_dbg + ((sweep * 2 + (blockIdx.x ? 1 : 0)) * 16 + w) * 4;
+    unsigned long long* d = g_dbg + ((sweep * 2 + (blockIdx.x ? 1 : 0)) * 32 + w) * 4;
     atomicAdd(d + 0, (unsigned long long)(T1 - T0));
     atomicAdd(d + 1, (unsigned long long)(clock64() - T1));
     atomicAdd(d + 2, (unsigned long long)path);
