@@ -703,12 +703,17 @@ struct LeanImgRing {
   QRingOpt<kNSL, RHO> fr;     // RHO: q row x0-1+i
 };
 
-template <int MODE, bool RHO>
-__global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
-    img_lean_kernel(Geo g, Model m, int t, int unit_begin, int U, int gs,
-                    const float* __restrict__ lam_t, const float* __restrict__ F, float* ut,
-                    const float* __restrict__ utm1, const float* __restrict__ strip_tm2,
-                    double* __restrict__ acc_part, int do_recon) {
+// PW: every lane of the warp has its 4 cells inside the box columns (no ring
+// column, no cell outside the imaging region): the per-cell box / ring
+// predicates and the ring-strip loads compile away (ncu: 36% of the kernel's
+// instructions were ISETP / FSEL / SEL).
+template <int MODE, bool RHO, bool PW>
+__device__ __forceinline__ void img_lean_body(const Geo& g, const Model& m, int t, int unit_begin,
+                                              int U, int gs, const float* __restrict__ lam_t,
+                                              const float* __restrict__ F, float* ut,
+                                              const float* __restrict__ utm1,
+                                              const float* __restrict__ strip_tm2,
+                                              double* __restrict__ acc_part, int do_recon) {
   constexpr int NSL = kNSL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& ring = *reinterpret_cast<LeanImgRing<RHO>*>(smem_raw);
@@ -727,7 +732,7 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   if (sg.n == 0) return;
   const size_t N2 = (size_t)nx * nz;
   const int z4 = z0 + 4 * l;
-  const bool act = on && z4 < nz;
+  const bool act = PW || (on && z4 < nz);
   const int zc = act ? z4 : 0;
   const bool edge_l = on && l == 0 && z0 > 0, edge_r = on && l == kLS - 1 && z0 + kSW < nz;
   const bool has_edge = edge_l || edge_r;
@@ -740,6 +745,10 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
     if (MODE == 1 ? act : (act && z >= g.z_lo && z <= g.z_hi)) boxk |= 1u << k;
     if (MODE == 2 && act && z == g.z_lo - 1) ringl = k;
     if (MODE == 2 && act && z == g.z_hi + 1) ringr = k;
+  }
+  if (PW) {
+    boxk = 0xFu;
+    ringl = ringr = -1;
   }
   const bool recon_on = MODE == 2 && do_recon;
   const double pulse_t = __ldg(g.pulse + t);
@@ -895,6 +904,26 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
       p[1] = b;
     }
   }
+}
+
+template <int MODE, bool RHO>
+__global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
+    img_lean_kernel(Geo g, Model m, int t, int unit_begin, int U, int gs,
+                    const float* __restrict__ lam_t, const float* __restrict__ F, float* ut,
+                    const float* __restrict__ utm1, const float* __restrict__ strip_tm2,
+                    double* __restrict__ acc_part, int do_recon) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int l = lane % kLS;
+  const int z4 = blockIdx.x * kSW + 4 * l;
+  const int rlo = MODE == 2 ? g.x_lo : 0, rhi = MODE == 2 ? g.x_hi + 1 : g.nx;
+  const int x0 = rlo + ((blockIdx.y * kLeanWarps + warp) * kSPW + lane / kLS) * kImgTX;
+  const bool plain = x0 < rhi && (MODE == 1 ? z4 < g.nz : (z4 >= g.z_lo && z4 + 3 <= g.z_hi));
+  if (__all_sync(0xffffffffu, plain))
+    img_lean_body<MODE, RHO, true>(g, m, t, unit_begin, U, gs, lam_t, F, ut, utm1, strip_tm2,
+                                   acc_part, do_recon);
+  else
+    img_lean_body<MODE, RHO, false>(g, m, t, unit_begin, U, gs, lam_t, F, ut, utm1, strip_tm2,
+                                    acc_part, do_recon);
 }
 
 }  // namespace dufwi
