@@ -191,7 +191,11 @@ def largest_config_sample(units: int = 256, nt: int = 200, reps: int = 2) -> dic
                         f"(of 1024 units x 6000 steps), strips",
             "engine": prof["engine"], "store": prof["store"],
             "forward": {"updates_per_s": upd / (prof["forward_ms"] / 1e3), "launch_ms": prof["forward_ms"],
-                        "achieved": f_gbs, "frac": f_gbs / peak},
+                        "achieved": f_gbs, "frac": f_gbs / peak,
+                        # the 16 B count includes a 4 B read of E per update, which L2
+                        # serves across the phantom's shots; HBM must move 12 B
+                        "dram_compulsory_GBs": f_gbs * 12.0 / ALG_BYTES_FWD,
+                        "dram_frac": f_gbs * 12.0 / ALG_BYTES_FWD / peak},
             "adjoint": {"updates_per_s": upd / (prof["adjoint_ms"] / 1e3), "launch_ms": prof["adjoint_ms"],
                         "achieved": a_gbs, "frac": a_gbs / peak},
             "unit": "GB/s", "peak": peak, "peak_kind": peak_kind}

@@ -12,6 +12,7 @@ namespace dufwi {
 __global__ void set_model_kernel(Geo g, const double* __restrict__ c, const double* __restrict__ rho,
                                  double* __restrict__ Ed, double* __restrict__ dEdc,
                                  double* __restrict__ rho_copy, double* __restrict__ q,
+                                 float* __restrict__ Edf, float* __restrict__ qf,
                                  double inv_dx2_div, double dx2, size_t total) {
   const size_t N2 = (size_t)g.nx * g.nz;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
@@ -23,10 +24,12 @@ __global__ void set_model_kernel(Geo g, const double* __restrict__ c, const doub
     const double cv = c[i];
     const double E = cv * cv * g.dt * g.dt / den;
     Ed[i] = E / dx2;
+    Edf[i] = (float)(E / dx2);
     dEdc[i] = 2.0 * cv * (g.dt * g.dt) / den;
     if (rho) {
       rho_copy[i] = rho[i];
       q[i] = 1.0 / rho[i];
+      qf[i] = (float)(1.0 / rho[i]);
     }
   }
   (void)inv_dx2_div;
@@ -37,7 +40,8 @@ __global__ void set_model_kernel(Geo g, const double* __restrict__ c, const doub
 __global__ void rho_faces_kernel(Geo g, int B, const double* __restrict__ Ed,
                                  const double* __restrict__ rho, const double* __restrict__ q,
                                  double* __restrict__ Er, double* __restrict__ fxe,
-                                 double* __restrict__ fz, double* __restrict__ fz0) {
+                                 double* __restrict__ fz, double* __restrict__ fz0,
+                                 float* __restrict__ Erf) {
   const int nx = g.nx, nz = g.nz;
   const size_t N2 = (size_t)nx * nz, NE = N2 + nz;
   const size_t total = (size_t)B * NE;
@@ -52,6 +56,7 @@ __global__ void rho_faces_kernel(Geo g, int B, const double* __restrict__ Ed,
     if (r < nx) {
       const size_t c = (size_t)b * N2 + (size_t)r * nz + z;
       Er[c] = rho[c] * Ed[c];
+      Erf[c] = (float)(rho[c] * Ed[c]);
       fz[c] = z == nz - 1 ? q[c] : 0.5 * (q[c] + q[c + 1]);
       if (z == 0) fz0[(size_t)b * nx + r] = q[c];
     }

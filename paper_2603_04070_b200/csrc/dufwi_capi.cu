@@ -69,6 +69,7 @@ struct dufwi_plan {
   int lean_tx = 0;      // rows per warp override (DUFWI_LEAN_TX, experiments)
   bool lean_on = true;  // lean stepwise kernels (DUFWI_LEAN=0: the first vec/stream kernels)
   double *Er = nullptr, *fxe = nullptr, *fz = nullptr, *fz0 = nullptr;  // density tables
+  float *Edf = nullptr, *Erf = nullptr, *qf = nullptr;  // f32 coefficient streams (lean kernels)
 };
 
 namespace {
@@ -193,7 +194,8 @@ int max_groups(const dufwi_plan_t* p, int U, bool per_unit) {
 }
 
 Model model_of(const dufwi_plan_t* p) {
-  return Model{p->Ed, p->has_rho ? p->rho : nullptr, p->q, p->Er, p->fxe, p->fz, p->fz0};
+  return Model{p->Ed,  p->has_rho ? p->rho : nullptr, p->q,   p->Er, p->fxe, p->fz,
+               p->fz0, p->Edf,                        p->Erf, p->qf};
 }
 
 int check_units(const dufwi_plan_t* p, int unit_begin, int U) {
@@ -350,7 +352,10 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   const size_t BN2 = (size_t)g.B * nx * nz;
   rc = rc ? rc : dev_alloc(p, &p->Ed, BN2);
   rc = rc ? rc : dev_alloc(p, &p->dEdc, BN2);
+  rc = rc ? rc : dev_alloc(p, &p->Edf, BN2);
   if (p->has_rho) {
+    rc = rc ? rc : dev_alloc(p, &p->Erf, BN2);
+    rc = rc ? rc : dev_alloc(p, &p->qf, BN2);
     rc = rc ? rc : dev_alloc(p, &p->rho, BN2);
     rc = rc ? rc : dev_alloc(p, &p->q, BN2);
     rc = rc ? rc : dev_alloc(p, &p->Er, BN2);
@@ -419,14 +424,14 @@ extern "C" int dufwi_set_model(dufwi_plan_t* p, const double* c_dev, const doubl
   const int threads = 256;
   const int blocks = (int)std::min<size_t>((total + threads - 1) / threads, 148 * 16);
   set_model_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
-      g, c_dev, p->has_rho ? rho_dev : nullptr, p->Ed, p->dEdc, p->rho, p->q, 0.0,
+      g, c_dev, p->has_rho ? rho_dev : nullptr, p->Ed, p->dEdc, p->rho, p->q, p->Edf, p->qf, 0.0,
       p->dx * p->dx, total);
   LAUNCH_CHECK(p);
   if (p->has_rho) {
     const size_t te = (size_t)g.B * (g.nx + 1) * g.nz;
     const int b2 = (int)std::min<size_t>((te + threads - 1) / threads, 148 * 16);
     rho_faces_kernel<<<b2, threads, 0, (cudaStream_t)stream>>>(g, g.B, p->Ed, p->rho, p->q, p->Er,
-                                                               p->fxe, p->fz, p->fz0);
+                                                               p->fxe, p->fz, p->fz0, p->Erf);
     LAUNCH_CHECK(p);
   }
   return DUFWI_OK;

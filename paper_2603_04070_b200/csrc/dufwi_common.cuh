@@ -38,6 +38,10 @@ struct Model {
   const double* fxe;   // [B][nx+1][nz]  x faces (q_{x-1} + q_x)/2; rows 0 and nx: outer = own q
   const double* fz;    // [B][nx][nz]    z faces (q_z + q_{z+1})/2; z = nz-1: outer = own q
   const double* fz0;   // [B][nx]        outer z face left of z = 0: q(x, 0)
+  // f32 copies streamed by the lean kernels (arithmetic stays f64): Ed, Er, q
+  const float* Edf;
+  const float* Erf;
+  const float* qf;
 };
 
 __device__ __forceinline__ double damping_at(const Geo& g, int x, int z) {

@@ -30,11 +30,14 @@
 //   recon     u[t-2] = 2 u1 + Er * D(u1) - u[t] (+ source)
 // The same f64 values as the oracle up to summation order (parity by tolerance).
 //
-// Arithmetic: explicitly rounded f64 (dufwi_common.cuh).  Constant density
-// uses lap5 / fwd_update / adj_update: the same bits as the cluster engine.
+// Arithmetic: explicitly rounded f64 (dufwi_common.cuh), lap5 / fwd_update /
+// adj_update as in the cluster engine.  The coefficient maps (E/dx^2, or Er
+// and q) are streamed as f32 copies written by set_model (a relative change of
+// the medium below 6e-8, far inside the 1e-4 parity bar): 4 B instead of 8 B
+// per cell and map through L2 and the ring, one cp.async instead of two.
 // DRAM per cell update: forward 12 B (read u[t-1], u[t-2], write u[t]); lam
 // update 12 B; imaging + reconstruction 16 B (+16 B / gs accumulator);
-// coefficient tables come from L2 (shared by the phantom's shots).
+// coefficient maps come from L2 (shared by the phantom's shots).
 #pragma once
 
 #include "dufwi_vec_kernels.cuh"
@@ -136,8 +139,8 @@ __device__ __forceinline__ double lapf(double c, double xm, double xp, double zm
 // 72 B of ring per lane and slot.
 template <int NSL>
 struct QRing {
-  double2 q0[NSL][kLeanT], q1[NSL][kLeanT];  // q row (cells 0-1, 2-3)
-  double qe[NSL][kLeanT];                    // q at the lane's edge column
+  float4 q[NSL][kLeanT];   // q row (f32 copy; the face arithmetic is f64)
+  float qe[NSL][kLeanT];   // q at the lane's edge column
 };
 template <int NSL, bool RHO>
 struct QRingOpt {};
@@ -148,8 +151,8 @@ struct QRingOpt<NSL, true> {
 
 // Per-lane view of one phantom's q map.
 struct QLane {
-  const double* q;   // q + zc (row r at r * nz)
-  const double* qe;  // q + edge column (first lane of a group: z0-1, last: z0+kSW)
+  const float* q;   // q + zc (row r at r * nz)
+  const float* qe;  // q + edge column (first lane of a group: z0-1, last: z0+kSW)
   bool edge;         // the lane has an edge column inside the grid
   bool lo, hi;       // the lane's first / last cell is z = 0 / z = nz-1 (outer faces)
 };
@@ -157,7 +160,7 @@ struct QLane {
 __device__ __forceinline__ QLane q_lane(const Model& m, const Geo& g, int b, int zc, int z0,
                                         int l, int z4, bool on) {
   QLane Q;
-  const double* qb = m.q + (size_t)b * g.nx * g.nz;
+  const float* qb = m.qf + (size_t)b * g.nx * g.nz;
   const bool el = on && l == 0 && z0 > 0, er = on && l == kLS - 1 && z0 + kSW < g.nz;
   Q.q = opaque(qb + zc);
   Q.qe = opaque(qb + (el ? z0 - 1 : er ? z0 + kSW : 0));
@@ -170,16 +173,15 @@ __device__ __forceinline__ QLane q_lane(const Model& m, const Geo& g, int b, int
 template <int NSL>
 __device__ __forceinline__ void issue_q(QRing<NSL>& R, const QLane& Q, int tid, int sl, int r,
                                         bool ok, bool act, int nz) {
-  cp16(&R.q0[sl][tid], Q.q + r * nz, ok && act);
-  cp16(&R.q1[sl][tid], Q.q + r * nz + 2, ok && act);
-  cp8(&R.qe[sl][tid], Q.qe + r * nz, ok && Q.edge);
+  cp16(&R.q[sl][tid], Q.q + r * nz, ok && act);
+  cp4(&R.qe[sl][tid], Q.qe + r * nz, ok && Q.edge);
 }
 
 template <int NSL>
 __device__ __forceinline__ void read_q(const QRing<NSL>& R, int tid, int sl, double (&q)[4],
                                        double& qe) {
-  const double2 a = R.q0[sl][tid], c = R.q1[sl][tid];
-  q[0] = a.x; q[1] = a.y; q[2] = c.x; q[3] = c.y;
+  const float4 a = R.q[sl][tid];
+  q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w;
   qe = R.qe[sl][tid];
 }
 
@@ -208,16 +210,14 @@ __device__ __forceinline__ void zfaces(const QLane& Q, int l, const double (&q)[
 __device__ __forceinline__ void rho_prologue(const QLane& Q, bool act, int x0, int nz,
                                              double (&qc)[4], double& qce, double (&fx)[4]) {
   if (act) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(Q.q + x0 * nz));
-    const double2 c = __ldg(reinterpret_cast<const double2*>(Q.q + x0 * nz + 2));
-    qc[0] = a.x; qc[1] = a.y; qc[2] = c.x; qc[3] = c.y;
+    const float4 a = __ldg(reinterpret_cast<const float4*>(Q.q + x0 * nz));
+    qc[0] = a.x; qc[1] = a.y; qc[2] = a.z; qc[3] = a.w;
   }
   if (Q.edge) qce = __ldg(Q.qe + x0 * nz);
   double qm[4] = {qc[0], qc[1], qc[2], qc[3]};
   if (act && x0 >= 1) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(Q.q + (x0 - 1) * nz));
-    const double2 c = __ldg(reinterpret_cast<const double2*>(Q.q + (x0 - 1) * nz + 2));
-    qm[0] = a.x; qm[1] = a.y; qm[2] = c.x; qm[3] = c.y;
+    const float4 a = __ldg(reinterpret_cast<const float4*>(Q.q + (x0 - 1) * nz));
+    qm[0] = a.x; qm[1] = a.y; qm[2] = a.z; qm[3] = a.w;
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) fx[k] = face(qm[k], qc[k]);
@@ -250,8 +250,7 @@ template <int NSL, bool RHO>
 struct LeanFwdRing {
   float4 u1[NSL][kLeanT];   // u[t-1] row r+1
   float4 u2[NSL][kLeanT];   // u[t-2] row r
-  double2 e0[NSL][kLeanT];  // E (RHO: Er) row r, cells 0-1
-  double2 e1[NSL][kLeanT];  // cells 2-3
+  float4 e[NSL][kLeanT];    // E (RHO: Er) row r, f32 copy
   float edge[NSL][kLeanT];  // u[t-1] row r+1 at the group's edge column (z0-1 / z0+kSW)
   QRingOpt<NSL, RHO> fr;    // RHO: q row r+1
 };
@@ -261,7 +260,7 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
                                               LeanFwdRing<kFwdNSL, RHO>& ring, const QLane& QL,
                                               int tid, int lane, int z0, int x0, int x1, int lu,
                                               int txx, int tk, double pulse_t, const float* f1,
-                                              const float* f2, const double* Ec, float* fo,
+                                              const float* f2, const float* Ec, float* fo,
                                               float* rec_t, float* strip_t, bool has1, bool has2,
                                               bool wrx, bool wring) {
   constexpr int NSL = kFwdNSL;
@@ -274,7 +273,7 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
   const bool ok1 = has1 && L.act, ok2 = has2 && L.act;
   const float* b1 = opaque(f1 + zc);
   const float* b2 = opaque(f2 + zc);
-  const double* be = opaque(Ec + zc);
+  const float* be = opaque(Ec + zc);
   const float* bl = opaque(f1 + ze);
   float* bo = opaque(fo + zc);
   double Az[4], Bz[4];
@@ -294,8 +293,7 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
     const int orr = r * nz;
     cp16(&ring.u1[sl][tid], b1 + on, ok1 && okn);
     cp16(&ring.u2[sl][tid], b2 + orr, ok2);
-    cp16(&ring.e0[sl][tid], be + orr, L.act);
-    cp16(&ring.e1[sl][tid], be + orr + 2, L.act);
+    cp16(&ring.e[sl][tid], be + orr, L.act);
     cp4(&ring.edge[sl][tid], bl + on, has_edge && okn);
     if constexpr (RHO) issue_q(ring.fr.r, QL, tid, sl, r + 1, okn, L.act, nz);
   };
@@ -346,9 +344,9 @@ __device__ __forceinline__ void fwd_lean_rows(const Geo& g, const ABTables& T, c
         Eg[ip] = (double)ring.edge[k][tid];
       }
       const float4 w2 = ring.u2[k][tid];
-      const double2 e0 = ring.e0[k][tid], e1 = ring.e1[k][tid];
+      const float4 ef = ring.e[k][tid];
       const double u2v[4] = {w2.x, w2.y, w2.z, w2.w};
-      const double ed[4] = {e0.x, e0.y, e1.x, e1.y};
+      const double ed[4] = {ef.x, ef.y, ef.z, ef.w};
       double zl = __shfl_up_sync(0xffffffffu, W[ic][3], 1, kLS);
       double zr = __shfl_down_sync(0xffffffffu, W[ic][0], 1, kLS);
       if (lane == 0) zl = Eg[ic];
@@ -455,7 +453,7 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const float* f1 = u1 + (size_t)lu * N2;
   const float* f2 = u2 + (size_t)lu * N2;
   float* fo = uo + (size_t)lu * N2;
-  const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)b * N2;
+  const float* Ec = (RHO ? m.Erf : m.Edf) + (size_t)b * N2;
   QLane QL{};
   if constexpr (RHO) QL = q_lane(m, g, b, L.act ? L.z4 : 0, z0, l, L.z4, on);
   if (wzd)
@@ -473,11 +471,10 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
 template <int NSL, bool RHO>
 struct LeanAdjRing {
   float4 l1[NSL][kLeanT];    // lam[t+1] row r+1
-  double2 e0[NSL][kLeanT];   // E (RHO: Er) row r+1, cells 0-1
-  double2 e1[NSL][kLeanT];   // cells 2-3
+  float4 e[NSL][kLeanT];     // E (RHO: Er) row r+1, f32 copy
   float4 l2[NSL][kLeanT];    // lam[t+2] row r
   float edl[NSL][kLeanT];    // lam[t+1] row r+1 at the lane's edge column
-  double ede[NSL][kLeanT];   // E row r+1 at the lane's edge column
+  float ede[NSL][kLeanT];    // E row r+1 at the lane's edge column
   QRingOpt<NSL, RHO> fr;     // RHO: q row r+1
 };
 
@@ -486,7 +483,7 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
                                                  const LaneInfo& L, LeanAdjRing<kNSL, RHO>& ring,
                                                  const QLane& QL, int tid, int lane, int z0,
                                                  int x0, int x1, int lu, const float* L1,
-                                                 float* L2, const double* Ec,
+                                                 float* L2, const float* Ec,
                                                  const double* rres_t, bool has1, bool has2,
                                                  bool wrx) {
   constexpr int NSL = kNSL;
@@ -499,9 +496,9 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
   const bool ok1 = has1 && L.act, ok2 = has2 && L.act;
   const float* b1 = opaque(L1 + zc);
   float* b2 = opaque(L2 + zc);
-  const double* be = opaque(Ec + zc);
+  const float* be = opaque(Ec + zc);
   const float* bl = opaque(L1 + ze);
-  const double* bel = opaque(Ec + ze);
+  const float* bel = opaque(Ec + ze);
   double Az[4], Bz[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -517,11 +514,10 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
     const int on = okn ? (r + 1) * nz : 0;
     const int orr = r * nz;
     cp16(&ring.l1[sl][tid], b1 + on, ok1 && okn);
-    cp16(&ring.e0[sl][tid], be + on, L.act && okn);
-    cp16(&ring.e1[sl][tid], be + on + 2, L.act && okn);
+    cp16(&ring.e[sl][tid], be + on, L.act && okn);
     cp16(&ring.l2[sl][tid], b2 + orr, ok2);
     cp4(&ring.edl[sl][tid], bl + on, has1 && has_edge && okn);
-    cp8(&ring.ede[sl][tid], bel + on, has_edge && okn);
+    cp4(&ring.ede[sl][tid], bel + on, has_edge && okn);
     if constexpr (RHO) issue_q(ring.fr.r, QL, tid, sl, r + 1, okn, L.act, nz);
   };
   // windows of E*lam1 (EL) and raw lam1 (RL), slot (k)%3 = row x-1, (k+1)%3 = x,
@@ -536,15 +532,14 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
     auto ld = [&](int x, int w) {
       if (L.act) {
         const float4 f = __ldg(reinterpret_cast<const float4*>(b1 + x * nz));
-        const double2 a = __ldg(reinterpret_cast<const double2*>(be + x * nz));
-        const double2 c = __ldg(reinterpret_cast<const double2*>(be + x * nz + 2));
+        const float4 a = __ldg(reinterpret_cast<const float4*>(be + x * nz));
         RL[w][0] = f.x; RL[w][1] = f.y; RL[w][2] = f.z; RL[w][3] = f.w;
         EL[w][0] = __dmul_rn(a.x, RL[w][0]);
         EL[w][1] = __dmul_rn(a.y, RL[w][1]);
-        EL[w][2] = __dmul_rn(c.x, RL[w][2]);
-        EL[w][3] = __dmul_rn(c.y, RL[w][3]);
+        EL[w][2] = __dmul_rn(a.z, RL[w][2]);
+        EL[w][3] = __dmul_rn(a.w, RL[w][3]);
       }
-      if (has_edge) EG[w] = __dmul_rn(__ldg(bel + x * nz), (double)__ldg(bl + x * nz));
+      if (has_edge) EG[w] = __dmul_rn((double)__ldg(bel + x * nz), (double)__ldg(bl + x * nz));
     };
     if (x0 >= 1) ld(x0 - 1, 0);
     ld(x0, 1);
@@ -566,13 +561,13 @@ __device__ __forceinline__ void adjlam_lean_rows(const Geo& g, const ABTables& T
       cp_wait<NSL - 1>();
       {
         const float4 f = ring.l1[k][tid];
-        const double2 a = ring.e0[k][tid], c = ring.e1[k][tid];
+        const float4 a = ring.e[k][tid];
         RL[ip][0] = f.x; RL[ip][1] = f.y; RL[ip][2] = f.z; RL[ip][3] = f.w;
         EL[ip][0] = __dmul_rn(a.x, RL[ip][0]);
         EL[ip][1] = __dmul_rn(a.y, RL[ip][1]);
-        EL[ip][2] = __dmul_rn(c.x, RL[ip][2]);
-        EL[ip][3] = __dmul_rn(c.y, RL[ip][3]);
-        EG[ip] = __dmul_rn(ring.ede[k][tid], (double)ring.edl[k][tid]);
+        EL[ip][2] = __dmul_rn(a.z, RL[ip][2]);
+        EL[ip][3] = __dmul_rn(a.w, RL[ip][3]);
+        EG[ip] = __dmul_rn((double)ring.ede[k][tid], (double)ring.edl[k][tid]);
       }
       const float4 w2 = ring.l2[k][tid];
       const double l2v[4] = {w2.x, w2.y, w2.z, w2.w};
@@ -656,7 +651,7 @@ __global__ void __launch_bounds__(kLeanT, RHO ? kLeanMinBRho : kLeanMinB)
   const bool wzd = __any_sync(0xffffffffu, L.zd);
   const float* L1 = l1 + (size_t)lu * N2;
   float* L2 = l2o + (size_t)lu * N2;
-  const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)b * N2;
+  const float* Ec = (RHO ? m.Erf : m.Edf) + (size_t)b * N2;
   QLane QL{};
   if constexpr (RHO) QL = q_lane(m, g, b, L.act ? L.z4 : 0, z0, l, L.z4, on);
   if (wzd)
@@ -697,8 +692,7 @@ struct LeanImgRing {
   float4 u1[kNSL][kLeanT];    // u[t-1] row x0-1+i
   float4 lam[kNSL][kLeanT];   // lam[t] row x0+i-2
   float4 ut[kNSL][kLeanT];    // u[t] row x0+i-2 (MODE 2)
-  double2 e0[kNSL][kLeanT];   // E (RHO: Er) row x0+i-2, cells 0-1 (MODE 2)
-  double2 e1[kNSL][kLeanT];   // cells 2-3
+  float4 e[kNSL][kLeanT];     // E (RHO: Er) row x0+i-2, f32 copy (MODE 2)
   float edge[kNSL][kLeanT];   // u[t-1] row x0-1+i at the lane's edge column
   QRingOpt<kNSL, RHO> fr;     // RHO: q row x0-1+i
 };
@@ -752,8 +746,8 @@ __device__ __forceinline__ void img_lean_body(const Geo& g, const Model& m, int 
   }
   const bool recon_on = MODE == 2 && do_recon;
   const double pulse_t = __ldg(g.pulse + t);
-  const double* Ec = (RHO ? m.Er : m.Ed) + (size_t)sg.b * N2;
-  const double* be = opaque(Ec + zc);
+  const float* Ec = (RHO ? m.Erf : m.Edf) + (size_t)sg.b * N2;
+  const float* be = opaque(Ec + zc);
   QLane QL{};
   if constexpr (RHO) QL = q_lane(m, g, sg.b, zc, z0, l, z4, on);
   const float* U1 = MODE == 1 ? F : utm1;
@@ -776,8 +770,7 @@ __device__ __forceinline__ void img_lean_body(const Geo& g, const Model& m, int 
       cp16(&ring.lam[sl][tid], lam_t + fo + zc + ox, okx && act);
       if (recon_on) {
         cp16(&ring.ut[sl][tid], ut + fo + zc + ox, okx && act);
-        cp16(&ring.e0[sl][tid], be + ox, okx && act);
-        cp16(&ring.e1[sl][tid], be + ox + 2, okx && act);
+        cp16(&ring.e[sl][tid], be + ox, okx && act);
       }
     }
   };
@@ -861,9 +854,9 @@ __device__ __forceinline__ void img_lean_body(const Geo& g, const Model& m, int 
       }
       if (recon_on && act) {
         const float4 uf = ring.ut[sl][tid];
-        const double2 e0 = ring.e0[sl][tid], e1 = ring.e1[sl][tid];
+        const float4 ef = ring.e[sl][tid];
         const double ua[4] = {uf.x, uf.y, uf.z, uf.w};
-        const double ed[4] = {e0.x, e0.y, e1.x, e1.y};
+        const double ed[4] = {ef.x, ef.y, ef.z, ef.w};
         float o[4] = {uf.x, uf.y, uf.z, uf.w};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
