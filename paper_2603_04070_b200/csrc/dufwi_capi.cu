@@ -10,6 +10,7 @@
 #include "../../include/dufwi.h"
 #include "dufwi_aux_kernels.cuh"
 #include "dufwi_cluster_kernels.cuh"
+#include "dufwi_fused_kernels.cuh"
 #include "dufwi_step_kernels.cuh"
 #include "dufwi_vec_kernels.cuh"
 #include "dufwi_lean_kernels.cuh"
@@ -67,6 +68,8 @@ struct dufwi_plan {
   ClusterCfg ccfg_adj{};            // the adjoint's
   bool cluster_ok = false;
   int lean_tx = 0;      // rows per warp override (DUFWI_LEAN_TX, experiments)
+  bool fused_adj = false;  // constant density: one-pass adjoint kernel (DUFWI_FUSED_ADJ, experiment)
+  int fused_minb = 3;      // resident CTAs per SM of the fused adjoint (DUFWI_FUSED_MINB: 2 or 3)
   bool lean_on = true;  // lean stepwise kernels (DUFWI_LEAN=0: the first vec/stream kernels)
   double *Er = nullptr, *fxe = nullptr, *fz = nullptr, *fz0 = nullptr;  // density tables
   float *Edf = nullptr, *Erf = nullptr, *qf = nullptr;  // f32 coefficient streams (lean kernels)
@@ -382,6 +385,8 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.col_flag = p->col_flag;
   if (const char* e = getenv("DUFWI_LEAN")) p->lean_on = atoi(e) != 0;
   if (const char* e = getenv("DUFWI_LEAN_TX")) p->lean_tx = std::max(0, atoi(e));
+  if (const char* e = getenv("DUFWI_FUSED_ADJ")) p->fused_adj = atoi(e) != 0;
+  if (const char* e = getenv("DUFWI_FUSED_MINB")) p->fused_minb = atoi(e);
   {  // lean rings may exceed the 48 KB default of dynamic shared memory
     auto big = [](const void* f, size_t bytes) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -394,6 +399,9 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
     big((const void*)fwd_lean_kernel<2, true>, sizeof(LeanFwdRing<kFwdNSL, true>));
     big((const void*)adjlam_lean_kernel<false>, sizeof(LeanAdjRing<kNSL, false>));
     big((const void*)adjlam_lean_kernel<true>, sizeof(LeanAdjRing<kNSL, true>));
+    big((const void*)adjimg_lean_kernel<1, 3>, sizeof(FusedAdjRing));
+    big((const void*)adjimg_lean_kernel<2, 3>, sizeof(FusedAdjRing));
+    big((const void*)adjimg_lean_kernel<2, 2>, sizeof(FusedAdjRing));
     big((const void*)img_lean_kernel<1, false>, sizeof(LeanImgRing<false>));
     big((const void*)img_lean_kernel<2, false>, sizeof(LeanImgRing<false>));
     big((const void*)img_lean_kernel<1, true>, sizeof(LeanImgRing<true>));
@@ -654,6 +662,29 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
       if (warps >= 148L * 32) { vtx = c; break; }
     }
     if (p->lean_tx > 0) vtx = p->lean_tx;
+    if (use_lean(p) && !p->has_rho && p->fused_adj) {
+      // fused adjoint: lam update, imaging and reconstruction in one pass (24 B/update).
+      // Bit-identical to the split kernels but slower (config 4: 363 vs 318 ms per
+      // 256 units x 200 steps), so off by default.
+      const dim3 fgrid((g.nz + kSW - 1) / kSW,
+                       (g.nx + kLeanWarps * kImgTX * kSPW - 1) / (kLeanWarps * kImgTX * kSPW),
+                       G.ngroups);
+      const float* st_tm2 = (mode == DUFWI_STORE_STRIPS && do_recon) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
+      if (mode == DUFWI_STORE_FULL)
+        adjimg_lean_kernel<1, 3><<<fgrid, kLeanT, sizeof(FusedAdjRing), st>>>(
+            g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o, rres_t, has1, has2, F, ut, utm1, st_tm2,
+            acc_part, do_recon);
+      else if (p->fused_minb == 2)
+        adjimg_lean_kernel<2, 2><<<fgrid, kLeanT, sizeof(FusedAdjRing), st>>>(
+            g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o, rres_t, has1, has2, F, ut, utm1, st_tm2,
+            acc_part, do_recon);
+      else
+        adjimg_lean_kernel<2, 3><<<fgrid, kLeanT, sizeof(FusedAdjRing), st>>>(
+            g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o, rres_t, has1, has2, F, ut, utm1, st_tm2,
+            acc_part, do_recon);
+      LAUNCH_CHECK(p);
+      continue;
+    }
     if (use_lean(p)) {
       // split adjoint: lam update (12 B/update) then imaging + reconstruction
       const dim3 lgrid((g.nz + kSW - 1) / kSW, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx),

@@ -1,5 +1,5 @@
 """Dump traces and gradient of a short config run (diagnostics: compare library
-builds bit for bit).  usage: bitcmp.py CONFIG UNITS NT OUT.txt (sha256 per array)   (DUFWI_LIB selects the build)"""
+builds bit for bit).  usage: bitcmp.py CONFIG UNITS NT OUT.txt [STORE] [norho] (sha256 per array)   (DUFWI_LIB selects the build)"""
 import dataclasses
 import sys
 from pathlib import Path
@@ -13,10 +13,14 @@ from paper_2603_04070_b200 import configs
 from paper_2603_04070_b200 import forward as fwd
 
 cfg, units, nt, out = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+store = sys.argv[5] if len(sys.argv) > 5 else "auto"
+norho = len(sys.argv) > 6 and sys.argv[6] == "norho"
 torch.cuda.set_device(0)
 spec = dataclasses.replace(configs.get_config(cfg), nt=nt)
 B = max(1, -(-units // spec.n_tx))
 wl = configs.make_workload(spec, seed=0, n_phantoms=B)
+if norho:
+    wl = dataclasses.replace(wl, rho=None)
 grid = pk.Grid2D(spec.n, spec.n, spec.dx, spec.dt, spec.nt)
 geom = pk.AcquisitionGeometry(grid, wl.nodes, wl.rx, 0.0, tx_elements=wl.tx)
 damp = pk.build_pml(grid, spec.pml)
@@ -26,7 +30,7 @@ eng.set_model(wl.c_true, wl.rho)
 obs = eng.forward(units=(0, eng.n_units)).double()
 c1 = wl.c_true * 0.999 + 1.5
 eng.set_model(c1, wl.rho)
-mis, g = eng.misfit_and_gradient(obs)
+mis, g = eng.misfit_and_gradient(obs, store=store)
 import hashlib  # noqa: E402
 arrs = {"obs": obs.cpu().numpy(), "mis": mis.cpu().numpy(), "g": g.cpu().numpy()}
 with open(out, "w") as f:
