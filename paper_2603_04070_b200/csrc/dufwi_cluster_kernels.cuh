@@ -665,7 +665,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   load_static<RPT>(g, m, c, pb, txx, txz,
                    reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)),
                    io,
-                   MODE != 1, st);
+                   true, st);  // (FULL too: the history store is in every step variant)
   const uint32_t tx_bytes =
       (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T);
   double ua[RPT], ub[RPT];

@@ -1,6 +1,7 @@
 """Dump traces and gradient of a short config run (diagnostics: compare library
 builds bit for bit).  usage: bitcmp.py CONFIG UNITS NT OUT.txt [STORE] [norho] (sha256 per array)   (DUFWI_LIB selects the build)"""
 import dataclasses
+import os
 import sys
 from pathlib import Path
 
@@ -25,7 +26,7 @@ grid = pk.Grid2D(spec.n, spec.n, spec.dx, spec.dt, spec.nt)
 geom = pk.AcquisitionGeometry(grid, wl.nodes, wl.rx, 0.0, tx_elements=wl.tx)
 damp = pk.build_pml(grid, spec.pml)
 eng = fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes, wl.pulse, damp,
-                     n_phantoms=B, has_rho=wl.rho is not None, engine="stepwise")
+                     n_phantoms=B, has_rho=wl.rho is not None, engine=os.environ.get("BITCMP_ENGINE", "stepwise"))
 eng.set_model(wl.c_true, wl.rho)
 obs = eng.forward(units=(0, eng.n_units)).double()
 c1 = wl.c_true * 0.999 + 1.5
