@@ -126,6 +126,21 @@ int dufwi_finalize_gradient(dufwi_plan_t* plan, const double* acc_dev, int32_t a
                             int32_t guard_radius, double* grad_dev, int32_t* nonfinite_dev,
                             void* stream);
 
+/* Input of a DUFWI update network for B maps of n cells each (no plan needed):
+ * x_out [B][2][n] f32 = ((c - offset) * (1 / scale), g / max|g|), the second channel 0
+ * where max|g| == 0; peak_ws: B doubles of device scratch.  Replaces the
+ * reference's normalize_sos / normalize_gradient and channel stack
+ * (network.py:56-68, 265) on the device (f64; the first channel multiplies by
+ * the reciprocal, as torch's CUDA division by a scalar does). */
+int dufwi_net_input(const double* c_dev, const double* g_dev, int32_t B, int64_t n,
+                    double offset, double scale, double* peak_ws, float* x_out, void* stream);
+
+/* c_out = clamp(c + scale * h, lo, hi) for count cells, h the network's f32
+ * output: the denormalised update and clamp_sos of one unfolded stage
+ * (unfold.py:263-265, network.py:229).  NaN propagates as in NumPy's clip. */
+int dufwi_apply_update(const double* c_dev, const float* h_dev, int64_t count, double scale,
+                       double lo, double hi, double* c_out, void* stream);
+
 /* Number of kernels this plan has launched so far (evidence for benchmarks). */
 int64_t dufwi_plan_launch_count(const dufwi_plan_t* plan);
 

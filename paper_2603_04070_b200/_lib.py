@@ -25,7 +25,13 @@ EXPORTED_SYMBOLS = (
     "dufwi_plan_create", "dufwi_plan_destroy", "dufwi_set_model", "dufwi_workspace_bytes",
     "dufwi_forward", "dufwi_history_offset", "dufwi_residual", "dufwi_adjoint",
     "dufwi_finalize_gradient", "dufwi_plan_launch_count", "dufwi_plan_last_engine", "dufwi_plan_info", "dufwi_last_error", "dufwi_version",
+    "dufwi_net_input", "dufwi_apply_update",
 )
+
+
+# plan-less library kernels launched (the update-net glue: dufwi_net_input = 2,
+# dufwi_apply_update = 1), for launch-count evidence next to the plans' counters
+GLUE_LAUNCHES = [0]
 
 
 class ExtensionUnavailable(RuntimeError):
@@ -79,11 +85,15 @@ def _declare(so: ctypes.CDLL) -> None:
     so.dufwi_plan_last_engine.restype = i32
     so.dufwi_plan_info.argtypes = [vp, ctypes.POINTER(i64), i32]
     so.dufwi_plan_info.restype = i32
+    f64 = ctypes.c_double
+    so.dufwi_net_input.argtypes = [vp, vp, i32, i64, f64, f64, vp, vp, vp]
+    so.dufwi_apply_update.argtypes = [vp, vp, i64, f64, f64, f64, vp, vp]
     so.dufwi_last_error.restype = ctypes.c_char_p
     so.dufwi_version.restype = ctypes.c_char_p
     for name in ("dufwi_plan_create", "dufwi_plan_destroy", "dufwi_set_model",
                  "dufwi_workspace_bytes", "dufwi_forward", "dufwi_history_offset", "dufwi_residual",
-                 "dufwi_adjoint", "dufwi_finalize_gradient"):
+                 "dufwi_adjoint", "dufwi_finalize_gradient", "dufwi_net_input",
+                 "dufwi_apply_update"):
         getattr(so, name).restype = ctypes.c_int
 
 

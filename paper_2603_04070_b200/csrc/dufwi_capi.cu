@@ -794,3 +794,75 @@ extern "C" int dufwi_debug_counters(unsigned long long* out, int n) {
 #endif
 extern "C" const char* dufwi_last_error(void) { return g_last_error.c_str(); }
 extern "C" const char* dufwi_version(void) { return "dufwi-b200 0.1.0 (sm_100a)"; }
+
+// ------------------------------------------------------- update-net glue
+namespace dufwi {
+// max |g| per map as ordered bits (|g| >= 0: integer order = float order; NaN sorts last)
+__global__ void net_peak_kernel(const double* __restrict__ g, long long n,
+                                unsigned long long* __restrict__ peak) {
+  const int b = blockIdx.y;
+  const double* gb = g + (size_t)b * n;
+  unsigned long long m = 0ull;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)__double_as_longlong(fabs(gb[i])));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(peak + b, m);
+}
+__global__ void net_input_kernel(const double* __restrict__ c, const double* __restrict__ g,
+                                 long long n, double offset, double inv_scale,
+                                 const unsigned long long* __restrict__ peak,
+                                 float* __restrict__ x) {
+  const int b = blockIdx.y;
+  const double pk = __longlong_as_double((long long)peak[b]);
+  const bool pos = pk > 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const size_t k = (size_t)b * n + i;
+    // (c - offset) * (1 / scale): the scalar division of torch's CUDA kernels
+    x[(size_t)b * 2 * n + i] = __double2float_rn(__dmul_rn(__dsub_rn(c[k], offset), inv_scale));
+    x[(size_t)b * 2 * n + n + i] = pos ? __double2float_rn(__ddiv_rn(g[k], pk)) : 0.f;
+  }
+}
+__global__ void apply_update_kernel(const double* __restrict__ c, const float* __restrict__ h,
+                                    long long count, double scale, double lo, double hi,
+                                    double* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = __dadd_rn(c[i], __dmul_rn((double)h[i], scale));
+    out[i] = v < lo ? lo : (v > hi ? hi : v);
+  }
+}
+}  // namespace dufwi
+
+extern "C" int dufwi_net_input(const double* c_dev, const double* g_dev, int32_t B, int64_t n,
+                               double offset, double scale, double* peak_ws, float* x_out,
+                               void* stream) {
+  using namespace dufwi;
+  if (!c_dev || !g_dev || !peak_ws || !x_out) return fail(DUFWI_EINVAL, "null argument");
+  if (B <= 0 || n <= 0) return fail(DUFWI_EINVAL, "need B > 0 maps of n > 0 cells");
+  if (!(scale != 0.0)) return fail(DUFWI_EINVAL, "scale must be non-zero");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(peak_ws, 0, (size_t)B * sizeof(double), st));
+  const int bx = (int)std::min<long long>((n + 255) / 256, 148);
+  const dim3 grid(bx, B);
+  net_peak_kernel<<<grid, 256, 0, st>>>(g_dev, n, reinterpret_cast<unsigned long long*>(peak_ws));
+  CUDA_TRY(cudaGetLastError());
+  net_input_kernel<<<grid, 256, 0, st>>>(c_dev, g_dev, n, offset, 1.0 / scale,
+                                         reinterpret_cast<const unsigned long long*>(peak_ws), x_out);
+  CUDA_TRY(cudaGetLastError());
+  return DUFWI_OK;
+}
+
+extern "C" int dufwi_apply_update(const double* c_dev, const float* h_dev, int64_t count,
+                                  double scale, double lo, double hi, double* c_out, void* stream) {
+  using namespace dufwi;
+  if (!c_dev || !h_dev || !c_out) return fail(DUFWI_EINVAL, "null argument");
+  if (count <= 0) return fail(DUFWI_EINVAL, "count must be positive");
+  if (!(lo < hi)) return fail(DUFWI_EINVAL, "bounds must satisfy lo < hi");
+  const int blocks = (int)std::min<long long>((count + 255) / 256, 148 * 8);
+  apply_update_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(c_dev, h_dev, count, scale, lo, hi,
+                                                                c_out);
+  CUDA_TRY(cudaGetLastError());
+  return DUFWI_OK;
+}

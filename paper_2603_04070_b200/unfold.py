@@ -95,15 +95,17 @@ class Reconstructor:
             _, g = self.engine.misfit_and_gradient(obs, guard_radius=self.guard_radius,
                                                    check_finite=False)
             flags.append(self.engine.last_flags())
-            if hasattr(net, "predict_update_device"):
-                upd = net.predict_update_device(c, g)
+            if hasattr(net, "stage_device") and c.is_cuda:
+                c = net.stage_device(c, g, lo, hi)  # normalisation + update in libdufwi
+            elif hasattr(net, "predict_update_device"):
+                c = torch.clamp(c + net.predict_update_device(c, g), lo, hi)
             else:  # a host network (e.g. the reference's NumPy CNN): one round trip per stage
                 if check_finite:
                     raise_nonfinite(flags[-1].cpu())
                 upd = torch.stack([torch.as_tensor(net.predict_update(ci.cpu().numpy(),
                                                                       gi.cpu().numpy()))
                                    for ci, gi in zip(c, g)]).to(c.device)
-            c = torch.clamp(c + upd, lo, hi)
+                c = torch.clamp(c + upd, lo, hi)
             maps.append(c)
             if keep_gradients:
                 grads.append(g)
@@ -139,10 +141,12 @@ class Reconstructor:
                     self._stages(s_obs, s_c0, False, False)
             torch.cuda.current_stream(obs.device).wait_stream(side)
             graph = torch.cuda.CUDAGraph()
-            n0 = self.engine.launch_count
+            from . import _lib
+
+            n0 = self.engine.launch_count + _lib.GLUE_LAUNCHES[0]
             with torch.cuda.graph(graph):
                 maps, _, flags = self._stages(s_obs, s_c0, False, False)
-            self._g = (key, graph, s_obs, s_c0, maps, flags, self.engine.launch_count - n0,
+            self._g = (key, graph, s_obs, s_c0, maps, flags, self.engine.launch_count + _lib.GLUE_LAUNCHES[0] - n0,
                        self.engine.ws_generation)
         _, graph, s_obs, s_c0, maps, flags, n_launch, _ = self._g
         s_obs.copy_(obs)

@@ -149,3 +149,22 @@ def test_graphed_reconstruct_equals_eager(gpu):
     assert rec._g is not first
     assert all(torch.equal(a, b) for a, b in zip(eager, g3))
     assert rec.replayed_launches > 0
+
+
+def test_stage_device_equals_torch_update_bitwise(gpu):
+    """libdufwi's net input / update kernels give the bits of the torch stage
+    clamp(c + predict_update_device(c, g), lo, hi) (unfold.py:263-265)."""
+    import torch
+
+    from paper_2603_04070_b200.network import make_update_nets
+
+    net = make_update_nets(1, seed=3, device="cuda")[0]
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    c = 1540.0 + 30.0 * torch.randn((2, 64, 48), dtype=torch.float64, device="cuda", generator=gen)
+    g = torch.randn((2, 64, 48), dtype=torch.float64, device="cuda", generator=gen) * 1e-7
+    g[1] = 0.0  # all-zero gradient: second channel 0
+    lo, hi = 1500.0, 1560.0
+    want = torch.clamp(c + net.predict_update_device(c, g), lo, hi)
+    got = net.stage_device(c, g, lo, hi)
+    assert torch.equal(got, want)
+    assert (got == lo).any() and (got == hi).any()
