@@ -174,6 +174,7 @@ class Reconstructor:
 
 _RECON_CACHE: dict = {}
 _PINNED: dict = {}
+_STAGE_EVENTS: dict = {}  # id(staging buffer) -> event after its last upload DMA
 
 
 def _pinned(shape, device) -> "torch.Tensor":
@@ -200,6 +201,9 @@ def _upload(arrays, device) -> "torch.Tensor":
     arrays = [np.asarray(a) for a in arrays]
     n = sum(a.shape[0] for a in arrays)
     stage = _pinned((n,) + arrays[0].shape[1:], device)
+    ev = _STAGE_EVENTS.pop(id(stage), None)
+    if ev is not None:
+        ev.synchronize()  # the previous upload's DMA out of this buffer is done
     o = 0
     for a in arrays:
         with warnings.catch_warnings():  # read-only ChannelData arrays: only read here
@@ -209,8 +213,10 @@ def _upload(arrays, device) -> "torch.Tensor":
         o += a.shape[0]
     out = torch.empty(stage.shape, dtype=torch.float64, device=device)
     out.copy_(stage, non_blocking=True)
-    # the staging buffer is reused by the next call: order its reuse after this copy
-    torch.cuda.current_stream(device).synchronize()
+    # the staging buffer is reused by a later call: its next host write waits on this event
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(device))
+    _STAGE_EVENTS[id(stage)] = ev
     return out
 
 
@@ -266,7 +272,7 @@ def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) ->
     except FloatingPointError as exc:
         raise NumericError(str(exc)) from exc
     host = _download(maps)
-    return [SosMap(grid, host[k, 0]) for k in range(host.shape[0])]
+    return SosMap.stack_checked(grid, host[:, 0])
 
 
 def unfold_infer_batch(m_obs_list, c0_list, nets, setup: InversionSetup) -> list[list[SosMap]]:
@@ -308,4 +314,4 @@ def unfold_infer_batch(m_obs_list, c0_list, nets, setup: InversionSetup) -> list
     except FloatingPointError as exc:
         raise NumericError(str(exc)) from exc
     host = _download(maps)  # (K, B, nx, nz)
-    return [[SosMap(grid, host[k, b]) for k in range(host.shape[0])] for b in range(B)]
+    return [SosMap.stack_checked(grid, host[:, b]) for b in range(B)]

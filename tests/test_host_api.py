@@ -201,3 +201,17 @@ def test_product_path_fails_loudly_without_gpu():
     geom = pk.AcquisitionGeometry(g, z["nodes"], z["rx_pattern"], 0.028)
     with pytest.raises(pk.ExtensionUnavailable):
         pk.simulate_all(pk.SosMap(g, z["c0"]), geom, pk.SourcePulse(z["pulse"], g.dt, 2e5))
+
+
+def test_sos_stack_checked_applies_the_map_rules():
+    import numpy as np
+
+    import paper_2603_04070_b200 as pk
+
+    g = pk.Grid2D(8, 8, 1e-4, 2e-8, 10)
+    maps = pk.SosMap.stack_checked(g, np.full((3, 8, 8), 1500.0))
+    assert len(maps) == 3 and all(isinstance(m, pk.SosMap) for m in maps)
+    assert not maps[0].values.flags.writeable and maps[1].c_max == 1500.0
+    for bad in (np.full((2, 8, 8), np.nan), np.full((2, 8, 8), -1.0), np.full((2, 7, 8), 1500.0)):
+        with pytest.raises(ValueError):
+            pk.SosMap.stack_checked(g, bad)
