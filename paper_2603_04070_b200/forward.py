@@ -158,12 +158,34 @@ _ENGINE_CACHE: "OrderedDict[str, object]" = OrderedDict()
 _ENGINE_CACHE_SIZE = 4
 
 
+_ARRAY_DIGESTS: OrderedDict = OrderedDict()  # id -> (array, digest) of large read-only arrays
+
+
+def _array_digest(p: np.ndarray) -> bytes:
+    """sha1 of an array's dtype, shape and bytes; memoised for large read-only
+    arrays (the immutable containers' damping maps and pulses), which keeps the
+    engine lookup of a repeated public-API call off the host's critical path.
+    The memo holds a reference, so an id is never reused while it is cached."""
+    memo = p.nbytes >= 4096 and not p.flags.writeable
+    if memo:
+        hit = _ARRAY_DIGESTS.get(id(p))
+        if hit is not None and hit[0] is p:
+            return hit[1]
+    h = hashlib.sha1(str((p.dtype, p.shape)).encode())
+    h.update(np.ascontiguousarray(p).tobytes())
+    d = h.digest()
+    if memo:
+        _ARRAY_DIGESTS[id(p)] = (p, d)
+        while len(_ARRAY_DIGESTS) > 32:
+            _ARRAY_DIGESTS.popitem(last=False)
+    return d
+
+
 def _digest(*parts) -> str:
     h = hashlib.sha1()
     for p in parts:
         if isinstance(p, np.ndarray):
-            h.update(str((p.dtype, p.shape)).encode())
-            h.update(np.ascontiguousarray(p).tobytes())
+            h.update(_array_digest(p))
         else:
             h.update(repr(p).encode())
     return h.hexdigest()
