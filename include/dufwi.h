@@ -141,6 +141,22 @@ int dufwi_net_input(const double* c_dev, const double* g_dev, int32_t B, int64_t
 int dufwi_apply_update(const double* c_dev, const float* h_dev, int64_t count, double scale,
                        double lo, double hi, double* c_out, void* stream);
 
+/* 5-point Laplacian with zeros outside the grid of `batch` f64 fields [nx][nz]
+ * (u_dev, out_dev: batch*nx*nz doubles, out must not alias u), in the
+ * reference's accumulation order: out = -4u, += x-1, += x+1, += z-1, += z+1,
+ * /= dx*dx — bit-identical to NumPy.  Replaces forward.laplacian
+ * (forward.py:211-223). */
+int dufwi_laplacian(const double* u_dev, int64_t batch, int32_t nx, int32_t nz, double dx,
+                    double* out_dev, void* stream);
+
+/* One explicit step of one f64 field (forward.py:237-253):
+ * out = A u1 + B u2 + E lap(u1) + s with A, B, E = step_coefficients(c, d, dt)
+ * (forward.py:226-234), every operation rounded as NumPy does.  All arrays
+ * [nx][nz]; out must not alias u1.  Replaces forward.step_wavefield. */
+int dufwi_step_field(const double* u1_dev, const double* u2_dev, const double* c_dev,
+                     const double* d_dev, const double* s_dev, int32_t nx, int32_t nz, double dx,
+                     double dt, double* out_dev, void* stream);
+
 /* Number of kernels this plan has launched so far (evidence for benchmarks). */
 int64_t dufwi_plan_launch_count(const dufwi_plan_t* plan);
 

@@ -10,11 +10,11 @@ __version__ = "0.1.0"
 from .grid import (SOS_LIMIT, AcquisitionGeometry, ChannelData, CflCheck, DensityMap,
                    GeometryError, Grid2D, SosMap, build_geometry, check_cfl, homogeneous_map,
                    linear_geometry)
-from .forward import (DampingProfile, NumericError, SourcePulse, Wavefield, build_pml,
+from .forward import (DampingProfile, NumericError, SourcePulse, Wavefield, build_pml, laplacian,
                       make_source_pulse, simulate_all, simulate_transmission, simulate_wavefield,
-                      zero_damping)
-from .adjoint import (GradientMap, compute_gradient, data_misfit, gradient_mask,
-                      misfit_and_gradient, misfit_and_gradient_batch)
+                      step_wavefield, zero_damping)
+from .adjoint import (GradientMap, compute_gradient, data_misfit, fd_gradient_oracle,
+                      gradient_mask, misfit_and_gradient, misfit_and_gradient_batch)
 from .unfold import (InversionSetup, Reconstructor, cfl_safe_bounds, clamp_sos, unfold_infer,
                      unfold_infer_batch)
 from ._lib import DufwiError, ExtensionUnavailable
@@ -22,9 +22,10 @@ from ._lib import DufwiError, ExtensionUnavailable
 __all__ = [
     "AcquisitionGeometry", "ChannelData", "CflCheck", "DensityMap", "GeometryError", "Grid2D",
     "SosMap", "SOS_LIMIT", "build_geometry", "check_cfl", "homogeneous_map", "linear_geometry",
-    "DampingProfile", "NumericError", "SourcePulse", "Wavefield", "build_pml",
+    "DampingProfile", "NumericError", "SourcePulse", "Wavefield", "build_pml", "laplacian",
     "make_source_pulse", "simulate_all", "simulate_transmission", "simulate_wavefield",
-    "zero_damping", "GradientMap", "compute_gradient", "data_misfit", "gradient_mask",
+    "step_wavefield", "zero_damping", "GradientMap", "compute_gradient", "data_misfit",
+    "fd_gradient_oracle", "gradient_mask",
     "misfit_and_gradient", "misfit_and_gradient_batch", "InversionSetup", "Reconstructor",
     "cfl_safe_bounds", "clamp_sos", "unfold_infer", "unfold_infer_batch", "DufwiError", "ExtensionUnavailable",
 ]

@@ -25,7 +25,7 @@ EXPORTED_SYMBOLS = (
     "dufwi_plan_create", "dufwi_plan_destroy", "dufwi_set_model", "dufwi_workspace_bytes",
     "dufwi_forward", "dufwi_history_offset", "dufwi_residual", "dufwi_adjoint",
     "dufwi_finalize_gradient", "dufwi_plan_launch_count", "dufwi_plan_last_engine", "dufwi_plan_info", "dufwi_last_error", "dufwi_version",
-    "dufwi_net_input", "dufwi_apply_update",
+    "dufwi_net_input", "dufwi_apply_update", "dufwi_laplacian", "dufwi_step_field",
 )
 
 
@@ -88,12 +88,14 @@ def _declare(so: ctypes.CDLL) -> None:
     f64 = ctypes.c_double
     so.dufwi_net_input.argtypes = [vp, vp, i32, i64, f64, f64, vp, vp, vp]
     so.dufwi_apply_update.argtypes = [vp, vp, i64, f64, f64, f64, vp, vp]
+    so.dufwi_laplacian.argtypes = [vp, i64, i32, i32, f64, vp, vp]
+    so.dufwi_step_field.argtypes = [vp, vp, vp, vp, vp, i32, i32, f64, f64, vp, vp]
     so.dufwi_last_error.restype = ctypes.c_char_p
     so.dufwi_version.restype = ctypes.c_char_p
     for name in ("dufwi_plan_create", "dufwi_plan_destroy", "dufwi_set_model",
                  "dufwi_workspace_bytes", "dufwi_forward", "dufwi_history_offset", "dufwi_residual",
                  "dufwi_adjoint", "dufwi_finalize_gradient", "dufwi_net_input",
-                 "dufwi_apply_update"):
+                 "dufwi_apply_update", "dufwi_laplacian", "dufwi_step_field"):
         getattr(so, name).restype = ctypes.c_int
 
 

@@ -22,7 +22,7 @@ from .forward import (DampingProfile, NumericError, SourcePulse, _check_simulati
 from .grid import ChannelData, Grid2D, SosMap
 
 __all__ = ["GradientMap", "data_misfit", "gradient_mask", "misfit_and_gradient",
-           "compute_gradient", "misfit_and_gradient_batch"]
+           "compute_gradient", "misfit_and_gradient_batch", "fd_gradient_oracle"]
 
 
 @dataclass(frozen=True)
@@ -106,11 +106,17 @@ def misfit_and_gradient_batch(sos_list, obs_list, pulse: SourcePulse,
     """
     import torch
 
+    if len(sos_list) != len(obs_list) or not sos_list:
+        raise ValueError("need one observed data set per speed map")
     geometry = obs_list[0].geometry
     grid = sos_list[0].grid
     damping = damping if damping is not None else zero_damping(grid)
     for s, o in zip(sos_list, obs_list):
+        if not o.geometry.same_acquisition(geometry):
+            raise ValueError("batched gradients need one acquisition geometry")
         _check_simulation_inputs(s, o.geometry, pulse, damping)
+    if density_list is not None and len(density_list) != len(sos_list):
+        raise ValueError("need one density map per speed map")
     B = len(sos_list)
     rho = None
     if density_list is not None:
@@ -126,3 +132,49 @@ def misfit_and_gradient_batch(sos_list, obs_list, pulse: SourcePulse,
         raise NumericError(str(exc)) from exc
     g = grad.cpu().numpy()
     return [float(m) for m in misfit.cpu().numpy()], [GradientMap(grid, g[b]) for b in range(B)]
+
+
+def fd_gradient_oracle(sos: SosMap, m_obs: ChannelData, pulse: SourcePulse, cells, eps: float,
+                       damping: DampingProfile | None = None, *, density=None) -> np.ndarray:
+    """Central-difference misfit derivatives at selected cells (adjoint.py:154-186).
+
+    All 2*len(cells) perturbed models run as phantoms of ONE batched forward
+    sweep on the device; each misfit sum((obs - sim)^2) is reduced in f64 by
+    the residual kernel.  Noise floor: the receiver samples leave the sweep as
+    f32 (the ChannelData format of the engine), so each misfit carries a
+    relative rounding error of order 1e-7 * (trace/residual energy ratio);
+    choose ``eps`` so that the misfit change 2*eps*|g| stays well above it
+    (the reference's own grad-check case, eps = 1e-3 m/s on its 16x16 grid,
+    is checked against the reference's values in tests/test_gpu_api_extras.py).
+    """
+    import torch
+
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    geometry = m_obs.geometry
+    damping = damping if damping is not None else zero_damping(sos.grid)
+    cells = [tuple(int(v) for v in c) for c in cells]
+    if not cells:
+        return np.empty(0)
+    base = np.array(sos.values)
+    maps = []
+    for ix, iz in cells:
+        plus = np.array(base)
+        plus[ix, iz] += eps
+        minus = np.array(base)
+        minus[ix, iz] -= eps
+        for m in (plus, minus):
+            _check_simulation_inputs(sos.with_values(m), geometry, pulse, damping)
+            maps.append(m)
+    rho = _density_values(density, sos.grid)
+    B = len(maps)
+    eng = get_engine(sos.grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
+                     pulse.samples, damping, n_phantoms=B, has_rho=rho is not None)
+    eng.set_model(np.stack(maps), None if rho is None else np.broadcast_to(rho, (B,) + rho.shape))
+    obs = torch.as_tensor(np.ascontiguousarray(m_obs.traces), dtype=torch.float64).to(eng.device)
+    obs = obs.repeat(B, 1, 1)
+    try:
+        j = eng.misfit(obs).cpu().numpy()
+    except FloatingPointError as exc:
+        raise NumericError(str(exc)) from exc
+    return (j[0::2] - j[1::2]) / (2.0 * eps)

@@ -8,9 +8,9 @@
 #include <vector>
 
 #include "../../include/dufwi.h"
+#include "dufwi_api_kernels.cuh"
 #include "dufwi_aux_kernels.cuh"
 #include "dufwi_cluster_kernels.cuh"
-#include "dufwi_fused_kernels.cuh"
 #include "dufwi_step_kernels.cuh"
 #include "dufwi_vec_kernels.cuh"
 #include "dufwi_lean_kernels.cuh"
@@ -43,6 +43,15 @@ int fail(int code, const std::string& msg) {
 
 inline size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
 
+// SMs of the current device (launch sizing; 148 on B200)
+int device_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    return 148;
+  return n;
+}
+
 }  // namespace
 
 struct dufwi_plan {
@@ -51,6 +60,7 @@ struct dufwi_plan {
   double dx = 0, dt = 0;
   bool box_ok = false;  // D == 0 exactly on a rectangle and > 0 elsewhere
   int device = 0;
+  int sms = 148;  // SM count of the plan's device (cudaDevAttrMultiProcessorCount)
   int64_t launches = 0;
   // device tables (owned)
   double *px = nullptr, *pz = nullptr, *d2d = nullptr, *pulse = nullptr;
@@ -68,8 +78,6 @@ struct dufwi_plan {
   ClusterCfg ccfg_adj{};            // the adjoint's
   bool cluster_ok = false;
   int lean_tx = 0;      // rows per warp override (DUFWI_LEAN_TX, experiments)
-  bool fused_adj = false;  // constant density: one-pass adjoint kernel (DUFWI_FUSED_ADJ, experiment)
-  int fused_minb = 3;      // resident CTAs per SM of the fused adjoint (DUFWI_FUSED_MINB: 2 or 3)
   bool lean_on = true;  // lean stepwise kernels (DUFWI_LEAN=0: the first vec/stream kernels)
   double *Er = nullptr, *fxe = nullptr, *fz = nullptr, *fz0 = nullptr;  // density tables
   float *Edf = nullptr, *Erf = nullptr, *qf = nullptr;  // f32 coefficient streams (lean kernels)
@@ -110,7 +118,6 @@ struct Groups {
 
 int zstrips(const Geo& g) { return (g.nz + kStripZ - 1) / kStripZ; }
 long warps_per_group(const Geo& g) { return (long)zstrips(g) * ((g.nx + kRXA - 1) / kRXA); }
-constexpr long kTargetWarps = 148L * 64;  // resident warps wanted per launch
 
 // Group count as enumerated by shot_group(): the chunk's first phantom (maybe
 // partial), then ceil(S/gs) groups for every further phantom.
@@ -131,14 +138,16 @@ Groups fwd_groups(const Geo& g, int unit_begin, int U) { return make_groups(g, u
 
 // Adjoint: as many shots per group as the warp target allows (one f64
 // accumulator read-modify-write per cell, group and step).
-Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec, bool lean) {
+Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec, bool lean,
+                  int sms) {
   if (per_unit) return make_groups(g, unit_begin, U, 1);
   // lean imaging kernel: ~8 groups, enough CTAs for several waves; the
   // accumulator read-modify-write costs 16 B / gs per cell update
   if (lean) return make_groups(g, unit_begin, U, std::max(1, (U + 7) / 8));
   const long wpg = vec ? (long)((g.nz + 127) / 128) * ((g.nx + kVecAdjTX - 1) / kVecAdjTX)
                        : warps_per_group(g);
-  const long target = vec ? 148L * 32 : kTargetWarps;
+  // resident warps wanted per launch
+  const long target = vec ? (long)sms * 32 : (long)sms * 64;
   const long wanted = std::max(1L, (target + wpg - 1) / wpg);
   int gs = (int)std::max(1L, ((long)U + wanted - 1) / wanted);
   if (!vec) gs = (gs + kNSA - 1) / kNSA * kNSA;
@@ -155,7 +164,7 @@ bool use_lean(const dufwi_plan_t* p) {
 }
 
 Groups groups_for(const dufwi_plan_t* p, int unit_begin, int U, bool per_unit) {
-  return adj_groups(p->geo, unit_begin, U, per_unit, use_vec(p), use_lean(p));
+  return adj_groups(p->geo, unit_begin, U, per_unit, use_vec(p), use_lean(p), p->sms);
 }
 
 // Upper bound of the group count over every placement of U units.
@@ -235,6 +244,7 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
 
   auto* p = new dufwi_plan();
   cudaGetDevice(&p->device);
+  p->sms = device_sms();
   p->E = geo->n_elements;
   p->has_rho = geo->has_rho ? 1 : 0;
   p->engine = geo->engine;
@@ -385,8 +395,6 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.col_flag = p->col_flag;
   if (const char* e = getenv("DUFWI_LEAN")) p->lean_on = atoi(e) != 0;
   if (const char* e = getenv("DUFWI_LEAN_TX")) p->lean_tx = std::max(0, atoi(e));
-  if (const char* e = getenv("DUFWI_FUSED_ADJ")) p->fused_adj = atoi(e) != 0;
-  if (const char* e = getenv("DUFWI_FUSED_MINB")) p->fused_minb = atoi(e);
   {  // lean rings may exceed the 48 KB default of dynamic shared memory
     auto big = [](const void* f, size_t bytes) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -399,9 +407,6 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
     big((const void*)fwd_lean_kernel<2, true>, sizeof(LeanFwdRing<kFwdNSL, true>));
     big((const void*)adjlam_lean_kernel<false>, sizeof(LeanAdjRing<kNSL, false>));
     big((const void*)adjlam_lean_kernel<true>, sizeof(LeanAdjRing<kNSL, true>));
-    big((const void*)adjimg_lean_kernel<1, 3>, sizeof(FusedAdjRing));
-    big((const void*)adjimg_lean_kernel<2, 3>, sizeof(FusedAdjRing));
-    big((const void*)adjimg_lean_kernel<2, 2>, sizeof(FusedAdjRing));
     big((const void*)img_lean_kernel<1, false>, sizeof(LeanImgRing<false>));
     big((const void*)img_lean_kernel<2, false>, sizeof(LeanImgRing<false>));
     big((const void*)img_lean_kernel<1, true>, sizeof(LeanImgRing<true>));
@@ -430,14 +435,14 @@ extern "C" int dufwi_set_model(dufwi_plan_t* p, const double* c_dev, const doubl
   const Geo& g = p->geo;
   const size_t total = (size_t)g.B * g.nx * g.nz;
   const int threads = 256;
-  const int blocks = (int)std::min<size_t>((total + threads - 1) / threads, 148 * 16);
+  const int blocks = (int)std::min<size_t>((total + threads - 1) / threads, (size_t)p->sms * 16);
   set_model_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
       g, c_dev, p->has_rho ? rho_dev : nullptr, p->Ed, p->dEdc, p->rho, p->q, p->Edf, p->qf, 0.0,
       p->dx * p->dx, total);
   LAUNCH_CHECK(p);
   if (p->has_rho) {
     const size_t te = (size_t)g.B * (g.nx + 1) * g.nz;
-    const int b2 = (int)std::min<size_t>((te + threads - 1) / threads, 148 * 16);
+    const int b2 = (int)std::min<size_t>((te + threads - 1) / threads, (size_t)p->sms * 16);
     rho_faces_kernel<<<b2, threads, 0, (cudaStream_t)stream>>>(g, g.B, p->Ed, p->rho, p->q, p->Er,
                                                                p->fxe, p->fz, p->fz0, p->Erf);
     LAUNCH_CHECK(p);
@@ -517,7 +522,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     int vtx = 4;
     for (int c : {32, 16, 8, 4}) {
       const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
-      if (warps >= 148L * 32) { vtx = c; break; }
+      if (warps >= (long)p->sms * 32) { vtx = c; break; }
     }
     if (p->lean_tx > 0) vtx = p->lean_tx;
     const dim3 vgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
@@ -571,7 +576,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   }
   if (traces_dev) {
     const size_t total = (size_t)U * g.R * g.nt;
-    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)p->sms * 16);
     gather_traces_kernel<<<blocks, 256, 0, st>>>(g, unit_begin, U, rec, p->rx_slot, traces_dev,
                                                  nonfinite_dev ? nonfinite_dev : p->flag);
     LAUNCH_CHECK(p);
@@ -659,32 +664,9 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     int vtx = 4;  // rows per warp of the lam update: enough warps for the device
     for (int c : {32, 16, 8, 4}) {
       const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
-      if (warps >= 148L * 32) { vtx = c; break; }
+      if (warps >= (long)p->sms * 32) { vtx = c; break; }
     }
     if (p->lean_tx > 0) vtx = p->lean_tx;
-    if (use_lean(p) && !p->has_rho && p->fused_adj) {
-      // fused adjoint: lam update, imaging and reconstruction in one pass (24 B/update).
-      // Bit-identical to the split kernels but slower (config 4: 363 vs 318 ms per
-      // 256 units x 200 steps), so off by default.
-      const dim3 fgrid((g.nz + kSW - 1) / kSW,
-                       (g.nx + kLeanWarps * kImgTX * kSPW - 1) / (kLeanWarps * kImgTX * kSPW),
-                       G.ngroups);
-      const float* st_tm2 = (mode == DUFWI_STORE_STRIPS && do_recon) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
-      if (mode == DUFWI_STORE_FULL)
-        adjimg_lean_kernel<1, 3><<<fgrid, kLeanT, sizeof(FusedAdjRing), st>>>(
-            g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o, rres_t, has1, has2, F, ut, utm1, st_tm2,
-            acc_part, do_recon);
-      else if (p->fused_minb == 2)
-        adjimg_lean_kernel<2, 2><<<fgrid, kLeanT, sizeof(FusedAdjRing), st>>>(
-            g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o, rres_t, has1, has2, F, ut, utm1, st_tm2,
-            acc_part, do_recon);
-      else
-        adjimg_lean_kernel<2, 3><<<fgrid, kLeanT, sizeof(FusedAdjRing), st>>>(
-            g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o, rres_t, has1, has2, F, ut, utm1, st_tm2,
-            acc_part, do_recon);
-      LAUNCH_CHECK(p);
-      continue;
-    }
     if (use_lean(p)) {
       // split adjoint: lam update (12 B/update) then imaging + reconstruction
       const dim3 lgrid((g.nz + kSW - 1) / kSW, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx),
@@ -746,7 +728,7 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   }
   {
     const size_t total = (size_t)G.nb * N2;
-    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)p->sms * 16);
     // the lean density kernels sum D(u) lam; L_rho = rho D: scale by rho once here
     const double* scale = (!clus && p->has_rho && use_lean(p)) ? p->rho : nullptr;
     reduce_groups_kernel<<<blocks, 256, 0, st>>>(g, G.b0, G.nb, G.first, G.gpp, acc_part, acc_dev,
@@ -763,7 +745,7 @@ extern "C" int dufwi_finalize_gradient(dufwi_plan_t* p, const double* acc_dev, i
   if (guard < 0) return fail(DUFWI_EINVAL, "guard radius must be >= 0");
   const Geo& g = p->geo;
   const size_t total = (size_t)g.B * g.nx * g.nz;
-  const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)p->sms * 16);
   finalize_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       g, acc_dev, p->dEdc, p->elements, p->E, apply_mask, guard, p->dx * p->dx, grad_dev,
       nonfinite_dev);
@@ -844,7 +826,7 @@ extern "C" int dufwi_net_input(const double* c_dev, const double* g_dev, int32_t
   if (!(scale != 0.0)) return fail(DUFWI_EINVAL, "scale must be non-zero");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaMemsetAsync(peak_ws, 0, (size_t)B * sizeof(double), st));
-  const int bx = (int)std::min<long long>((n + 255) / 256, 148);
+  const int bx = (int)std::min<long long>((n + 255) / 256, device_sms());
   const dim3 grid(bx, B);
   net_peak_kernel<<<grid, 256, 0, st>>>(g_dev, n, reinterpret_cast<unsigned long long*>(peak_ws));
   CUDA_TRY(cudaGetLastError());
@@ -860,9 +842,44 @@ extern "C" int dufwi_apply_update(const double* c_dev, const float* h_dev, int64
   if (!c_dev || !h_dev || !c_out) return fail(DUFWI_EINVAL, "null argument");
   if (count <= 0) return fail(DUFWI_EINVAL, "count must be positive");
   if (!(lo < hi)) return fail(DUFWI_EINVAL, "bounds must satisfy lo < hi");
-  const int blocks = (int)std::min<long long>((count + 255) / 256, 148 * 8);
+  const int blocks = (int)std::min<long long>((count + 255) / 256, (long long)device_sms() * 8);
   apply_update_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(c_dev, h_dev, count, scale, lo, hi,
                                                                 c_out);
+  CUDA_TRY(cudaGetLastError());
+  return DUFWI_OK;
+}
+
+// ----------------------------------------------------- field utilities
+extern "C" int dufwi_laplacian(const double* u_dev, int64_t batch, int32_t nx, int32_t nz,
+                               double dx, double* out_dev, void* stream) {
+  using namespace dufwi;
+  if (!u_dev || !out_dev) return fail(DUFWI_EINVAL, "null argument");
+  if (batch < 0 || nx < 1 || nz < 1) return fail(DUFWI_EINVAL, "bad field shape");
+  if (!(dx > 0)) return fail(DUFWI_EINVAL, "dx must be positive");
+  if (u_dev == out_dev) return fail(DUFWI_EINVAL, "out must not alias u");
+  const long long total = batch * (long long)nx * nz;
+  if (total == 0) return DUFWI_OK;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)device_sms() * 8);
+  laplacian_f64_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(u_dev, batch, nx, nz, dx * dx,
+                                                                 out_dev);
+  CUDA_TRY(cudaGetLastError());
+  return DUFWI_OK;
+}
+
+extern "C" int dufwi_step_field(const double* u1_dev, const double* u2_dev, const double* c_dev,
+                                const double* d_dev, const double* s_dev, int32_t nx, int32_t nz,
+                                double dx, double dt, double* out_dev, void* stream) {
+  using namespace dufwi;
+  if (!u1_dev || !u2_dev || !c_dev || !d_dev || !s_dev || !out_dev)
+    return fail(DUFWI_EINVAL, "null argument");
+  if (nx < 1 || nz < 1) return fail(DUFWI_EINVAL, "bad field shape");
+  if (!(dx > 0) || !(dt > 0)) return fail(DUFWI_EINVAL, "dx, dt must be positive");
+  if (out_dev == u1_dev) return fail(DUFWI_EINVAL, "out must not alias u_prev");
+  const long long n = (long long)nx * nz;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)device_sms() * 8);
+  step_field_f64_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(u1_dev, u2_dev, c_dev, d_dev,
+                                                                  s_dev, nx, nz, dx * dx, dt,
+                                                                  out_dev);
   CUDA_TRY(cudaGetLastError());
   return DUFWI_OK;
 }

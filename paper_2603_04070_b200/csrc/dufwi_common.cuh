@@ -2,8 +2,11 @@
 //
 // Arithmetic model: wavefields are stored in f32 in HBM, every
 // per-cell update is evaluated in f64 registers from the f32 inputs and rounded
-// once when stored.  Coefficients (E/dx^2, dE/dc, damping profiles, pulse) stay
-// f64 so the only rounding per step is the f32 store.
+// once when stored.  The cluster engine and the first-generation stepwise
+// kernels read f64 coefficients (E/dx^2, dE/dc, density); the lean stepwise
+// kernels stream f32 copies of E/dx^2, rho E/dx^2 and 1/rho (Model::Edf/Erf/qf,
+// half the bytes) and widen them to f64 before the arithmetic.  Damping
+// profiles, (A, B) tables and the pulse are f64 everywhere.
 #pragma once
 
 #include <cuda_runtime.h>

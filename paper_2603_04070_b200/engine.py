@@ -325,11 +325,15 @@ class PhysicsEngine:
 
         ``obs`` is the observed data for all units, (B*S, R, nt) f64 on device
         (the ChannelData layout of grid.py:164-183, phantoms stacked).
-        Under torch.distributed the default unit range is this rank's shard and
-        the partial sums are all-reduced before the mask/scaling epilogue.
+        Under torch.distributed, and only when ``units`` is None, the call is a
+        collective: the unit range is this rank's shard and the partial sums are
+        all-reduced (``reduce``) before the mask/scaling epilogue.  An explicit
+        ``units`` range is a local computation on every rank.
         """
         self._require_model()
+        self._check_obs(obs)
         dist = torch.distributed.is_available() and torch.distributed.is_initialized()
+        collective = dist and units is None
         u0, u1 = units if units is not None else self.local_units()
         mode = self.pick_store(mask, store)
         n = u1 - u0
@@ -351,7 +355,7 @@ class PhysicsEngine:
                                           _ptr(self._misfit), _ptr(ws.buf), ws.buf.numel(), st))
             check(self._so.dufwi_adjoint(self._plan, mode, a, U, _ptr(ws.buf), ws.buf.numel(),
                                          _ptr(self._acc), st))
-        if dist and reduce:
+        if collective and reduce:
             self._red[-1] = self._flag[0].double()
             combine_partials(self._red)
             self._flag[0] = (self._red[-1] > 0).int()
@@ -366,6 +370,37 @@ class PhysicsEngine:
             return misfit, grad, traces
         return misfit, grad
 
+    def _check_obs(self, obs) -> None:
+        """Observed data must cover every unit: (B*S, R, nt) (grid.py:164-183 per phantom)."""
+        want = (self.n_units, self.R, self.nt)
+        if tuple(obs.shape) != want:
+            raise ValueError(f"observed data shape {tuple(obs.shape)} != (units, R, nt) {want}")
+
+    def misfit(self, obs: torch.Tensor, units: tuple[int, int] | None = None,
+               check_finite: bool = True) -> torch.Tensor:
+        """Per-phantom misfit sum((traces - obs)^2) (B,) f64 of a forward sweep alone
+        (data_misfit of simulate_all, adjoint.py:67-72); local, never a collective."""
+        self._require_model()
+        self._check_obs(obs)
+        u0, u1 = units if units is not None else (0, self.n_units)
+        n = u1 - u0
+        chunk = self.chunk_units(STORE_NONE, n)
+        ws = self._workspace(STORE_NONE, chunk)
+        st = self._stream()
+        self._flag.zero_()
+        mis = torch.zeros(self.B, dtype=torch.float64, device=self.device)
+        tr = torch.empty((chunk, self.R, self.nt), dtype=torch.float32, device=self.device)
+        obs = obs.to(self.device, torch.float64).contiguous()
+        for a in range(u0, u1, chunk):
+            U = min(chunk, u1 - a)
+            check(self._so.dufwi_forward(self._plan, STORE_NONE, a, U, _ptr(tr), _ptr(self._flag),
+                                         _ptr(ws.buf), ws.buf.numel(), st))
+            check(self._so.dufwi_residual(self._plan, a, U, _ptr(tr), _ptr(obs[a:]), _ptr(mis),
+                                          _ptr(ws.buf), ws.buf.numel(), st))
+        if check_finite and int(self._flag[0].item()):
+            raise NonFiniteResult("simulation diverged: non-finite receiver samples")
+        return mis
+
     def last_flags(self) -> torch.Tensor:
         """Device copy of the last call's non-finite flags [traces, gradient] (no sync);
         pass to :func:`raise_nonfinite` after a host sync to check deferred results."""
@@ -377,6 +412,7 @@ class PhysicsEngine:
         """Average CUDA-event time of one forward and one adjoint C-ABI call over this
         rank's units (one chunk), on the launching stream — the roofline denominators."""
         self._require_model()
+        self._check_obs(obs)
         u0, u1 = units if units is not None else self.local_units()
         mode = self.pick_store(mask, store)
         U = u1 - u0

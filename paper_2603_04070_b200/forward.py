@@ -26,8 +26,8 @@ from .grid import (AcquisitionGeometry, ChannelData, DensityMap, GeometryError, 
                    check_cfl)
 
 __all__ = ["PML_REFERENCE_SPEED", "NumericError", "DampingProfile", "zero_damping", "build_pml",
-           "SourcePulse", "make_source_pulse", "Wavefield", "simulate_wavefield",
-           "simulate_transmission", "simulate_all", "get_engine"]
+           "SourcePulse", "make_source_pulse", "Wavefield", "laplacian", "step_wavefield",
+           "simulate_wavefield", "simulate_transmission", "simulate_all", "get_engine"]
 
 #: damping calibration speed (forward.py:47-48)
 PML_REFERENCE_SPEED = 1500.0
@@ -59,9 +59,27 @@ class DampingProfile:
         v = np.ascontiguousarray(v)
         v.flags.writeable = False
         object.__setattr__(self, "values", v)
+        if self.profiles is None:
+            object.__setattr__(self, "profiles", _separable_profiles(v))
 
     def interior_mask(self) -> np.ndarray:
         return self.values == 0.0
+
+
+def _separable_profiles(v: np.ndarray):
+    """Axis ramps (px, pz) with max(px[i], pz[j]) == v exactly, or None.
+
+    A map built like build_pml's (forward.py:135-137) but handed over as plain
+    values (e.g. loaded from disk) is recognised, so the kernels read the two
+    1-D ramps: with an undamped cell (i0, j0), px = v[:, j0] and pz = v[i0, :]."""
+    zeros = np.argwhere(v == 0.0)
+    if zeros.size == 0:
+        return None
+    i0, j0 = zeros[0]
+    px, pz = v[:, j0].copy(), v[i0, :].copy()
+    if not np.array_equal(np.maximum(px[:, None], pz[None, :]), v):
+        return None
+    return px, pz
 
 
 def zero_damping(grid: Grid2D) -> DampingProfile:
@@ -151,6 +169,70 @@ class Wavefield:
     u_curr: np.ndarray
     u_prev: np.ndarray
     t: int
+
+
+# ------------------------------------------------------------ field utilities
+def _device():
+    import torch
+
+    from . import _lib
+
+    _lib.lib()  # fails loudly without the extension
+    if not torch.cuda.is_available():
+        raise _lib.ExtensionUnavailable("no CUDA device visible; the DUFWI path is GPU-only")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def laplacian(u: np.ndarray, dx: float) -> np.ndarray:
+    """5-point Laplacian with zeros outside the grid on the trailing two axes
+    (forward.py:211-223), computed by ``dufwi_laplacian`` in float64 with the
+    reference's accumulation order (bit-identical).  Returns float64."""
+    import torch
+
+    from . import _lib
+
+    a = np.asarray(u, dtype=np.float64)
+    if a.ndim < 2:
+        raise ValueError("laplacian needs at least two axes")
+    nx, nz = a.shape[-2:]
+    batch = int(np.prod(a.shape[:-2], dtype=np.int64))
+    if a.size == 0:
+        return np.zeros(a.shape)
+    dev = _device()
+    src = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    out = torch.empty_like(src)
+    _lib.check(_lib.lib().dufwi_laplacian(src.data_ptr(), batch, nx, nz, float(dx), out.data_ptr(),
+                                          torch.cuda.current_stream(dev).cuda_stream))
+    return out.cpu().numpy()
+
+
+def step_wavefield(u_prev: np.ndarray, u_prev2: np.ndarray, sos: SosMap,
+                   damping: DampingProfile, s_t, dt: float) -> np.ndarray:
+    """Single explicit time step (forward.py:237-253), same checks and exceptions;
+    the update runs in ``dufwi_step_field`` (f64, bit-identical to NumPy)."""
+    import torch
+
+    from . import _lib
+
+    if np.shape(u_prev) != sos.grid.shape or np.shape(u_prev2) != sos.grid.shape:
+        raise ValueError("wavefield shape does not match the grid")
+    for name, arr in (("u_prev", u_prev), ("u_prev2", u_prev2), ("s_t", s_t)):
+        if not np.all(np.isfinite(arr)):
+            raise NumericError(f"non-finite values in {name}")
+    grid = sos.grid
+    dev = _device()
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(
+            np.broadcast_to(np.asarray(a, dtype=np.float64), grid.shape))).to(dev)
+
+    u1, u2, c, d, s = (up(a) for a in (u_prev, u_prev2, sos.values, damping.values, s_t))
+    out = torch.empty_like(u1)
+    _lib.check(_lib.lib().dufwi_step_field(u1.data_ptr(), u2.data_ptr(), c.data_ptr(), d.data_ptr(),
+                                           s.data_ptr(), grid.nx, grid.nz, float(grid.dx),
+                                           float(dt), out.data_ptr(),
+                                           torch.cuda.current_stream(dev).cuda_stream))
+    return out.cpu().numpy()
 
 
 # ---------------------------------------------------------------- engine cache

@@ -218,7 +218,7 @@ class _DataTerm:
     def __init__(self, m_obs_list, grid, pulse: SourcePulse, damping: DampingProfile):
         geom = m_obs_list[0].geometry
         for m in m_obs_list:
-            if m.geometry != geom:
+            if not m.geometry.same_acquisition(geom):
                 raise ValueError("batched FWI needs one acquisition geometry")
         self.grid = grid
         self.eng = get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes,

@@ -148,7 +148,7 @@ def batched_gradients(c_maps, samples, setup: InversionSetup, batch: int | None 
         raise ValueError("maps and samples are misaligned")
     geometry = samples[0][0].geometry
     for m_obs, _ in samples:
-        if m_obs.geometry != geometry:
+        if not m_obs.geometry.same_acquisition(geometry):
             raise ValueError("batched gradients need one acquisition geometry for all samples")
     batch = n if batch is None else max(1, int(batch))
     grads = np.zeros_like(c_maps)

@@ -68,12 +68,23 @@ class Reconstructor:
     stages eagerly.
     """
 
-    def __init__(self, engine, nets, bounds, guard_radius: int = 2, rho=None, graph: bool | None = None):
+    def __init__(self, engine, nets, bounds, guard_radius: int = 2, rho=None,
+                 graph: bool | None = None, collective: bool = True, cfl_grid=None):
         self.engine = engine
         self.nets = list(nets)
         self.bounds = bounds
         self.guard_radius = guard_radius
         self.rho = rho
+        # collective=False: every rank computes all units of its own call (the
+        # per-sample public API); True: units sharded across torch.distributed ranks
+        self.collective = collective
+        # when the upper clamp bound exceeds the CFL limit of this grid, each
+        # stage's input maximum is recorded on the device and checked after the
+        # sync, raising the reference's ValueError (forward.py:259-263 runs in
+        # every stage's compute_gradient, adjoint.py:105)
+        self.cfl_grid = None
+        if cfl_grid is not None and not check_cfl(cfl_grid, bounds[1]).ok:
+            self.cfl_grid = cfl_grid
         # DUFWI_GRAPH=0 launches the stages eagerly (A/B timing, debugging)
         self.graph = (os.environ.get("DUFWI_GRAPH", "1") != "0") if graph is None else graph
         self._g = None  # (key, graph, static obs, static c0, maps, flags, launches, ws generation)
@@ -87,13 +98,18 @@ class Reconstructor:
 
         lo, hi = self.bounds
         c = torch.clamp(c0.to(torch.float64), lo, hi)
-        maps, grads, flags = [], [], []
+        maps, grads, flags, cmax = [], [], [], []
+        dist = (self.collective and torch.distributed.is_available()
+                and torch.distributed.is_initialized() and torch.distributed.get_world_size() > 1)
+        units = None if self.collective else (0, self.engine.n_units)
         for net in self.nets:
+            if self.cfl_grid is not None:
+                cmax.append(c.amax().reshape(1))
             self.engine.set_model(c, self.rho)
             # non-finite checks are deferred to one host sync after the last stage,
             # so the stages queue back to back on the device
             _, g = self.engine.misfit_and_gradient(obs, guard_radius=self.guard_radius,
-                                                   check_finite=False)
+                                                   check_finite=False, units=units)
             flags.append(self.engine.last_flags())
             if hasattr(net, "stage_device") and c.is_cuda:
                 c = net.stage_device(c, g, lo, hi)  # normalisation + update in libdufwi
@@ -106,16 +122,34 @@ class Reconstructor:
                                                                       gi.cpu().numpy()))
                                    for ci, gi in zip(c, g)]).to(c.device)
                 c = torch.clamp(c + upd, lo, hi)
+            if dist:
+                # one update for all ranks: rank 0's map (replicated networks could
+                # otherwise round differently per rank, e.g. other cuDNN algorithms)
+                torch.distributed.broadcast(c, src=0)
             maps.append(c)
             if keep_gradients:
                 grads.append(g)
-        return maps, grads, torch.stack(flags)
+        stage_cmax = torch.cat(cmax) if cmax else None
+        return maps, grads, torch.stack(flags), stage_cmax
+
+    def _check_stages(self, flags, stage_cmax) -> None:
+        """Raise for the first failing stage, in the reference's order: the CFL check of
+        the stage input (forward.py:259-263), then the non-finite checks."""
+        from .engine import raise_nonfinite
+
+        cm = stage_cmax.cpu().tolist() if stage_cmax is not None else None
+        for k, f in enumerate(flags.cpu()):
+            if cm is not None:
+                cfl = check_cfl(self.cfl_grid, cm[k])
+                if not cfl.ok:
+                    raise ValueError(f"CFL violated: ratio {cfl.ratio:.4f} > 1 for c_max={cm[k]} m/s")
+            raise_nonfinite(f)
 
     def _graphable(self, obs, keep_gradients: bool) -> bool:
         import torch
 
         dist = torch.distributed.is_available() and torch.distributed.is_initialized()
-        return (self.graph and not keep_gradients and not dist and obs.is_cuda
+        return (self.graph and not keep_gradients and not (dist and self.collective) and obs.is_cuda
                 and all(hasattr(n, "predict_update_device") for n in self.nets))
 
     def _graph_key(self, obs, c0):
@@ -145,30 +179,28 @@ class Reconstructor:
 
             n0 = self.engine.launch_count + _lib.GLUE_LAUNCHES[0]
             with torch.cuda.graph(graph):
-                maps, _, flags = self._stages(s_obs, s_c0, False, False)
-            self._g = (key, graph, s_obs, s_c0, maps, flags, self.engine.launch_count + _lib.GLUE_LAUNCHES[0] - n0,
+                maps, _, flags, cmax = self._stages(s_obs, s_c0, False, False)
+            self._g = (key, graph, s_obs, s_c0, maps, (flags, cmax),
+                       self.engine.launch_count + _lib.GLUE_LAUNCHES[0] - n0,
                        self.engine.ws_generation)
-        _, graph, s_obs, s_c0, maps, flags, n_launch, _ = self._g
+        _, graph, s_obs, s_c0, maps, (flags, cmax), n_launch, _ = self._g
         s_obs.copy_(obs)
         s_c0.copy_(c0)
         graph.replay()
         self.replayed_launches += n_launch  # the library's kernels inside the graph
-        return [m.clone() for m in maps], flags
+        return [m.clone() for m in maps], flags.clone(), None if cmax is None else cmax.clone()
 
     def reconstruct(self, obs, c0, keep_gradients: bool = False, check_finite: bool = True):
-        from .engine import raise_nonfinite
-
         graphable = self._graphable(obs, keep_gradients)
         key = self._graph_key(obs, c0) if graphable else None
         if graphable and (self._g is not None and self._g[0] == key or self._seen == key):
-            maps, flags = self._replay(obs, c0)
+            maps, flags, cmax = self._replay(obs, c0)
             grads = []
         else:
             self._seen = key
-            maps, grads, flags = self._stages(obs, c0, keep_gradients, check_finite)
+            maps, grads, flags, cmax = self._stages(obs, c0, keep_gradients, check_finite)
         if check_finite:
-            for f in flags.cpu():  # first failing stage raises
-                raise_nonfinite(f)
+            self._check_stages(flags, cmax)  # first failing stage raises
         return (maps, grads) if keep_gradients else maps
 
 
@@ -231,17 +263,18 @@ def _download(maps) -> np.ndarray:
     return stage.numpy().copy()
 
 
-def _reconstructor(eng, nets, bounds, rho) -> Reconstructor:
+def _reconstructor(eng, nets, bounds, rho, collective: bool, grid) -> Reconstructor:
     """Reconstructor (and its captured graph) reused across calls with the same
     engine, networks and bounds; models with a density map are not cached."""
     if rho is not None:
-        return Reconstructor(eng, nets, bounds, rho=rho)
-    key = (id(eng), tuple(id(n) for n in nets), tuple(bounds))
+        return Reconstructor(eng, nets, bounds, rho=rho, collective=collective, cfl_grid=grid)
+    key = (id(eng), tuple(id(n) for n in nets), tuple(bounds), collective)
     rec = _RECON_CACHE.get(key)
     if rec is None or rec.engine is not eng or any(a is not b for a, b in zip(rec.nets, nets)):
         while len(_RECON_CACHE) >= 4:
             _RECON_CACHE.pop(next(iter(_RECON_CACHE)))
-        rec = _RECON_CACHE[key] = Reconstructor(eng, nets, bounds)
+        rec = _RECON_CACHE[key] = Reconstructor(eng, nets, bounds, collective=collective,
+                                                cfl_grid=grid)
     return rec
 
 
@@ -256,14 +289,14 @@ def unfold_infer(m_obs: ChannelData, c0: SosMap, nets, setup: InversionSetup) ->
     damping = setup.damping if setup.damping is not None else zero_damping(grid)
     geometry = m_obs.geometry
     c_first = clamp_sos(c0, setup.bounds)
+    # stage 1's input; later stages' inputs are checked on the device when the
+    # clamp's upper bound lies above the CFL limit (Reconstructor.cfl_grid)
     _check_simulation_inputs(c_first, geometry, setup.pulse, damping)
-    # every later iterate is clamped to the same bounds: CFL holds for all of them
-    if not check_cfl(grid, hi).ok and not check_cfl(grid, max(c_first.c_max, lo)).ok:
-        raise ValueError("CFL violated by the clamp bounds")
     rho = None if setup.density is None else np.asarray(setup.density, dtype=np.float64)[None]
     eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
                      setup.pulse.samples, damping, has_rho=rho is not None)
-    rec = _reconstructor(eng, nets, setup.bounds, rho)
+    # a per-sample call: never a hidden collective under torch.distributed
+    rec = _reconstructor(eng, nets, setup.bounds, rho, collective=False, grid=grid)
     # ChannelData arrays are read-only views: a writable host copy for torch
     obs = _upload([m_obs.traces], eng.device)
     c = _upload([np.asarray(c0.values, dtype=np.float64)[None]], eng.device)
@@ -295,18 +328,15 @@ def unfold_infer_batch(m_obs_list, c0_list, nets, setup: InversionSetup) -> list
     damping = setup.damping if setup.damping is not None else zero_damping(grid)
     geometry = m_obs_list[0].geometry
     for m, c0 in zip(m_obs_list, c0_list):
-        if m.geometry != geometry:
+        if not m.geometry.same_acquisition(geometry):
             raise ValueError("batched inference needs one acquisition geometry")
-        c_first = clamp_sos(c0, setup.bounds)
-        _check_simulation_inputs(c_first, geometry, setup.pulse, damping)
-        if not check_cfl(grid, hi).ok and not check_cfl(grid, max(c_first.c_max, lo)).ok:
-            raise ValueError("CFL violated by the clamp bounds")
+        _check_simulation_inputs(clamp_sos(c0, setup.bounds), geometry, setup.pulse, damping)
     B = len(c0_list)
     rho = None if setup.density is None else np.broadcast_to(
         np.asarray(setup.density, dtype=np.float64), (B,) + grid.shape).copy()
     eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
                      setup.pulse.samples, damping, n_phantoms=B, has_rho=rho is not None)
-    rec = _reconstructor(eng, nets, setup.bounds, rho)
+    rec = _reconstructor(eng, nets, setup.bounds, rho, collective=True, grid=grid)
     obs = _upload([m.traces for m in m_obs_list], eng.device)
     c = _upload([np.asarray(c0.values, np.float64)[None] for c0 in c0_list], eng.device)
     try:
