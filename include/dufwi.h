@@ -46,6 +46,9 @@ extern "C" {
 #define DUFWI_STORE_FULL 1   /* full f32 history [nt][units][nx][nz] in workspace  */
 #define DUFWI_STORE_STRIPS 2 /* 1-cell ring around the undamped box per step + the
                                 last two states; interior reconstructed backwards */
+#define DUFWI_STORE_CHECKPOINT 3 /* snapshots (u[s0-1], u[s0-2]) every K = ceil(sqrt(2 nt))
+                                    steps; the adjoint recomputes each segment's fields
+                                    from its snapshot (any damping; bit-identical to FULL) */
 
 /* Engine selection (dufwi_geometry_t.engine). */
 #define DUFWI_ENGINE_AUTO 0    /* persistent cluster sweep when the grid fits, else stepwise */
@@ -163,10 +166,13 @@ int64_t dufwi_plan_launch_count(const dufwi_plan_t* plan);
 /* Engine actually used for the last forward/adjoint call (DUFWI_ENGINE_*). */
 int32_t dufwi_plan_last_engine(const dufwi_plan_t* plan);
 
-/* Engine diagnostics: out[0..11] = cluster_ok, cluster CTAs, rows per CTA,
+/* Engine diagnostics: out[0..12] = cluster_ok, cluster CTAs, rows per CTA,
  * rows per thread, threads per CTA, f64 exchange, smem forward, smem adjoint,
  * co-resident clusters (the forward's shape), then the adjoint's cluster CTAs,
- * rows per thread and threads per CTA — for all units at once.
+ * rows per thread and threads per CTA — for all units at once — and the
+ * stepwise kernel family (0 lean: nz % 4 == 0, separable damping with a
+ * rectangular undamped box; 1 vec: other constant-density grids with
+ * nz % 4 == 0; 2 stream: everything else).
  * Returns the number of values written (<= n). */
 int32_t dufwi_plan_info(const dufwi_plan_t* plan, int64_t* out, int32_t n);
 

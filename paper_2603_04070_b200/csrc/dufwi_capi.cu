@@ -106,9 +106,18 @@ int upload(dufwi_plan_t* p, T** out, const T* host, size_t count) {
 // Offsets are independent of where the unit range starts; the residual area
 // comes first so every store mode finds it at the same place.
 struct Layout {
-  size_t rres = 0, mis = 0, rec = 0, ubuf = 0, hist = 0, strips = 0, lbuf = 0, acc_part = 0,
-         total = 0;
+  size_t rres = 0, mis = 0, rec = 0, ubuf = 0, hist = 0, strips = 0, snap = 0, lbuf = 0,
+         acc_part = 0, total = 0;
 };
+
+// Snapshot checkpointing (DUFWI_STORE_CHECKPOINT): segments of K steps,
+// K = ceil(sqrt(2 nt)) minimising the snapshot pairs (2 nt / K fields) plus
+// one segment's recomputed history (K fields).
+int ck_len(int nt) {
+  int k = (int)std::ceil(std::sqrt(2.0 * nt));
+  return std::max(2, std::min(k, nt));
+}
+int ck_segments(int nt) { return (nt + ck_len(nt) - 1) / ck_len(nt); }
 
 // Shot groups of the stepwise kernels for a concrete unit range: groups of up
 // to `gs` shots of one phantom; the adjoint keeps one f64 accumulator per group.
@@ -186,6 +195,11 @@ Layout layout(const dufwi_plan_t* p, int mode, int U) {
   L.ubuf = take(2 * (size_t)U * N2 * sizeof(float));
   if (mode == DUFWI_STORE_FULL) L.hist = take((size_t)g.nt * U * N2 * sizeof(float));
   if (mode == DUFWI_STORE_STRIPS) L.strips = take((size_t)g.nt * U * g.SL * sizeof(float));
+  if (mode == DUFWI_STORE_CHECKPOINT) {
+    // snapshots (u[s0-1], u[s0-2]) of every segment start + one segment's history
+    L.snap = take((size_t)ck_segments(g.nt) * 2 * U * N2 * sizeof(float));
+    L.hist = take((size_t)ck_len(g.nt) * U * N2 * sizeof(float));
+  }
   if (mode != DUFWI_STORE_NONE) {
     L.lbuf = take(2 * (size_t)U * N2 * sizeof(float));
     const int ng = std::max(max_groups(p, U, false), p->cluster_ok ? max_groups(p, U, true) : 0);
@@ -453,7 +467,7 @@ extern "C" int dufwi_set_model(dufwi_plan_t* p, const double* c_dev, const doubl
 extern "C" int dufwi_workspace_bytes(const dufwi_plan_t* p, int32_t mode, int32_t U,
                                      size_t* bytes_out) {
   if (!p || !bytes_out) return fail(DUFWI_EINVAL, "null argument");
-  if (mode < 0 || mode > 2) return fail(DUFWI_EINVAL, "bad store mode");
+  if (mode < 0 || mode > 3) return fail(DUFWI_EINVAL, "bad store mode");
   if (U <= 0) return fail(DUFWI_EINVAL, "unit_count must be positive");
   *bytes_out = layout(p, mode, U).total;
   return DUFWI_OK;
@@ -470,9 +484,137 @@ int ws_check(const dufwi_plan_t* p, int mode, int unit_begin, int U, size_t ws_b
   return 0;
 }
 
-bool use_cluster(const dufwi_plan_t* p) {
-  if (p->engine == DUFWI_ENGINE_STEPWISE) return false;
+bool use_cluster(const dufwi_plan_t* p, int mode) {
+  if (p->engine == DUFWI_ENGINE_STEPWISE || mode == DUFWI_STORE_CHECKPOINT) return false;
   return p->cluster_ok;
+}
+
+// Rows per warp of the stepwise forward / lam-update kernels: enough warps to
+// fill the device.
+int stepwise_tx(const dufwi_plan_t* p, int U) {
+  const Geo& g = p->geo;
+  int vtx = 4;
+  for (int c : {32, 16, 8, 4}) {
+    const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
+    if (warps >= (long)p->sms * 32) { vtx = c; break; }
+  }
+  return p->lean_tx > 0 ? p->lean_tx : vtx;
+}
+
+// One stepwise forward step (forward.py:301-308) over units [unit_begin,
+// unit_begin+U): u[t] -> uo from u1 = u[t-1], u2 = u[t-2] (has1 / has2: those
+// exist), receiver samples -> rec_t, ring strips -> st_t (kmode 2).
+int fwd_step_launch(dufwi_plan_t* p, const Model& m, int kmode, int t, int unit_begin, int U,
+                    const float* u1, const float* u2, float* uo, float* rec_t, float* st_t,
+                    int has1, int has2, cudaStream_t st) {
+  const Geo& g = p->geo;
+  const Groups G = fwd_groups(g, unit_begin, U);
+  const int vtx = stepwise_tx(p, U);
+  const dim3 vgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
+  const dim3 lgrid((g.nz + kSW - 1) / kSW, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx),
+                   (U + kSPW - 1) / kSPW);
+  const dim3 block(kWarpsX * 32);
+  const dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXF - 1) / (kWarpsX * kRXF), G.ngroups);
+#define DUFWI_FWD(R, M)                                                                         \
+  fwd_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, u1, u2,   \
+                                                  uo, rec_t, st_t, has1, has2)
+#define DUFWI_VEC(M)                                                                            \
+  fwd_vec_kernel<M><<<vgrid, kPipeWarps * 32, sizeof(FwdRing), st>>>(g, m, p->ab, t, unit_begin, \
+                                                      vtx, u1, u2, uo, rec_t, st_t, has1, has2)
+#define DUFWI_LEAN(M, R)                                                                        \
+  fwd_lean_kernel<M, R><<<lgrid, kLeanT, sizeof(LeanFwdRing<kFwdNSL, R>), st>>>(                 \
+      g, m, p->ab, t, unit_begin, U, vtx, u1, u2, uo, rec_t, st_t, has1, has2)
+  if (use_lean(p)) {
+    if (p->has_rho) {
+      if (kmode == 2) DUFWI_LEAN(2, true); else DUFWI_LEAN(0, true);
+    } else {
+      if (kmode == 2) DUFWI_LEAN(2, false); else DUFWI_LEAN(0, false);
+    }
+  } else if (use_vec(p)) {
+    if (kmode == 2) DUFWI_VEC(2); else DUFWI_VEC(0);
+  } else if (p->has_rho) {
+    if (kmode == 2) DUFWI_FWD(true, 2); else DUFWI_FWD(true, 0);
+  } else {
+    if (kmode == 2) DUFWI_FWD(false, 2); else DUFWI_FWD(false, 0);
+  }
+#undef DUFWI_FWD
+#undef DUFWI_VEC
+#undef DUFWI_LEAN
+  LAUNCH_CHECK(p);
+  return 0;
+}
+
+// One stepwise adjoint step (adjoint.py:125-131): lam[t] -> l2o from l1 =
+// lam[t+1] and l2o = lam[t+2] (in place), residual injection, and for t >= 1
+// the imaging term with u[t-1]: kmode 1 reads it from F, kmode 2 reconstructs
+// it into ut / utm1 from the strips st_tm1 / st_tm2.
+int adj_step_launch(dufwi_plan_t* p, const Model& m, int kmode, int t, int unit_begin, int U,
+                    const Groups& G, const float* l1, float* l2o, const double* rres_t,
+                    const float* F, float* ut, const float* utm1, const float* st_tm1,
+                    const float* st_tm2, double* acc_part, cudaStream_t st) {
+  const Geo& g = p->geo;
+  const int has1 = t <= g.nt - 2, has2 = t <= g.nt - 3;
+  const int do_img = t >= 1, do_recon = t >= 2;
+  const int vtx = stepwise_tx(p, U);
+  if (use_lean(p)) {
+    // split adjoint: lam update (12 B/update) then imaging + reconstruction
+    const dim3 lgrid((g.nz + kSW - 1) / kSW, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx),
+                     (U + kSPW - 1) / kSPW);
+    if (p->has_rho)
+      adjlam_lean_kernel<true><<<lgrid, kLeanT, sizeof(LeanAdjRing<kNSL, true>), st>>>(
+          g, m, p->ab, t, unit_begin, U, vtx, l1, l2o, rres_t, has1, has2);
+    else
+      adjlam_lean_kernel<false><<<lgrid, kLeanT, sizeof(LeanAdjRing<kNSL, false>), st>>>(
+          g, m, p->ab, t, unit_begin, U, vtx, l1, l2o, rres_t, has1, has2);
+    LAUNCH_CHECK(p);
+    if (do_img) {
+      const int rows = kmode == 2 ? g.Lx : g.nx;
+      const dim3 igrid((g.nz + kSW - 1) / kSW,
+                       (rows + kLeanWarps * kImgTX * kSPW - 1) / (kLeanWarps * kImgTX * kSPW),
+                       G.ngroups);
+#define DUFWI_IMG(M, R)                                                                         \
+  img_lean_kernel<M, R><<<igrid, kLeanT, sizeof(LeanImgRing<R>), st>>>(                          \
+      g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm2, acc_part, do_recon)
+      if (kmode == 1) {
+        if (p->has_rho) DUFWI_IMG(1, true); else DUFWI_IMG(1, false);
+      } else {
+        if (p->has_rho) DUFWI_IMG(2, true); else DUFWI_IMG(2, false);
+      }
+#undef DUFWI_IMG
+      LAUNCH_CHECK(p);
+    }
+    return 0;
+  }
+  if (use_vec(p)) {
+    const dim3 lgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
+    adjlam_pipe_kernel<<<lgrid, kPipeWarps * 32, sizeof(AdjRing), st>>>(
+        g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
+    LAUNCH_CHECK(p);
+    if (do_img) {
+      const dim3 igrid((g.nz + 127) / 128,
+                       (g.nx + kVecAdjWarps * kVecAdjTX - 1) / (kVecAdjWarps * kVecAdjTX), G.ngroups);
+      if (kmode == 1)
+        img_vec_kernel<1><<<igrid, kVecAdjWarps * 32, 0, st>>>(g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm1, acc_part, do_recon);
+      else
+        img_vec_kernel<2><<<igrid, kVecAdjWarps * 32, 0, st>>>(g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm1, acc_part, do_recon);
+      LAUNCH_CHECK(p);
+    }
+    return 0;
+  }
+  const dim3 block(kWarpsX * 32);
+  const dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXA - 1) / (kWarpsX * kRXA), G.ngroups);
+#define DUFWI_ADJ(R, M)                                                                          \
+  adj_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o,  \
+                                                  F, ut, utm1, st_tm1,                            \
+                                                  rres_t, acc_part, has1, has2, do_img, do_recon)
+  if (p->has_rho) {
+    if (kmode == 1) DUFWI_ADJ(true, 1); else DUFWI_ADJ(true, 2);
+  } else {
+    if (kmode == 1) DUFWI_ADJ(false, 1); else DUFWI_ADJ(false, 2);
+  }
+#undef DUFWI_ADJ
+  LAUNCH_CHECK(p);
+  return 0;
 }
 
 }  // namespace
@@ -488,7 +630,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
                              float* traces_dev, int32_t* nonfinite_dev, void* ws, size_t ws_bytes,
                              void* stream) {
   if (!p || !ws) return fail(DUFWI_EINVAL, "null argument");
-  if (mode < 0 || mode > 2) return fail(DUFWI_EINVAL, "bad store mode");
+  if (mode < 0 || mode > 3) return fail(DUFWI_EINVAL, "bad store mode");
   int rc = check_units(p, unit_begin, U);
   if (rc) return rc;
   Layout L;
@@ -504,10 +646,11 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   float* ubuf = reinterpret_cast<float*>(base + L.ubuf);
   float* hist = reinterpret_cast<float*>(base + L.hist);
   float* strips = reinterpret_cast<float*>(base + L.strips);
+  float* snap = reinterpret_cast<float*>(base + L.snap);
   const size_t N2 = (size_t)g.nx * g.nz;
   const size_t fieldU = (size_t)U * N2;
 
-  if (use_cluster(p)) {
+  if (use_cluster(p, mode)) {
     p->last_engine = DUFWI_ENGINE_CLUSTER;
     rc = cluster_forward(g, m, pick_cluster(p->ccands, U), mode, unit_begin, U, rec,
                          mode == DUFWI_STORE_FULL ? hist : nullptr,
@@ -516,21 +659,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     ++p->launches;
   } else {
     p->last_engine = DUFWI_ENGINE_STEPWISE;
-    const Groups G = fwd_groups(g, unit_begin, U);
-    // vectorised kernel: constant density, rows of whole float4s
-    const bool vec = use_vec(p);
-    int vtx = 4;
-    for (int c : {32, 16, 8, 4}) {
-      const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
-      if (warps >= (long)p->sms * 32) { vtx = c; break; }
-    }
-    if (p->lean_tx > 0) vtx = p->lean_tx;
-    const dim3 vgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
-    const bool lean = use_lean(p);
-    const dim3 lgrid((g.nz + kSW - 1) / kSW, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx),
-                     (U + kSPW - 1) / kSPW);
-    dim3 block(kWarpsX * 32);
-    dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXF - 1) / (kWarpsX * kRXF), G.ngroups);
+    const int K = ck_len(g.nt);
     for (int t = 0; t < g.nt; ++t) {
       float* rec_t = rec + (size_t)t * U * g.M;
       const int has1 = t >= 1, has2 = t >= 2;
@@ -546,32 +675,20 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
         uo = ubuf + (size_t)(t & 1) * fieldU;
         u2 = uo;
       }
-#define DUFWI_FWD(R, M)                                                                         \
-  fwd_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, u1, u2,   \
-                                                  uo, rec_t, st_t, has1, has2)
-#define DUFWI_VEC(M)                                                                            \
-  fwd_vec_kernel<M><<<vgrid, kPipeWarps * 32, sizeof(FwdRing), st>>>(g, m, p->ab, t, unit_begin, \
-                                                      vtx, u1, u2, uo, rec_t, st_t, has1, has2)
-#define DUFWI_LEAN(M, R)                                                                        \
-  fwd_lean_kernel<M, R><<<lgrid, kLeanT, sizeof(LeanFwdRing<kFwdNSL, R>), st>>>(                     \
-      g, m, p->ab, t, unit_begin, U, vtx, u1, u2, uo, rec_t, st_t, has1, has2)
-      if (lean) {
-        if (p->has_rho) {
-          if (mode == 0) DUFWI_LEAN(0, true); else if (mode == 1) DUFWI_LEAN(1, true); else DUFWI_LEAN(2, true);
+      if (mode == DUFWI_STORE_CHECKPOINT && t % K == 0) {
+        // segment start: keep (u[t-1], u[t-2]) for the adjoint's recomputation
+        float* sp = snap + (size_t)(t / K) * 2 * fieldU;
+        if (t == 0) {
+          CUDA_TRY(cudaMemsetAsync(sp, 0, 2 * fieldU * sizeof(float), st));
         } else {
-          if (mode == 0) DUFWI_LEAN(0, false); else if (mode == 1) DUFWI_LEAN(1, false); else DUFWI_LEAN(2, false);
+          CUDA_TRY(cudaMemcpyAsync(sp, u1, fieldU * sizeof(float), cudaMemcpyDeviceToDevice, st));
+          CUDA_TRY(cudaMemcpyAsync(sp + fieldU, u2, fieldU * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, st));
         }
-      } else if (vec) {
-        if (mode == 0) DUFWI_VEC(0); else if (mode == 1) DUFWI_VEC(1); else DUFWI_VEC(2);
-      } else if (p->has_rho) {
-        if (mode == 0) DUFWI_FWD(true, 0); else if (mode == 1) DUFWI_FWD(true, 1); else DUFWI_FWD(true, 2);
-      } else {
-        if (mode == 0) DUFWI_FWD(false, 0); else if (mode == 1) DUFWI_FWD(false, 1); else DUFWI_FWD(false, 2);
       }
-#undef DUFWI_FWD
-#undef DUFWI_VEC
-#undef DUFWI_LEAN
-      LAUNCH_CHECK(p);
+      rc = fwd_step_launch(p, m, mode == DUFWI_STORE_STRIPS ? 2 : 0, t, unit_begin, U, u1, u2, uo,
+                           rec_t, st_t, has1, has2, st);
+      if (rc) return rc;
     }
   }
   if (traces_dev) {
@@ -613,8 +730,8 @@ extern "C" int dufwi_residual(dufwi_plan_t* p, int32_t unit_begin, int32_t U,
 extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, int32_t U,
                              void* ws, size_t ws_bytes, double* acc_dev, void* stream) {
   if (!p || !ws || !acc_dev) return fail(DUFWI_EINVAL, "null argument");
-  if (mode != DUFWI_STORE_FULL && mode != DUFWI_STORE_STRIPS)
-    return fail(DUFWI_EINVAL, "adjoint needs FULL or STRIPS history");
+  if (mode != DUFWI_STORE_FULL && mode != DUFWI_STORE_STRIPS && mode != DUFWI_STORE_CHECKPOINT)
+    return fail(DUFWI_EINVAL, "adjoint needs FULL, STRIPS or CHECKPOINT history");
   int rc = check_units(p, unit_begin, U);
   if (rc) return rc;
   Layout L;
@@ -625,15 +742,17 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   const Model m = model_of(p);
   char* base = static_cast<char*>(ws);
   const double* rres = reinterpret_cast<const double*>(base + L.rres);
+  float* rec = reinterpret_cast<float*>(base + L.rec);
   float* ubuf = reinterpret_cast<float*>(base + L.ubuf);
   float* hist = reinterpret_cast<float*>(base + L.hist);
   float* strips = reinterpret_cast<float*>(base + L.strips);
+  float* snap = reinterpret_cast<float*>(base + L.snap);
   float* lbuf = reinterpret_cast<float*>(base + L.lbuf);
   double* acc_part = reinterpret_cast<double*>(base + L.acc_part);
   const size_t N2 = (size_t)g.nx * g.nz;
   const size_t fieldU = (size_t)U * N2;
 
-  const bool clus = use_cluster(p);
+  const bool clus = use_cluster(p, mode);
   const Groups G = groups_for(p, unit_begin, U, clus);
   if (clus) {
     p->last_engine = DUFWI_ENGINE_CLUSTER;
@@ -646,85 +765,48 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     if (rc) return fail(DUFWI_ECUDA, std::string("cluster adjoint: ") + cudaGetErrorString((cudaError_t)rc));
     ++p->launches;
   } else {
-  p->last_engine = DUFWI_ENGINE_STEPWISE;
-  CUDA_TRY(cudaMemsetAsync(acc_part, 0, (size_t)G.ngroups * N2 * sizeof(double), st));
-  dim3 block(kWarpsX * 32);
-  dim3 grid(zstrips(g), (g.nx + kWarpsX * kRXA - 1) / (kWarpsX * kRXA), G.ngroups);
-  for (int t = g.nt - 1; t >= 0; --t) {
-    const int has1 = t <= g.nt - 2, has2 = t <= g.nt - 3;
-    const float* l1 = lbuf + (size_t)((t + 1) & 1) * fieldU;
-    float* l2o = lbuf + (size_t)(t & 1) * fieldU;
-    const double* rres_t = rres + (size_t)t * U * g.M;
-    const int do_img = t >= 1;
-    const float* F = (mode == DUFWI_STORE_FULL && do_img) ? hist + (size_t)(t - 1) * fieldU : nullptr;
-    float* ut = ubuf + (size_t)(t & 1) * fieldU;
-    const float* utm1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
-    const float* st_tm1 = (mode == DUFWI_STORE_STRIPS && do_img) ? strips + (size_t)(t - 1) * U * g.SL : nullptr;
-    const int do_recon = t >= 2;
-    int vtx = 4;  // rows per warp of the lam update: enough warps for the device
-    for (int c : {32, 16, 8, 4}) {
-      const long warps = (long)((g.nz + 127) / 128) * ((g.nx + c - 1) / c) * U;
-      if (warps >= (long)p->sms * 32) { vtx = c; break; }
-    }
-    if (p->lean_tx > 0) vtx = p->lean_tx;
-    if (use_lean(p)) {
-      // split adjoint: lam update (12 B/update) then imaging + reconstruction
-      const dim3 lgrid((g.nz + kSW - 1) / kSW, (g.nx + kLeanWarps * vtx - 1) / (kLeanWarps * vtx),
-                       (U + kSPW - 1) / kSPW);
-      if (p->has_rho)
-        adjlam_lean_kernel<true><<<lgrid, kLeanT, sizeof(LeanAdjRing<kNSL, true>), st>>>(
-            g, m, p->ab, t, unit_begin, U, vtx, l1, l2o, rres_t, has1, has2);
-      else
-        adjlam_lean_kernel<false><<<lgrid, kLeanT, sizeof(LeanAdjRing<kNSL, false>), st>>>(
-            g, m, p->ab, t, unit_begin, U, vtx, l1, l2o, rres_t, has1, has2);
-      LAUNCH_CHECK(p);
-      if (do_img) {
-        const int rows = mode == DUFWI_STORE_STRIPS ? g.Lx : g.nx;
-        const dim3 igrid((g.nz + kSW - 1) / kSW,
-                         (rows + kLeanWarps * kImgTX * kSPW - 1) / (kLeanWarps * kImgTX * kSPW),
-                         G.ngroups);
-        const float* st_tm2 = (mode == DUFWI_STORE_STRIPS && do_recon) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
-#define DUFWI_IMG(M, R)                                                                         \
-  img_lean_kernel<M, R><<<igrid, kLeanT, sizeof(LeanImgRing<R>), st>>>(                          \
-      g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm2, acc_part, do_recon)
-        if (mode == DUFWI_STORE_FULL) {
-          if (p->has_rho) DUFWI_IMG(1, true); else DUFWI_IMG(1, false);
-        } else {
-          if (p->has_rho) DUFWI_IMG(2, true); else DUFWI_IMG(2, false);
+    p->last_engine = DUFWI_ENGINE_STEPWISE;
+    CUDA_TRY(cudaMemsetAsync(acc_part, 0, (size_t)G.ngroups * N2 * sizeof(double), st));
+    auto adj_step = [&](int t, const float* F) {
+      const float* l1 = lbuf + (size_t)((t + 1) & 1) * fieldU;
+      float* l2o = lbuf + (size_t)(t & 1) * fieldU;
+      const double* rres_t = rres + (size_t)t * U * g.M;
+      float* ut = ubuf + (size_t)(t & 1) * fieldU;
+      const float* utm1 = ubuf + (size_t)((t - 1) & 1) * fieldU;
+      const bool strip = mode == DUFWI_STORE_STRIPS;
+      const float* st_tm1 = (strip && t >= 1) ? strips + (size_t)(t - 1) * U * g.SL : nullptr;
+      const float* st_tm2 = (strip && t >= 2) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
+      return adj_step_launch(p, m, strip ? 2 : 1, t, unit_begin, U, G, l1, l2o, rres_t,
+                             t >= 1 ? F : nullptr, ut, utm1, st_tm1, st_tm2, acc_part, st);
+    };
+    if (mode == DUFWI_STORE_CHECKPOINT) {
+      // segments last to first: recompute the segment's fields u[s0-1 .. s1-2]
+      // from its snapshot (the same kernels on the same f32 inputs: the same
+      // bits as the first forward), then run its adjoint steps on them
+      const int K = ck_len(g.nt), nseg = ck_segments(g.nt);
+      for (int sgi = nseg - 1; sgi >= 0; --sgi) {
+        const int s0 = sgi * K, s1 = std::min(g.nt, s0 + K);
+        const float* sp = snap + (size_t)sgi * 2 * fieldU;
+        CUDA_TRY(cudaMemcpyAsync(hist, sp, fieldU * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        for (int t = s0; t <= s1 - 2; ++t) {
+          const float* u1 = hist + (size_t)(t - s0) * fieldU;
+          const float* u2 = t == s0 ? sp + fieldU : hist + (size_t)(t - s0 - 1) * fieldU;
+          rc = fwd_step_launch(p, m, 0, t, unit_begin, U, u1, u2, hist + (size_t)(t - s0 + 1) * fieldU,
+                               rec + (size_t)t * U * g.M, nullptr, t >= 1, t >= 2, st);
+          if (rc) return rc;
         }
-#undef DUFWI_IMG
-        LAUNCH_CHECK(p);
+        for (int t = s1 - 1; t >= s0; --t) {
+          rc = adj_step(t, hist + (size_t)(t - s0) * fieldU);  // F = u[t-1]
+          if (rc) return rc;
+        }
       }
-      continue;
-    }
-    if (use_vec(p)) {
-      const dim3 lgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
-      adjlam_pipe_kernel<<<lgrid, kPipeWarps * 32, sizeof(AdjRing), st>>>(
-          g, m, p->ab, t, unit_begin, vtx, l1, l2o, rres_t, has1, has2);
-      LAUNCH_CHECK(p);
-      if (do_img) {
-        const dim3 igrid((g.nz + 127) / 128,
-                         (g.nx + kVecAdjWarps * kVecAdjTX - 1) / (kVecAdjWarps * kVecAdjTX), G.ngroups);
-        if (mode == DUFWI_STORE_FULL)
-          img_vec_kernel<1><<<igrid, kVecAdjWarps * 32, 0, st>>>(g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm1, acc_part, do_recon);
-        else
-          img_vec_kernel<2><<<igrid, kVecAdjWarps * 32, 0, st>>>(g, m, t, unit_begin, U, G.gs, l2o, F, ut, utm1, st_tm1, acc_part, do_recon);
-        LAUNCH_CHECK(p);
-      }
-      continue;
-    }
-#define DUFWI_ADJ(R, M)                                                                          \
-  adj_stream_kernel<R, M><<<grid, block, 0, st>>>(g, m, p->ab, t, unit_begin, U, G.gs, l1, l2o,  \
-                                                  F, ut, utm1, st_tm1,                            \
-                                                  rres_t, acc_part, has1, has2, do_img, do_recon)
-    if (p->has_rho) {
-      if (mode == DUFWI_STORE_FULL) DUFWI_ADJ(true, 1); else DUFWI_ADJ(true, 2);
     } else {
-      if (mode == DUFWI_STORE_FULL) DUFWI_ADJ(false, 1); else DUFWI_ADJ(false, 2);
+      for (int t = g.nt - 1; t >= 0; --t) {
+        const float* F = (mode == DUFWI_STORE_FULL && t >= 1) ? hist + (size_t)(t - 1) * fieldU : nullptr;
+        rc = adj_step(t, F);
+        if (rc) return rc;
+      }
     }
-#undef DUFWI_ADJ
-    LAUNCH_CHECK(p);
-  }
   }
   {
     const size_t total = (size_t)G.nb * N2;
@@ -757,11 +839,12 @@ extern "C" int64_t dufwi_plan_launch_count(const dufwi_plan_t* p) { return p ? p
 extern "C" int32_t dufwi_plan_last_engine(const dufwi_plan_t* p) { return p ? p->last_engine : -1; }
 extern "C" int32_t dufwi_plan_info(const dufwi_plan_t* p, int64_t* out, int32_t n) {
   if (!p || !out) return 0;
-  const int64_t v[12] = {p->cluster_ok ? 1 : 0, p->ccfg.cs, p->ccfg.rows, p->ccfg.rpt,
+  const int64_t v[13] = {p->cluster_ok ? 1 : 0, p->ccfg.cs, p->ccfg.rows, p->ccfg.rpt,
                          p->ccfg.threads, p->ccfg.dbl, (int64_t)p->ccfg.smem_fwd,
                          (int64_t)p->ccfg_adj.smem_adj, p->ccfg.maxc, p->ccfg_adj.cs,
-                         p->ccfg_adj.rpt, p->ccfg_adj.threads};
-  const int k = n < 12 ? n : 12;
+                         p->ccfg_adj.rpt, p->ccfg_adj.threads,
+                         use_lean(p) ? 0 : use_vec(p) ? 1 : 2};
+  const int k = n < 13 ? n : 13;
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;
 }

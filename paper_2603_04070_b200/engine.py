@@ -24,10 +24,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import STORE_FULL, STORE_NONE, STORE_STRIPS, check
+from ._lib import STORE_CHECKPOINT, STORE_FULL, STORE_NONE, STORE_STRIPS, check
 
 __all__ = ["PhysicsEngine", "shard_range", "NonFiniteResult", "STORE_NONE", "STORE_FULL",
-           "STORE_STRIPS"]
+           "STORE_STRIPS", "STORE_CHECKPOINT"]
 
 _ENGINES = {"auto": _lib.ENGINE_AUTO, "stepwise": _lib.ENGINE_STEPWISE,
             "cluster": _lib.ENGINE_CLUSTER}
@@ -190,13 +190,16 @@ class PhysicsEngine:
 
     def info(self) -> dict:
         """Engine configuration chosen by the plan (cluster shape, shared memory)."""
-        buf = (ctypes.c_int64 * 12)()
-        n = self._so.dufwi_plan_info(self._plan, buf, 12)
+        buf = (ctypes.c_int64 * 13)()
+        n = self._so.dufwi_plan_info(self._plan, buf, 13)
         keys = ("cluster_ok", "cluster_ctas", "rows_per_cta", "rows_per_thread",
                 "threads_per_cta", "f64_exchange", "smem_forward", "smem_adjoint",
                 "clusters_resident", "adjoint_cluster_ctas", "adjoint_rows_per_thread",
-                "adjoint_threads_per_cta")
-        return {k: int(buf[i]) for i, k in enumerate(keys[:n])}
+                "adjoint_threads_per_cta", "stepwise_kernels")
+        out = {k: int(buf[i]) for i, k in enumerate(keys[:n])}
+        if "stepwise_kernels" in out:
+            out["stepwise_kernels"] = ("lean", "vec", "stream")[out["stepwise_kernels"]]
+        return out
 
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
@@ -305,16 +308,29 @@ class PhysicsEngine:
         return flat.view(self.nt, self.nx, self.nz).clone()
 
     def pick_store(self, mask: bool, store: str = "auto") -> int:
+        """Forward-history strategy of a gradient: "full" f32 history, "strips"
+        (1-cell ring of the undamped box + backward reconstruction),
+        "checkpoint" (snapshots + segment recomputation, any damping) or
+        "auto": strips where they apply, else full history when one unit's
+        fits the memory budget, else checkpointing."""
         if store == "full":
             return STORE_FULL
+        if store == "checkpoint":
+            return STORE_CHECKPOINT
         if store == "strips":
             if self.box is None:
                 raise ValueError("strip storage needs a rectangular undamped box")
             if not mask and self.box != (0, self.nx - 1, 0, self.nz - 1):
                 raise ValueError("strip storage only reconstructs the undamped box; use mask=True")
             return STORE_STRIPS
+        if store != "auto":
+            raise ValueError(f"unknown store {store!r}")
         if self.box is not None and (mask or self.box == (0, self.nx - 1, 0, self.nz - 1)):
             return STORE_STRIPS
+        free, _ = torch.cuda.mem_get_info(self.device)
+        held = sum(w.buf.numel() for w in self._ws.values())
+        if self._ws_bytes(STORE_FULL, 1) > (free + held) * self.memory_fraction:
+            return STORE_CHECKPOINT
         return STORE_FULL
 
     def misfit_and_gradient(self, obs: torch.Tensor, *, mask: bool = True, guard_radius: int = 2,
@@ -438,5 +454,6 @@ class PhysicsEngine:
         f = [ev[r][0].elapsed_time(ev[r][1]) for r in range(1, reps + 1)]
         a = [ev[r][2].elapsed_time(ev[r][3]) for r in range(1, reps + 1)]
         return {"units": U, "forward_ms": sum(f) / reps, "adjoint_ms": sum(a) / reps,
-                "store": {STORE_FULL: "full", STORE_STRIPS: "strips"}.get(mode, "none"),
+                "store": {STORE_FULL: "full", STORE_STRIPS: "strips",
+                          STORE_CHECKPOINT: "checkpoint"}.get(mode, "none"),
                 "engine": self.last_engine}

@@ -12,7 +12,6 @@ import torch
 import oracle
 import paper_2603_04070_b200 as pk
 from paper_2603_04070_b200 import forward as fwd
-from paper_2603_04070_b200.engine import PhysicsEngine
 
 from ._cases import config_setup, gradcheck16, rel_l2, ring48, small_linear
 
@@ -239,32 +238,3 @@ def test_errors_match_reference_types(gpu):
     big = pk.SourcePulse(np.full(grid.nt, 1e300), grid.dt, 2e5)
     with pytest.raises(pk.NumericError):
         pk.simulate_all(pk.SosMap(grid, z["c0"]), geom, big, damp)
-
-
-@pytest.mark.parametrize("store", STORES)
-def test_fused_adjoint_kernel_bit_identical_to_split(gpu, monkeypatch, store):
-    """The experimental one-pass adjoint (DUFWI_FUSED_ADJ=1, adjimg_lean_kernel) must give
-    the split lam / imaging kernels' bits: same f64 operations in the same order."""
-    wl, grid, geom, pulse, damp = small_linear(n=52, pml=6, nt=200, n_el=12, n_tx=4, seed=5)
-    prof = damp.profiles
-
-    def make():
-        return PhysicsEngine(nx=grid.nx, nz=grid.nz, nt=grid.nt, dx=grid.dx, dt=grid.dt,
-                             tx_nodes=geom.tx_nodes(), rx_nodes=geom.rx_nodes(),
-                             element_nodes=geom.element_nodes, pulse=pulse.samples,
-                             damping_profiles=prof, n_phantoms=1, engine="stepwise")
-
-    monkeypatch.delenv("DUFWI_FUSED_ADJ", raising=False)
-    split = make()
-    monkeypatch.setenv("DUFWI_FUSED_ADJ", "1")
-    fused = make()
-    out = []
-    for eng in (split, fused):
-        eng.set_model(wl.c_true)
-        obs = eng.forward(units=(0, eng.n_units)).double()
-        eng.set_model(wl.c_true * 0.999 + 1.5)
-        mis, g = eng.misfit_and_gradient(obs, store=store)
-        out.append((mis.cpu().numpy(), g.cpu().numpy()))
-    assert np.array_equal(out[0][0], out[1][0])
-    assert np.array_equal(out[0][1], out[1][1])
-    assert np.abs(out[0][1]).max() > 0

@@ -95,3 +95,77 @@ def test_two_rank_gloo_combine_equals_single_process():
                                          mask=False)
         assert np.linalg.norm(got[b * N * N:(b + 1) * N * N].reshape(N, N) - g) <= 1e-12 * np.linalg.norm(g)
         assert abs(got[B * N * N + b] - m) <= 1e-12 * m
+
+
+# ------------------------------------------------- Reconstructor under gloo
+class _StubEngine:
+    """Host stand-in for PhysicsEngine: records the unit ranges it is asked for and
+    returns a rank-dependent 'gradient' (what diverging replicated state would do)."""
+
+    def __init__(self, rank, B=2, n=6):
+        self.rank, self.B, self.n, self.n_units = rank, B, n, 4 * B
+        self.calls = []
+
+    def set_model(self, c, rho=None):
+        self.c = c
+
+    def misfit_and_gradient(self, obs, guard_radius=2, check_finite=True, units=None):
+        self.calls.append(units)
+        g = torch.full((self.B, self.n, self.n), 1e-3 * (1 + self.rank), dtype=torch.float64)
+        return torch.zeros(self.B, dtype=torch.float64), g
+
+    def last_flags(self):
+        return torch.zeros(2, dtype=torch.int32)
+
+
+class _RankNet:
+    """Update network whose output differs per rank (e.g. other cuDNN algorithms)."""
+
+    def __init__(self, rank):
+        self.rank = rank
+
+    def predict_update_device(self, c, g):
+        return g * 1e3 + 0.25 * self.rank
+
+
+def _recon_worker(rank, world, port, q):
+    from paper_2603_04070_b200.unfold import Reconstructor
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = {}
+        for collective in (True, False):
+            eng = _StubEngine(rank)
+            rec = Reconstructor(eng, [_RankNet(rank)] * 3, (1000.0, 2000.0), graph=False,
+                                collective=collective)
+            maps = rec.reconstruct(torch.zeros(8, 1, 1), torch.full((2, 6, 6), 1500.0))
+            out[collective] = (np.stack([m.numpy() for m in maps]), eng.calls)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reconstructor_collective_broadcasts_rank0_maps():
+    """Collective reconstructions broadcast rank 0's stage maps (ranks cannot
+    diverge); per-sample ones (collective=False) compute all units locally."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_recon_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    coll0, calls0 = got[0][True]
+    coll1, calls1 = got[1][True]
+    assert np.array_equal(coll0, coll1)  # rank 1 took rank 0's maps
+    assert np.allclose(coll0[0], 1500.0 + 1.0)  # rank 0's update: 1e-3*1e3 + 0
+    assert calls0 == [None] * 3 and calls1 == [None] * 3  # sharded default ranges
+    loc0, lcalls0 = got[0][False]
+    loc1, _ = got[1][False]
+    assert lcalls0 == [(0, 8)] * 3  # every unit, locally
+    assert not np.array_equal(loc0, loc1)  # no hidden collective
