@@ -135,26 +135,96 @@ def _oracle_shot(args):
     return oracle.misfit_gradient(c, d, dx, dt, pulse, tx, rx, obs, element_nodes=nodes)[:2]
 
 
-def cpu_gradient_sample(wl, grid, geom, pulse, damp, workers: int):
-    """One gradient evaluation (forward + adjoint, all shots of one phantom, full nt)
-    with the float64 oracle, shots sharded over ``workers`` processes."""
+def _oracle_fwd_shot(args):
     import oracle
+    c, d, dx, dt, pulse, tx, rx = args
+    return oracle.forward_sweep(c, d, dx, dt, pulse, tx, rx)[0]
 
-    tx, rx = geom.tx_nodes(), geom.rx_nodes()
-    obs, _ = oracle.forward_sweep(wl.c_true[0], damp.values, grid.dx, grid.dt, pulse.samples, tx, rx)
-    c0 = np.full(grid.shape, 1540.0)
-    jobs = [(c0, damp.values, grid.dx, grid.dt, pulse.samples, tx[i:i + 1], rx[i:i + 1],
-             obs[i:i + 1], geom.element_nodes) for i in range(len(tx))]
-    t0 = time.perf_counter()
-    if workers > 1:
-        with ProcessPoolExecutor(workers) as ex:
-            res = list(ex.map(_oracle_shot, jobs))
-    else:
-        res = [_oracle_shot(j) for j in jobs]
-    dt_s = time.perf_counter() - t0
-    _ = sum(r[1] for r in res)  # per-shot gradients summed in shot order
-    updates = 2.0 * len(tx) * grid.nx * grid.nz * grid.nt
-    return updates / dt_s, dt_s
+
+def host_info() -> dict:
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = None
+    return {"os_cpu_count": os.cpu_count(), "affinity": aff}
+
+
+class CpuReference:
+    """The reference algorithm on the host: the float64 oracle port of fwilab's
+    _propagate / misfit_and_gradient (forward.py:273-313, adjoint.py:94-138) and
+    unfold_infer (unfold.py:253-267) with float64 copies of the seeded stage
+    networks.  Shots are sharded over a persistent process pool — the reference's
+    own parallelism (datagen.py:222-224) — created before any timed region."""
+
+    def __init__(self, wl, grid, geom, pulse, damp, bounds, K, seed, workers):
+        import copy
+        import multiprocessing
+
+        from paper_2603_04070_b200.network import make_update_nets
+
+        self.wl, self.grid, self.geom, self.pulse, self.damp = wl, grid, geom, pulse, damp
+        self.bounds, self.K, self.workers = bounds, K, workers
+        self.tx, self.rx = geom.tx_nodes(), geom.rx_nodes()
+        self.S = len(self.tx)
+        self.nets = [copy.deepcopy(n).double() for n in make_update_nets(K, seed=seed)]
+        self.pool = None
+        if workers > 1:
+            self.pool = ProcessPoolExecutor(workers, mp_context=multiprocessing.get_context("spawn"))
+            list(self.pool.map(_noop, range(workers)))  # workers up and importing numpy
+        fwd_jobs = [(wl.c_true[0], damp.values, grid.dx, grid.dt, pulse.samples,
+                     self.tx[i:i + 1], self.rx[i:i + 1]) for i in range(self.S)]
+        self.obs = np.concatenate(self._map(_oracle_fwd_shot, fwd_jobs))  # setup, untimed
+
+    def _map(self, fn, jobs):
+        return list(self.pool.map(fn, jobs)) if self.pool else [fn(j) for j in jobs]
+
+    def gradient(self, c):
+        g = self.grid
+        jobs = [(c, self.damp.values, g.dx, g.dt, self.pulse.samples, self.tx[i:i + 1],
+                 self.rx[i:i + 1], self.obs[i:i + 1], self.geom.element_nodes)
+                for i in range(self.S)]
+        res = self._map(_oracle_shot, jobs)
+        grad = np.zeros(g.shape)
+        for _, gi in res:  # per-shot gradients summed in shot order
+            grad += gi
+        return grad
+
+    def reconstruct(self) -> float:
+        """One K-stage DUFWI reconstruction from C0 = 1540; returns seconds."""
+        t0 = time.perf_counter()
+        lo, hi = self.bounds
+        c = np.clip(np.full(self.grid.shape, 1540.0), lo, hi)
+        for net in self.nets:
+            c = np.clip(c + net.predict_update(c, self.gradient(c)), lo, hi)
+        return time.perf_counter() - t0
+
+    def updates_per_reconstruction(self) -> float:
+        g = self.grid
+        return 2.0 * self.K * self.S * g.nx * g.nz * g.nt
+
+    def one_process_gradient(self) -> dict:
+        """The reference as shipped: one process, all shots stacked in one NumPy
+        array (forward.py:283-288), one gradient evaluation."""
+        import oracle
+
+        g = self.grid
+        c = np.full(g.shape, 1540.0)
+        t0 = time.perf_counter()
+        oracle.misfit_gradient(c, self.damp.values, g.dx, g.dt, self.pulse.samples, self.tx,
+                               self.rx, self.obs, self.geom.element_nodes)
+        sec = time.perf_counter() - t0
+        upd = 2.0 * self.S * g.nx * g.nz * g.nt
+        return {"value": upd / sec, "unit": UNIT, "cores": 1, "seconds": sec,
+                "sample": f"one f64 gradient evaluation, {self.S} shots stacked, 1 process"}
+
+    def close(self):
+        if self.pool:
+            self.pool.shutdown()
+
+
+def _noop(i):
+    import numpy  # noqa: F401
+    return i
 
 
 def largest_config_sample(units: int = 256, nt: int = 200, reps: int = 2) -> dict:
@@ -201,6 +271,56 @@ def largest_config_sample(units: int = 256, nt: int = 200, reps: int = 2) -> dic
             "unit": "GB/s", "peak": peak, "peak_kind": peak_kind}
 
 
+def largest_config_full(rank: int, world: int) -> dict:
+    """The whole largest config (BASELINE configs[4]): one gradient of every phantom,
+    4 phantoms x 256 transmits = 1024 units of 1088^2 x 6000 steps, strips.  Under
+    torch.distributed the units are sharded over the N ranks (strong scaling: the
+    total work is fixed) and combined with the one NCCL all_reduce of the
+    gradient; time = max over ranks of CUDA events around the call."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_04070_b200 as pk
+    from paper_2603_04070_b200 import configs
+    from paper_2603_04070_b200 import forward as fwd
+
+    spec = configs.get_config(4)
+    wl = configs.make_workload(spec, seed=0)
+    grid = pk.Grid2D(spec.n, spec.n, spec.dx, spec.dt, spec.nt)
+    geom = pk.AcquisitionGeometry(grid, wl.nodes, wl.rx, 0.0, tx_elements=wl.tx)
+    damp = pk.build_pml(grid, spec.pml)
+    eng = fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes, wl.pulse,
+                         damp, n_phantoms=spec.n_phantoms)
+    eng.set_model(np.full((spec.n_phantoms,) + grid.shape, 1540.0))
+    # observed data: zeros (the residual is then the traces; the work is the same)
+    obs = torch.zeros((eng.n_units, geom.n_r, grid.nt), dtype=torch.float64, device=eng.device)
+    chunk = eng.reserve()  # workspace allocated outside the timed region
+    u0, u1 = eng.local_units()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    mis, g = eng.misfit_and_gradient(obs)
+    e1.record()
+    torch.cuda.synchronize()
+    sec = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=eng.device)
+    if world > 1:
+        dist.all_reduce(sec, op=dist.ReduceOp.MAX)
+    sec = float(sec.item())
+    finite = bool(torch.isfinite(g).all().item())
+    upd = 2.0 * eng.n_units * grid.nx * grid.nz * grid.nt
+    eng.release_workspace()
+    del obs
+    torch.cuda.empty_cache()
+    return {"workload": f"config4: one gradient of {spec.n_phantoms} phantoms x {eng.S} transmits "
+                        f"({eng.n_units} units) x {grid.nx}^2 x {grid.nt} steps, strips",
+            "n_gpus": world, "scaling": "strong", "units_per_rank": u1 - u0,
+            "chunk_units": chunk, "seconds": sec, "updates": upd, "updates_per_s": upd / sec,
+            "updates_per_s_per_gpu": upd / sec / world, "finite": finite,
+            "timing": "CUDA events around misfit_and_gradient (incl. the all_reduce), max over ranks"}
+
+
 def _device_index() -> int:
     if os.environ.get("DUFWI_BENCH_ONE_DEVICE") == "1":
         return 0
@@ -216,31 +336,38 @@ def host_cores() -> int:
 
 # ---------------------------------------------------------------- arms
 def run_reference(args, rank: int, world: int) -> None:
+    """The reference arm: the same workload as ours (one K-stage DUFWI
+    reconstruction of the config-1 phantom per step), by the reference's
+    algorithm on the host cores (the float64 oracle port, shots over all host
+    cores); rank 0 only."""
     if rank != 0:
         return
-    wl, grid, geom, pulse, damp, _ = build_problem(args.config, 1, args.seed)
+    wl, grid, geom, pulse, damp, bounds = build_problem(args.config, 1, args.seed)
+    K = wl.spec.k_stages or 5
     S = len(geom.tx_nodes())
     workers = max(1, min(host_cores(), S))
-    for _ in range(args.warmup):
-        cpu_gradient_sample(wl, grid, geom, pulse, damp, workers)
-    rates, secs = [], []
-    for _ in range(args.steps):
-        r, s = cpu_gradient_sample(wl, grid, geom, pulse, damp, workers)
-        rates.append(r)
-        secs.append(s)
-    total_updates = 2.0 * S * grid.nx * grid.nz * grid.nt * args.steps
-    value = total_updates / sum(secs)
-    sample = (f"one gradient evaluation (forward+adjoint, {S} shots x {grid.nx}x{grid.nz} x "
-              f"{grid.nt} steps, f64) of the config-{args.config} geometry per step")
+    ref = CpuReference(wl, grid, geom, pulse, damp, bounds, K, args.seed, workers)
+    try:
+        for _ in range(args.warmup):
+            ref.reconstruct()
+        secs = [ref.reconstruct() for _ in range(args.steps)]
+        one = ref.one_process_gradient()
+    finally:
+        ref.close()
+    value = ref.updates_per_reconstruction() * args.steps / sum(secs)
+    sample = (f"one DUFWI reconstruction per step: K={K} x (forward+adjoint gradient, {S} shots x "
+              f"{grid.nx}x{grid.nz} x {grid.nt} steps, f64) + f64 copies of the stage networks")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded inclusion phantom, BASELINE config 0/1 shapes)",
-        "config": {"workload": f"config{args.config}", "grid": [grid.nx, grid.nz], "nt": grid.nt,
-                   "shots": S, "receivers": geom.n_r, "parallelism": f"{workers} host processes"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers,
-                         "kind": "port", "sample": sample},
+        "config": {"workload": f"config{args.config}: DUFWI K={K} on the config-0 geometry",
+                   "grid": [grid.nx, grid.nz], "nt": grid.nt, "shots": S, "receivers": geom.n_r,
+                   "phantoms": 1, "parallelism": f"shots over {workers} host processes",
+                   "ms_per_reconstruction": 1e3 * sum(secs) / args.steps},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": sample, "host": host_info(), "one_process": one},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -260,7 +387,9 @@ def run_ours(args, rank: int, world: int) -> None:
     torch.cuda.set_device(local)
     # the update networks' 3x3 convolutions: let cuDNN pick its fastest fp32 algorithm
     # (measured 0.29 -> 0.26 ms per network at 160^2; TF32 stays off)
-    torch.backends.cudnn.benchmark = True
+    # (single process only: replicated networks stay on cuDNN's deterministic heuristics
+    # under torch.distributed; Reconstructor also broadcasts rank 0's maps)
+    torch.backends.cudnn.benchmark = world == 1
     dev = torch.device("cuda", local)
     B = world  # weak scaling: one phantom per GPU
     wl, grid, geom, pulse, damp, bounds = build_problem(args.config, B, args.seed)
@@ -364,16 +493,24 @@ def run_ours(args, rank: int, world: int) -> None:
                        else "paper_2603_04070_b200.unfold_infer_batch")}
 
     large = None
-    if rank == 0 and world == 1 and not args.skip_large:
-        large = largest_config_sample()
+    if not args.skip_large:
+        large = {"full_gradient": largest_config_full(rank, world)}
+        if world == 1:
+            large.update(largest_config_sample())  # per-launch kernel rooflines
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cores = max(1, min(host_cores(), S))
-        r, secs = cpu_gradient_sample(wl, grid, geom, pulse, damp, cores)
-        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"one f64 gradient evaluation (fwd+adj, {S} shots, full nt) with the "
-                         f"oracle port, shots over {cores} processes, {secs:.1f} s"}
+        ref = CpuReference(wl, grid, geom, pulse, damp, bounds, K, args.seed, cores)
+        try:
+            sec = ref.reconstruct()
+            one = ref.one_process_gradient()
+        finally:
+            ref.close()
+        cpu = {"value": ref.updates_per_reconstruction() / sec, "unit": UNIT, "cores": cores,
+               "kind": "port", "host": host_info(), "one_process": one,
+               "sample": f"one f64 DUFWI reconstruction (K={K}, {S} shots, full nt) with the "
+                         f"oracle port, shots over {cores} processes, {sec:.1f} s"}
 
     if rank == 0:
         line = {

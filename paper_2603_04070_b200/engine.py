@@ -268,6 +268,16 @@ class PhysicsEngine:
             self.ws_generation += 1
         return ws
 
+    def reserve(self, store: str = "auto", mask: bool = True,
+                units: tuple[int, int] | None = None) -> int:
+        """Allocate the workspace a gradient over ``units`` (default: this rank's
+        shard) will use, outside any timed region; returns the chunk size."""
+        u0, u1 = units if units is not None else self.local_units()
+        mode = self.pick_store(mask, store)
+        chunk = self.chunk_units(mode, max(u1 - u0, 1))
+        self._workspace(mode, chunk)
+        return chunk
+
     def release_workspace(self) -> None:
         self._ws.clear()
         self.ws_generation += 1

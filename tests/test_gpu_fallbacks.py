@@ -63,7 +63,9 @@ def test_stepwise_family_vs_oracle(gpu, name):
     tx, rx = geom.tx_nodes(), geom.rx_nodes()
     obs, _ = oracle.forward_sweep(wl.c_true[0], damp.values, grid.dx, grid.dt, pulse.samples, tx,
                                   rx, rho=rho)
-    c0 = np.full(grid.shape, 1540.0)
+    # trial model 20 m/s below the background: residual/trace L2 3.7% (config 0: 1.3%);
+    # a 1540 start leaves 5e-4, where f32 storage rounding alone exceeds 1e-4
+    c0 = np.full(grid.shape, 1520.0)
     m_ref, g_ref, tr_ref = oracle.misfit_gradient(c0, damp.values, grid.dx, grid.dt, pulse.samples,
                                                   tx, rx, obs, geom.element_nodes, rho=rho)
     eng = fwd.get_engine(grid, tx, rx, geom.element_nodes, pulse.samples, damp,
