@@ -125,6 +125,8 @@ def dufwi_case(cfg: int, n_phantoms: int, out_name: str, key: str, meta):
     nets, wsha = nets_f64(spec.k_stages, seed=0)
     upd = [lambda c, g, n=n: n.predict_update(c, g) for n in nets]
     t0 = time.time()
+    S = len(tx)
+    sel_dec = np.array([0, S // 2, S - 1])  # transmits whose decimated traces are kept
     grads, maps, obs_dec, info = [], [], [], []
     for b in range(n_phantoms):
         rho = wl.rho[b] if wl.rho is not None else None
@@ -134,13 +136,13 @@ def dufwi_case(cfg: int, n_phantoms: int, out_name: str, key: str, meta):
                                        wl.nodes, rho=rho)
         grads.append(np.stack(gk).astype(np.float32))
         maps.append(np.stack(mk).astype(np.float32))
-        obs_dec.append(obs[:, :, ::DEC].astype(np.float32))
+        obs_dec.append(obs[sel_dec, :, ::DEC].astype(np.float32))
         info.append({"obs_sha256_f64": sha(obs), "final_sha256_f64": sha(mk[-1]),
                      "update_absmax": [float(np.abs(mk[i] - (mk[i - 1] if i else np.clip(c0, *bounds))).max())
                                        for i in range(len(mk))]})
         print(f"[{key}] phantom {b} done {time.time() - t0:.0f}s", flush=True)
     np.savez_compressed(OUT / out_name, grads=np.stack(grads), maps=np.stack(maps),
-                        obs_dec=np.stack(obs_dec), bounds=np.asarray(bounds))
+                        obs_dec=np.stack(obs_dec), obs_dec_shots=sel_dec, bounds=np.asarray(bounds))
     meta[key] = {"config": cfg, "phantoms": list(range(n_phantoms)), "K": spec.k_stages,
                  "net_seed": 0, "net_weights_sha256_f32": wsha, "bounds": list(bounds),
                  "per_phantom": info, "seconds": time.time() - t0}

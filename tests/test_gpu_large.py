@@ -127,8 +127,9 @@ def _dufwi(gpu, cfg, key, name, n_phantoms):
     assert bounds == pk.cfl_safe_bounds(grid, (1300.0, 3200.0))
     eng.set_model(wl.c_true, wl.rho)
     own = eng.forward().double()
-    o = own.cpu().numpy()[:, :, ::DEC]
-    assert rel_l2(o, z["obs_dec"].reshape(o.shape)) <= TOL
+    S = geom.n_p
+    o = own.cpu().numpy().reshape(n_phantoms, S, geom.n_r, -1)[:, z["obs_dec_shots"], :, ::DEC]
+    assert rel_l2(o, z["obs_dec"]) <= TOL
     rec = Reconstructor(eng, nets, bounds, rho=None if wl.rho is None else torch.as_tensor(wl.rho).to(gpu))
     c0 = torch.full((n_phantoms,) + grid.shape, 1540.0, dtype=torch.float64, device=gpu)
     maps, grads = rec.reconstruct(own, c0, keep_gradients=True)
