@@ -46,6 +46,10 @@ extern "C" {
 #define DUFWI_STORE_FULL 1   /* full f32 history [nt][units][nx][nz] in workspace  */
 #define DUFWI_STORE_STRIPS 2 /* 1-cell ring around the undamped box per step + the
                                 last two states; interior reconstructed backwards */
+#define DUFWI_STORE_LAP 4  /* cluster engine: the forward stores L(u[t]) of every cell
+                              of the undamped box and step (f32), the imaging operand, so
+                              the adjoint carries only lam: no u state, no reconstruction
+                              (masked gradients, like STRIPS) */
 #define DUFWI_STORE_CHECKPOINT 3 /* snapshots (u[s0-1], u[s0-2]) every K = ceil(sqrt(2 nt))
                                     steps; the adjoint recomputes each segment's fields
                                     from its snapshot (any damping; bit-identical to FULL) */

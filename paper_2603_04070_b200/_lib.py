@@ -13,12 +13,12 @@ import os
 from pathlib import Path
 
 __all__ = ["LIB_PATH", "ExtensionUnavailable", "DufwiError", "Geometry", "lib", "check",
-           "EXPORTED_SYMBOLS", "STORE_NONE", "STORE_FULL", "STORE_STRIPS", "STORE_CHECKPOINT",
+           "EXPORTED_SYMBOLS", "STORE_NONE", "STORE_FULL", "STORE_STRIPS", "STORE_CHECKPOINT", "STORE_LAP",
            "ENGINE_AUTO", "ENGINE_STEPWISE", "ENGINE_CLUSTER"]
 
 LIB_PATH = Path(os.environ.get("DUFWI_LIB", Path(__file__).resolve().parent / "libdufwi.so"))
 
-STORE_NONE, STORE_FULL, STORE_STRIPS, STORE_CHECKPOINT = 0, 1, 2, 3
+STORE_NONE, STORE_FULL, STORE_STRIPS, STORE_CHECKPOINT, STORE_LAP = 0, 1, 2, 3, 4
 ENGINE_AUTO, ENGINE_STEPWISE, ENGINE_CLUSTER = 0, 1, 2
 
 EXPORTED_SYMBOLS = (

@@ -193,7 +193,8 @@ Layout layout(const dufwi_plan_t* p, int mode, int U) {
   L.mis = take((size_t)U * kResidualSplit * sizeof(double));
   L.rec = take((size_t)g.nt * U * g.M * sizeof(float));
   L.ubuf = take(2 * (size_t)U * N2 * sizeof(float));
-  if (mode == DUFWI_STORE_FULL) L.hist = take((size_t)g.nt * U * N2 * sizeof(float));
+  if (mode == DUFWI_STORE_FULL || mode == DUFWI_STORE_LAP)
+    L.hist = take((size_t)g.nt * U * N2 * sizeof(float));
   if (mode == DUFWI_STORE_STRIPS) L.strips = take((size_t)g.nt * U * g.SL * sizeof(float));
   if (mode == DUFWI_STORE_CHECKPOINT) {
     // snapshots (u[s0-1], u[s0-2]) of every segment start + one segment's history
@@ -467,7 +468,7 @@ extern "C" int dufwi_set_model(dufwi_plan_t* p, const double* c_dev, const doubl
 extern "C" int dufwi_workspace_bytes(const dufwi_plan_t* p, int32_t mode, int32_t U,
                                      size_t* bytes_out) {
   if (!p || !bytes_out) return fail(DUFWI_EINVAL, "null argument");
-  if (mode < 0 || mode > 3) return fail(DUFWI_EINVAL, "bad store mode");
+  if (mode < 0 || mode > 4) return fail(DUFWI_EINVAL, "bad store mode");
   if (U <= 0) return fail(DUFWI_EINVAL, "unit_count must be positive");
   *bytes_out = layout(p, mode, U).total;
   return DUFWI_OK;
@@ -481,6 +482,12 @@ int ws_check(const dufwi_plan_t* p, int mode, int unit_begin, int U, size_t ws_b
   if (ws_bytes < L.total) return fail(DUFWI_EINVAL, "workspace too small");
   if (mode == DUFWI_STORE_STRIPS && !p->box_ok)
     return fail(DUFWI_EINVAL, "strip storage needs a rectangular undamped box");
+  if (mode == DUFWI_STORE_LAP && (!p->cluster_ok || p->engine == DUFWI_ENGINE_STEPWISE))
+    return fail(DUFWI_EINVAL, "L(u) history storage needs the cluster engine");
+  if (mode == DUFWI_STORE_LAP && !p->box_ok)
+    return fail(DUFWI_EINVAL, "L(u) history storage needs a rectangular undamped box");
+  if (mode == DUFWI_STORE_LAP && p->geo.nz % 4 != 0)
+    return fail(DUFWI_EINVAL, "L(u) history storage needs nz % 4 == 0 (16-byte bulk copies)");
   return 0;
 }
 
@@ -630,7 +637,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
                              float* traces_dev, int32_t* nonfinite_dev, void* ws, size_t ws_bytes,
                              void* stream) {
   if (!p || !ws) return fail(DUFWI_EINVAL, "null argument");
-  if (mode < 0 || mode > 3) return fail(DUFWI_EINVAL, "bad store mode");
+  if (mode < 0 || mode > 4) return fail(DUFWI_EINVAL, "bad store mode");
   int rc = check_units(p, unit_begin, U);
   if (rc) return rc;
   Layout L;
@@ -653,7 +660,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   if (use_cluster(p, mode)) {
     p->last_engine = DUFWI_ENGINE_CLUSTER;
     rc = cluster_forward(g, m, pick_cluster(p->ccands, U), mode, unit_begin, U, rec,
-                         mode == DUFWI_STORE_FULL ? hist : nullptr,
+                         (mode == DUFWI_STORE_FULL || mode == DUFWI_STORE_LAP) ? hist : nullptr,
                          mode == DUFWI_STORE_STRIPS ? strips : nullptr, ubuf, st);
     if (rc) return fail(DUFWI_ECUDA, std::string("cluster forward: ") + cudaGetErrorString((cudaError_t)rc));
     ++p->launches;
@@ -730,8 +737,9 @@ extern "C" int dufwi_residual(dufwi_plan_t* p, int32_t unit_begin, int32_t U,
 extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, int32_t U,
                              void* ws, size_t ws_bytes, double* acc_dev, void* stream) {
   if (!p || !ws || !acc_dev) return fail(DUFWI_EINVAL, "null argument");
-  if (mode != DUFWI_STORE_FULL && mode != DUFWI_STORE_STRIPS && mode != DUFWI_STORE_CHECKPOINT)
-    return fail(DUFWI_EINVAL, "adjoint needs FULL, STRIPS or CHECKPOINT history");
+  if (mode != DUFWI_STORE_FULL && mode != DUFWI_STORE_STRIPS && mode != DUFWI_STORE_CHECKPOINT &&
+      mode != DUFWI_STORE_LAP)
+    return fail(DUFWI_EINVAL, "adjoint needs FULL, STRIPS, CHECKPOINT or LAP history");
   int rc = check_units(p, unit_begin, U);
   if (rc) return rc;
   Layout L;
@@ -759,7 +767,7 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     // per-unit accumulators: with one shot per group, group index == chunk-local unit
     const int acc_off = 0;
     rc = cluster_adjoint(g, m, pick_cluster(p->ccands, U, true), mode, unit_begin, U, rres,
-                         mode == DUFWI_STORE_FULL ? hist : nullptr,
+                         (mode == DUFWI_STORE_FULL || mode == DUFWI_STORE_LAP) ? hist : nullptr,
                          mode == DUFWI_STORE_STRIPS ? strips : nullptr, ubuf, acc_part, acc_off,
                          st);
     if (rc) return fail(DUFWI_ECUDA, std::string("cluster adjoint: ") + cudaGetErrorString((cudaError_t)rc));

@@ -62,6 +62,8 @@ struct ClusterCfg {
   int maxring = 0;  // ring-strip cells per CTA (upper bound) staged in shared memory
   int maxc = 0;     // clusters co-resident on the device (one wave)
   size_t smem_fwd = 0, smem_adj = 0;
+  size_t smem_lap = 0;     // adjoint over the L(u) history (DUFWI_STORE_LAP)
+  size_t smem_fwdlap = 0;  // forward storing it (staging slots)
 };
 
 // Receiver samples / ring strips / residuals move between HBM and the step loop
@@ -504,6 +506,107 @@ struct StepBufs {
   uint32_t wb, bar_r, bar_w, bar_wb;
 };
 
+// ---- L(u) history transport (DUFWI_STORE_LAP; the adjoint kernel is below)
+constexpr int kLapDepth = 4;  // adjoint ring slots
+constexpr int kLapStage = 3;  // forward staging slots
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// The CTA's rows inside the undamped box: [b0, b0 + nb) (nb <= 0: none).
+struct BoxRows {
+  int b0, nb;
+};
+__device__ __forceinline__ BoxRows box_rows(const Geo& g, const CellCtx& c) {
+  BoxRows r;
+  r.b0 = max(c.r0, g.x_lo);
+  r.nb = min(c.r0 + c.nr - 1, g.x_hi) - r.b0 + 1;
+  return r;
+}
+
+// Forward staging (MODE 3): kLapStage slots of rows x nz floats after the IO stage.
+template <class T>
+__host__ __device__ inline size_t lap_stage_offset(int rows, int rpt, int nz, int maxrec,
+                                                   int maxring) {
+  return al16(io_offset<T>(rows, rpt, nz, 2) + io_bytes(maxrec, maxring));
+}
+template <class T>
+__host__ __device__ inline size_t cluster_fwdlap_smem_bytes(int rows, int rpt, int nz, int maxrec,
+                                                            int maxring) {
+  return lap_stage_offset<T>(rows, rpt, nz, maxrec, maxring) + (size_t)kLapStage * rows * nz * 4;
+}
+// Adjoint ring: kLapDepth mbarriers (32 B) then kLapDepth slots of rows x nz floats.
+template <class T>
+__host__ __device__ inline size_t lap_ring_offset(int rows, int rpt, int nz, int maxrec) {
+  return al16(io_offset<T>(rows, rpt, nz, 2) + io_bytes(maxrec, 0));
+}
+template <class T>
+__host__ __device__ inline size_t cluster_lap_smem_bytes(int rows, int rpt, int nz, int maxrec) {
+  return lap_ring_offset<T>(rows, rpt, nz, maxrec) + 32 + (size_t)kLapDepth * rows * nz * 4;
+}
+
+// Forward, thread 0 after the step barrier of step t: write the staging slot of
+// step t-1 (slot (t-2) % 3, holding L(u[t-2])) to history slot t-2.  Slot
+// reuse: step t writes slot (t-1) % 3, whose last bulk read was issued at step
+// t-2 and completed by this thread's wait_group.read<1> at step t-1.
+__device__ __forceinline__ void lap_store(const Geo& g, const BoxRows& br, int rows, int t,
+                                          uint32_t stage_sa, float* hbox, size_t hstep) {
+  if (threadIdx.x == 0 && br.nb > 0 && t >= 2) {
+    const uint32_t slot = stage_sa + (uint32_t)(((t - 2) % kLapStage) * rows * g.nz) * 4u;
+    bulk_s2g(hbox + (size_t)(t - 2) * hstep, slot, (uint32_t)(br.nb * g.nz) * 4u);
+    bulk_commit();
+    bulk_wait_read<1>();
+  }
+}
+
+// Adjoint, thread 0: bulk load of step j's operand L(u[t-1]) (t = nt-1-j) into
+// ring slot j % depth, completing on that slot's mbarrier.
+__device__ __forceinline__ void lap_load(const Geo& g, const BoxRows& br, int rows, int j,
+                                         uint32_t ring_sa, uint32_t ringbar, const float* hbox,
+                                         size_t hstep) {
+  if (br.nb > 0 && j <= g.nt - 2) {
+    const int sl = j % kLapDepth;
+    const uint32_t bytes = (uint32_t)(br.nb * g.nz) * 4u;
+    const uint32_t bar = ringbar + 8u * (uint32_t)sl;
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(ring_sa + (uint32_t)(sl * rows * g.nz) * 4u, hbox + (size_t)(g.nt - 2 - j) * hstep,
+             bytes, bar);
+  }
+}
+
+// Forward side of a CTA: its box rows, staging slots and history base.
+struct LapFwd {
+  BoxRows br;
+  uint32_t stage_sa;
+  float* hbox;
+  size_t hstep;
+};
+
 // One forward step of a thread's cells (u1 = u[t-1] -> u2 := u[t]).  FULL:
 // every row slot active (no per-row predicates); PLAIN: undamped cells of the
 // box (A = 2, B = -1); IO: a PLAIN thread may hold the source (receivers are
@@ -519,12 +622,17 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
   const T* pp = pc + c.RS;
   double v[RPT];
   const double2 ab0 = (!PLAIN && UNIF) ? s.ab[0] : make_double2(2.0, -1.0);
+  // MODE 3: the step's L(u[t-1]) (5-point sum, f32) of the box cells into the
+  // shared-memory staging slot of step t (`hist`: the thread's first cell there),
+  // written to history slot t-1 by one bulk copy after the next step barrier
+  float* hl = hist;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const double xm = j > 0 ? u1[j - 1] : (double)pc[-1];
     const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
     const double xp = own_next ? u1[j + 1] : (double)pc[j + 1];
     const double lap = lap5(u1[j], xm, xp, (double)pm[j], (double)pp[j]);
+    if (MODE == 3 && t >= 1 && (PLAIN || ((s.interior >> j) & 1u))) hl[j * g.nz] = (float)lap;
     if (PLAIN) {
       v[j] = fwd_update_free(u1[j], u2[j], s.ed[j], lap);
     } else {
@@ -546,6 +654,7 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
     if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = (float)v[j];
   }
   push_edges<RPT, T>(c, s, B.wb, B.bar_wb, v, FULL);
+  if (MODE == 3) fence_proxy_async();  // the staged values are read by the bulk copy
 }
 
 // Receiver samples / ring cells of step t, read back from the exchange buffer
@@ -606,11 +715,13 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
                                          int lu, const StepBufs<T>& B, uint32_t tx_bytes,
                                          double pulse_t, const IoStage& io, int nrec, int nio,
                                          float* __restrict__ rec, float* __restrict__ strips,
-                                         float* __restrict__ hist, size_t N2, int grank) {
+                                         float* __restrict__ hist, size_t N2, int grank,
+                                         const LapFwd& lap) {
 #ifdef DUFWI_EXP_TIMING
   const long long T0 = clock64();
 #endif
   step_sync(c, t, B.bar_r, B.bar_w, tx_bytes);
+  if (MODE == 3) lap_store(g, lap.br, c.rows, t, lap.stage_sa, lap.hbox, lap.hstep);
   if (t >= 1) {
     io_gather<T, MODE>(io, nrec, nio, B.r, t - 1, grank);
     if (t % kStage == 0) flush_stage<MODE>(g, io, t - kStage, kStage, U, lu, rec, strips);
@@ -682,22 +793,43 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const uint32_t xb1 = (uint32_t)(xe * sizeof(T));
   const StepBufs<T> B0{X[1], X[0], 0u, bar[1], bar[0], bar_off};
   const StepBufs<T> B1{X[0], X[1], xb1, bar[0], bar[1], bar_off + 8u};
+  // MODE 3: staging slots of the box rows' L(u), written out by thread 0
+  LapFwd lap{};
+  float* stage = nullptr;
+  int lofs = 0;
+  const int slotf = rows * g.nz;
+  if (MODE == 3) {
+    lap.br = box_rows(g, c);
+    const size_t so = lap_stage_offset<T>(rows, RPT, g.nz, maxrec, maxring);
+    stage = reinterpret_cast<float*>(smem + so);
+    lap.stage_sa = smem_addr(stage);
+    lap.hstep = (size_t)U * N2;
+    lap.hbox = hist + (size_t)lu * N2 + (size_t)max(lap.br.b0, 0) * g.nz;
+    lofs = (c.r0 + c.lrow0 - lap.br.b0) * g.nz + c.z;  // slots start at box row b0
+  }
+  // the thread's cell in the staging slot of step t (MODE 3), else the history
+#define DUFWI_HS(t) (MODE == 3 ? stage + (size_t)(((t) + kLapStage - 1) % kLapStage) * slotf + lofs : hist)
   int t = 0;
   for (; t + 1 < g.nt; t += 2) {
     double p = p_next;
     if (owns_src) p_next = g.pulse[t + 1];
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p, io, nrec, nio, rec,
-                           strips, hist, N2, grank);
+                           strips, DUFWI_HS(t), N2, grank, lap);
     p = p_next;
     if (owns_src && t + 2 < g.nt) p_next = g.pulse[t + 2];
     fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, B1, tx_bytes, p, io, nrec, nio, rec,
-                           strips, hist, N2, grank);
+                           strips, DUFWI_HS(t + 1), N2, grank, lap);
   }
   if (t < g.nt)
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p_next, io, nrec, nio, rec,
-                           strips, hist, N2, grank);
+                           strips, DUFWI_HS(t), N2, grank, lap);
+#undef DUFWI_HS
   // the last step's samples, then the partial stage
   __syncthreads();
+  if (MODE == 3) {  // the last step's L(u[nt-2]); every store complete before exit
+    lap_store(g, lap.br, rows, g.nt, lap.stage_sa, lap.hbox, lap.hstep);
+    if (threadIdx.x == 0) bulk_wait<0>();
+  }
   io_gather<T, MODE>(io, nrec, nio, X[(g.nt - 1) & 1], g.nt - 1, gather_rank());
   {
     const int t0 = (g.nt - 1) / kStage * kStage;
@@ -707,7 +839,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   if (c.has_up || c.has_dn) mbar_wait(bar[(g.nt - 1) & 1], ((g.nt - 1) >> 1) & 1);
   cluster_sync_all();
 
-  if (MODE != 1) {
+  if (MODE == 0 || MODE == 2) {
     // final two states in the stepwise-engine layout: ubuf[t & 1][lu] holds u[t]
     const bool last_odd = ((g.nt - 1) & 1) != 0;
     float* d_last = ubuf + ((size_t)((g.nt - 1) & 1) * U + lu) * N2;
@@ -1009,6 +1141,180 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
     if (st.active & (1u << j)) dst[(size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = acc[j];
 }
 
+// ---------------------------------------------------------------------------
+// L(u) history (DUFWI_STORE_LAP).  The forward stores L(u[t-1]) of every
+// undamped-box cell and step (f32, 4 B per cell update: the masked gradient
+// only needs the box, like the strips store), so the reverse sweep carries only
+// lam: per step the lam update with its E*lam exchange, the residual at
+// receivers, and acc += L(u[t-1]) * lam.  No u state, no backward
+// reconstruction, no second exchange buffer or push.
+//
+// Both directions move a CTA's box rows of a step as ONE contiguous bulk copy
+// issued by one thread (the rows of a slab are contiguous in the [x][z]
+// layout): the forward stages L(u) in shared memory and writes it with
+// cp.async.bulk (shared -> global, bulk groups); the adjoint prefetches
+// kLapDepth steps ahead with cp.async.bulk (global -> shared) completing on a
+// per-slot mbarrier.  No per-thread global address arithmetic in the step.
+template <int RPT, class T, bool FULL, bool PLAIN, bool UNIF, bool IO, bool IMG>
+__device__ __forceinline__ void adjlap_body(const CellCtx& c, const CellStatic<RPT>& s,
+                                            double (&l1)[RPT], double (&l2)[RPT],
+                                            double (&acc)[RPT], int i, const AdjBufs<T>& B,
+                                            const IoStage& io, const float* lr, int nz) {
+  const int RS = c.RS;
+  const int k = i % kStage;
+  double el[RPT], lam[RPT];
+  const double2 ab0 = (!PLAIN && UNIF) ? s.ab[0] : make_double2(2.0, -1.0);
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
+  const T* pc = B.lr + c.xo;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const double xm = j > 0 ? el[j - 1] : (double)pc[-1];
+    const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
+    const double xp = own_next ? el[j + 1] : (double)pc[j + 1];
+    const double adj = lap5(el[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
+    if (PLAIN) {
+      lam[j] = adj_update_free(l1[j], l2[j], adj);
+    } else {
+      const double2 ab = UNIF ? ab0 : s.ab[j];
+      lam[j] = adj_update(ab.x, ab.y, l1[j], l2[j], adj);
+    }
+  }
+  if ((!PLAIN || IO) && s.rmask) {
+    const double* r = io.srec + (size_t)k * io.maxrec + s.rbase;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) lam[j] = __dadd_rn(lam[j], r[j]);
+  }
+  T* ql = B.lw + c.xo;
+  double elw[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    elw[j] = __dmul_rn(s.ed[j], lam[j]);
+    if (!FULL && !(s.active & (1u << j))) continue;
+    l2[j] = lam[j];
+    ql[j] = (T)elw[j];
+    if (IMG && (PLAIN || ((s.interior >> j) & 1u)))
+      acc[j] = __fma_rn((double)lr[j * nz], lam[j], acc[j]);
+  }
+  push_edges<RPT, T>(c, s, B.lwb, B.bar_wb, elw, FULL);
+}
+
+template <int RPT, class T, bool IMG>
+__device__ __forceinline__ void adjlap_step(const Geo& g, const CellCtx& c,
+                                            const CellStatic<RPT>& s, double (&l1)[RPT],
+                                            double (&l2)[RPT], double (&acc)[RPT], int i,
+                                            const AdjBufs<T>& B, uint32_t tx_bytes,
+                                            const IoStage& io, const BoxRows& br, int rows,
+                                            const float* ring, uint32_t ring_sa, uint32_t ringbar,
+                                            const float* hbox, size_t hstep, int lofs) {
+#ifdef DUFWI_EXP_TIMING
+  const long long T0 = clock64();
+#endif
+  step_sync(c, i, B.bar_r, B.bar_w, tx_bytes);
+  // every thread is past step i-1: its ring slot is free for step i-1+depth
+  if (threadIdx.x == 0 && i >= 1) lap_load(g, br, rows, i - 1 + kLapDepth, ring_sa, ringbar, hbox, hstep);
+  const int sl = i % kLapDepth;
+  if (IMG && br.nb > 0) mbar_wait(ringbar + 8u * (uint32_t)sl, (uint32_t)(i / kLapDepth) & 1u);
+#ifdef DUFWI_EXP_TIMING
+  const long long T1 = clock64();
+#endif
+  const float* lr = ring + (size_t)sl * rows * g.nz + lofs;
+  if (s.fast)
+    adjlap_body<RPT, T, true, true, false, false, IMG>(c, s, l1, l2, acc, i, B, io, lr, g.nz);
+  else if (s.plainio)
+    adjlap_body<RPT, T, true, true, false, true, IMG>(c, s, l1, l2, acc, i, B, io, lr, g.nz);
+  else if (s.unif)
+    adjlap_body<RPT, T, true, false, true, true, IMG>(c, s, l1, l2, acc, i, B, io, lr, g.nz);
+  else if (s.full)
+    adjlap_body<RPT, T, true, false, false, true, IMG>(c, s, l1, l2, acc, i, B, io, lr, g.nz);
+  else
+    adjlap_body<RPT, T, false, false, false, true, IMG>(c, s, l1, l2, acc, i, B, io, lr, g.nz);
+#ifdef DUFWI_EXP_TIMING
+  dbg_step(1, T0, T1, s.fast ? 0 : s.plainio ? 5 : s.unif ? 3 : s.full ? 1 : 2);
+#endif
+}
+
+template <int RPT, class T>
+__global__ void __maxnreg__(cluster_max_regs(RPT))
+    cluster_adjlap_kernel(Geo g, Model m, int cs, int rows, int maxrec, int unit_begin, int U,
+                          const double* __restrict__ rres, const float* __restrict__ hlap,
+                          double* __restrict__ acc_part, int acc_off) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  CellCtx c = make_ctx(cs, rows, g.nx, g.nz, RPT, smem);
+  const int lu = blockIdx.x / cs;
+  const int u = unit_begin + lu;
+  const int b = u / g.S;
+  const int s = u - b * g.S;
+  const int txx = g.tx[2 * s], txz = g.tx[2 * s + 1];
+  const size_t N2 = (size_t)g.nx * g.nz;
+  const size_t pb = (size_t)b * N2;
+  const size_t xe = xbuf_elems(rows, RPT, g.nz);
+  T* XL[2] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem) + xe};
+  const uint32_t bar_off = (uint32_t)bar_offset<T>(rows, RPT, g.nz, 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
+  const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
+  order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem), RPT, DUFWI_PLACE_ADJ);
+  for (size_t k = threadIdx.x; k < 2 * xe; k += blockDim.x) XL[0][k] = T(0);
+  const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 2), maxrec, 0);
+  unsigned char* rbase = smem + lap_ring_offset<T>(rows, RPT, g.nz, maxrec);
+  const uint32_t ringbar = smem_addr(rbase);
+  const float* ring = reinterpret_cast<const float*>(rbase + 32);
+  const uint32_t ring_sa = smem_addr(ring);
+  const BoxRows br = box_rows(g, c);
+  const size_t hstep = (size_t)U * N2;
+  const float* hbox = hlap + (size_t)lu * N2 + (size_t)max(br.b0, 0) * g.nz;
+  if (threadIdx.x == 0) {
+    mbar_init(bar[0], 1);
+    mbar_init(bar[1], 1);
+    for (int d = 0; d < kLapDepth; ++d) mbar_init(ringbar + 8u * d, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    io.counts[0] = io.counts[1] = 0;
+    for (int d = 0; d < kLapDepth; ++d) lap_load(g, br, rows, d, ring_sa, ringbar, hbox, hstep);
+  }
+  __syncthreads();
+  CellStatic<RPT> st;
+  load_static<RPT>(g, m, c, pb, txx, txz,
+                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)), io, true,
+                   st);
+  const uint32_t tx_bytes = (uint32_t)(((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T));
+  const int nt = g.nt;
+  // the thread's first cell in a ring slot (slots hold the box rows from b0)
+  const int lofs = (c.r0 + c.lrow0 - br.b0) * g.nz + c.z;
+  double la[RPT], lb[RPT], acc[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) la[j] = lb[j] = acc[j] = 0.0;
+  cluster_sync_all();
+
+  const uint32_t xsz = (uint32_t)(xe * sizeof(T));
+  const AdjBufs<T> B0{XL[1], XL[0], nullptr, nullptr, 0u, 0u, bar[1], bar[0], bar_off};
+  const AdjBufs<T> B1{XL[0], XL[1], nullptr, nullptr, xsz, 0u, bar[0], bar[1], bar_off + 8u};
+#define DUFWI_ADJLAP(IMG, L1, L2, BB, I)                                                          \
+  adjlap_step<RPT, T, IMG>(g, c, st, L1, L2, acc, I, BB, tx_bytes, io, br, rows, ring, ring_sa,   \
+                           ringbar, hbox, hstep, lofs)
+  int i = 0;
+  for (; i + 1 < nt - 1; i += 2) {  // steps with t >= 1: imaging
+    if (i % kStage == 0) prefetch_stage<1>(g, io, i, U, lu, rres, nullptr);
+    DUFWI_ADJLAP(true, la, lb, B0, i);
+    DUFWI_ADJLAP(true, lb, la, B1, i + 1);
+  }
+  for (; i < nt; ++i) {
+    if (i % kStage == 0) prefetch_stage<1>(g, io, i, U, lu, rres, nullptr);
+    const bool img = nt - 1 - i >= 1;
+    if (i & 1) {
+      if (img) DUFWI_ADJLAP(true, lb, la, B1, i); else DUFWI_ADJLAP(false, lb, la, B1, i);
+    } else {
+      if (img) DUFWI_ADJLAP(true, la, lb, B0, i); else DUFWI_ADJLAP(false, la, lb, B0, i);
+    }
+  }
+#undef DUFWI_ADJLAP
+  if (c.has_up || c.has_dn) mbar_wait(bar[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
+  cluster_sync_all();
+  double* dst = acc_part + (size_t)(lu + acc_off) * N2;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j)
+    if (st.active & (1u << j)) dst[(size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = acc[j];
+}
+
 // ------------------------------------------------------------------ host side
 template <class K>
 inline int max_active_clusters(K kernel, int cs, int threads, size_t smem) {
@@ -1087,11 +1393,15 @@ inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, 
   const size_t sf = cluster_smem_bytes<T>(rows, RPT, g.nz, 2, maxrec, maxring);
   const size_t sa = cluster_smem_bytes<T>(rows, RPT, g.nz, 4, maxrec, maxring);
   // clusters co-resident on the device: the least over the sweep kernels
+  const size_t sl = cluster_lap_smem_bytes<T>(rows, RPT, g.nz, maxrec);
+  const size_t sf3 = cluster_fwdlap_smem_bytes<T>(rows, RPT, g.nz, maxrec, maxring);
   int n = max_active_clusters(cluster_fwd_kernel<RPT, T, 0>, cs, threads, sf);
   n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 1>, cs, threads, sf));
   n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 2>, cs, threads, sf));
+  n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 3>, cs, threads, sf3));
   n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 1>, cs, threads, sa));
   n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 2>, cs, threads, sa));
+  n = std::min(n, max_active_clusters(cluster_adjlap_kernel<RPT, T>, cs, threads, sl));
   if (n <= 0) return false;
   out->cs = cs;
   out->rows = rows;
@@ -1101,6 +1411,8 @@ inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, 
   out->dbl = sizeof(T) == 8;
   out->smem_fwd = sf;
   out->smem_adj = sa;
+  out->smem_lap = sl;
+  out->smem_fwdlap = sf3;
   out->maxrec = maxrec;
   out->maxring = maxring;
   out->maxc = n;
@@ -1241,6 +1553,9 @@ inline cudaError_t cluster_forward_t(const Geo& g, const Model& m, const Cluster
   if (mode == 1)
     return launch_cluster(cluster_fwd_kernel<RPT, T, 1>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
                           c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
+  if (mode == 4)  // DUFWI_STORE_LAP: hist receives L(u[t]) (kernel MODE 3)
+    return launch_cluster(cluster_fwd_kernel<RPT, T, 3>, c, U, c.smem_fwdlap, st, g, m, c.cs, c.rows,
+                          c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
   return launch_cluster(cluster_fwd_kernel<RPT, T, 2>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
                         c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
 }
@@ -1250,6 +1565,9 @@ inline cudaError_t cluster_adjoint_t(const Geo& g, const Model& m, const Cluster
                                      int unit_begin, int U, const double* rres, const float* hist,
                                      const float* strips, const float* ubuf, double* acc_part,
                                      int acc_off, cudaStream_t st) {
+  if (mode == 4)
+    return launch_cluster(cluster_adjlap_kernel<RPT, T>, c, U, c.smem_lap, st, g, m, c.cs, c.rows,
+                          c.maxrec, unit_begin, U, rres, hist, acc_part, acc_off);
   if (mode == 1)
     return launch_cluster(cluster_adj_kernel<RPT, T, 1>, c, U, c.smem_adj, st, g, m, c.cs, c.rows,
                           c.maxrec, c.maxring, unit_begin, U, rres, hist, strips, ubuf, acc_part, acc_off);

@@ -18,16 +18,17 @@ sm_100a kernels of ``libdufwi.so``.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _lib
-from ._lib import STORE_CHECKPOINT, STORE_FULL, STORE_NONE, STORE_STRIPS, check
+from ._lib import STORE_CHECKPOINT, STORE_FULL, STORE_LAP, STORE_NONE, STORE_STRIPS, check
 
 __all__ = ["PhysicsEngine", "shard_range", "NonFiniteResult", "STORE_NONE", "STORE_FULL",
-           "STORE_STRIPS", "STORE_CHECKPOINT"]
+           "STORE_STRIPS", "STORE_CHECKPOINT", "STORE_LAP"]
 
 _ENGINES = {"auto": _lib.ENGINE_AUTO, "stepwise": _lib.ENGINE_STEPWISE,
             "cluster": _lib.ENGINE_CLUSTER}
@@ -119,6 +120,7 @@ class PhysicsEngine:
         self.S, self.R, self.B = tx.shape[0], rx.shape[1], int(n_phantoms)
         self.n_units = self.S * self.B
         self.has_rho = bool(has_rho)
+        self.engine_kind = engine
         self.tx, self.rx, self.elements, self.pulse = tx, rx, el, pulse
         geo = _lib.Geometry()
         geo.nx, geo.nz, geo.nt = self.nx, self.nz, self.nt
@@ -162,6 +164,8 @@ class PhysicsEngine:
         self._flag = torch.zeros(4, dtype=torch.int32, device=self.device)
         self._c = None
         self._rho = None
+        self._cluster_path = None
+        self._auto_store: dict[bool, int] = {}
         self.box = self._undamped_box()
         # one packed f64 buffer [acc (B*nx*nz) | misfit (B) | flags (1)] so the
         # per-gradient combine across ranks is a single all_reduce
@@ -317,16 +321,33 @@ class PhysicsEngine:
         flat = ws.buf[off.value: off.value + 4 * n].view(torch.float32)
         return flat.view(self.nt, self.nx, self.nz).clone()
 
+    @property
+    def cluster_path(self) -> bool:
+        """The sweeps run on the cluster engine (the grid fits, not forced stepwise)."""
+        if self._cluster_path is None:
+            self._cluster_path = bool(self.info().get("cluster_ok")) and self.engine_kind != "stepwise"
+        return self._cluster_path
+
     def pick_store(self, mask: bool, store: str = "auto") -> int:
         """Forward-history strategy of a gradient: "full" f32 history, "strips"
         (1-cell ring of the undamped box + backward reconstruction),
-        "checkpoint" (snapshots + segment recomputation, any damping) or
-        "auto": strips where they apply, else full history when one unit's
-        fits the memory budget, else checkpointing."""
+        "checkpoint" (snapshots + segment recomputation, any damping), "lap"
+        (cluster engine: the forward stores the imaging operand L(u), the
+        adjoint carries only lam) or "auto": lap on the cluster engine when a
+        wave of units fits the memory budget, else strips where they apply,
+        else full history when one unit's fits, else checkpointing."""
         if store == "full":
             return STORE_FULL
         if store == "checkpoint":
             return STORE_CHECKPOINT
+        if store == "lap":
+            if not self.cluster_path:
+                raise ValueError("L(u) history storage needs the cluster engine")
+            if self.box is None or (not mask and self.box != (0, self.nx - 1, 0, self.nz - 1)):
+                raise ValueError("L(u) history storage images the undamped box; use mask=True")
+            if self.nz % 4:
+                raise ValueError("L(u) history storage needs nz % 4 == 0")
+            return STORE_LAP
         if store == "strips":
             if self.box is None:
                 raise ValueError("strip storage needs a rectangular undamped box")
@@ -335,10 +356,24 @@ class PhysicsEngine:
             return STORE_STRIPS
         if store != "auto":
             raise ValueError(f"unknown store {store!r}")
-        if self.box is not None and (mask or self.box == (0, self.nx - 1, 0, self.nz - 1)):
-            return STORE_STRIPS
+        # decided once per mask setting: no device query inside captured CUDA graphs
+        hit = self._auto_store.get(bool(mask))
+        if hit is not None:
+            return hit
+        self._auto_store[bool(mask)] = mode = self._auto_pick(mask)
+        return mode
+
+    def _auto_pick(self, mask: bool) -> int:
         free, _ = torch.cuda.mem_get_info(self.device)
         held = sum(w.buf.numel() for w in self._ws.values())
+        box_ok = self.box is not None and (mask or self.box == (0, self.nx - 1, 0, self.nz - 1))
+        if (self.cluster_path and box_ok and self.nz % 4 == 0
+                and os.environ.get("DUFWI_LAP", "1") != "0"):
+            wave = min(self.n_units, 16)
+            if self._ws_bytes(STORE_LAP, wave) <= (free + held) * self.memory_fraction:
+                return STORE_LAP
+        if self.box is not None and (mask or self.box == (0, self.nx - 1, 0, self.nz - 1)):
+            return STORE_STRIPS
         if self._ws_bytes(STORE_FULL, 1) > (free + held) * self.memory_fraction:
             return STORE_CHECKPOINT
         return STORE_FULL
@@ -464,6 +499,6 @@ class PhysicsEngine:
         f = [ev[r][0].elapsed_time(ev[r][1]) for r in range(1, reps + 1)]
         a = [ev[r][2].elapsed_time(ev[r][3]) for r in range(1, reps + 1)]
         return {"units": U, "forward_ms": sum(f) / reps, "adjoint_ms": sum(a) / reps,
-                "store": {STORE_FULL: "full", STORE_STRIPS: "strips",
+                "store": {STORE_FULL: "full", STORE_STRIPS: "strips", STORE_LAP: "lap",
                           STORE_CHECKPOINT: "checkpoint"}.get(mode, "none"),
                 "engine": self.last_engine}

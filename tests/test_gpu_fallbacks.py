@@ -114,10 +114,13 @@ def test_checkpoint_auto_when_full_history_does_not_fit(gpu):
                          pulse.samples, damp, engine="stepwise")
     from paper_2603_04070_b200.engine import STORE_CHECKPOINT, STORE_FULL
 
+    eng._auto_store.clear()
     assert eng.pick_store(True) == STORE_FULL
     frac = eng.memory_fraction
     try:
         eng.memory_fraction = 1e-9
+        eng._auto_store.clear()
         assert eng.pick_store(True) == STORE_CHECKPOINT
     finally:
         eng.memory_fraction = frac
+        eng._auto_store.clear()

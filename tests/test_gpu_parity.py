@@ -238,3 +238,33 @@ def test_errors_match_reference_types(gpu):
     big = pk.SourcePulse(np.full(grid.nt, 1e300), grid.dt, 2e5)
     with pytest.raises(pk.NumericError):
         pk.simulate_all(pk.SosMap(grid, z["c0"]), geom, big, damp)
+
+
+def test_cluster_lap_store_vs_reference(gpu, golden_dir):
+    """The cluster engine's L(u)-history store (the forward keeps the imaging
+    operand, the adjoint carries only lam): ring48 and config 0 against the
+    reference fixtures; box-only like the strips (unmasked gradients refuse it); it is
+    the cluster engine's auto store."""
+    z, grid, geom, pulse, damp = ring48()
+    eng = _engine(grid, geom, pulse, damp, "cluster")
+    from paper_2603_04070_b200.engine import STORE_LAP
+
+    assert eng.pick_store(True) == STORE_LAP
+    eng.set_model(z["c0"][None])
+    obs = torch.as_tensor(z["obs"]).to(gpu)
+    mis, g = eng.misfit_and_gradient(obs, store="lap")
+    assert eng.last_engine == "cluster"
+    assert rel_l2(g[0].cpu().numpy(), z["grad"]) <= GRAD_TOL
+    assert abs(float(mis[0]) - float(z["misfit"])) <= 1e-4 * float(z["misfit"])
+    with pytest.raises(ValueError, match="mask=True"):
+        eng.misfit_and_gradient(obs, store="lap", mask=False)
+    _, gs = eng.misfit_and_gradient(obs, store="strips")
+    assert rel_l2(g.cpu().numpy(), gs.cpu().numpy()) <= 1e-6
+    wl, grid, geom, pulse, damp = config_setup(0)
+    zc = np.load(golden_dir / "config0.npz")
+    eng = _engine(grid, geom, pulse, damp, "cluster")
+    eng.set_model(np.full((1,) + grid.shape, 1540.0))
+    obs, _ = oracle.forward_sweep(wl.c_true[0], damp.values, grid.dx, grid.dt, pulse.samples,
+                                  geom.tx_nodes(), geom.rx_nodes())
+    _, g = eng.misfit_and_gradient(torch.as_tensor(obs).to(gpu), store="lap")
+    assert rel_l2(g[0].cpu().numpy(), zc["grad"]) <= GRAD_TOL
