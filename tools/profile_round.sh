@@ -5,10 +5,10 @@
 set -e
 R=${1:-r01}
 mkdir -p gpurun_out
-python bench.py --steps 2 --warmup 1 --skip-cpu --skip-e2e > gpurun_out/${R}_bench_plain.json 2> gpurun_out/${R}_bench_plain.err
+python bench.py --steps 2 --warmup 1 --skip-cpu --skip-e2e --skip-large > gpurun_out/${R}_bench_plain.json 2> gpurun_out/${R}_bench_plain.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${R}_launches.csv \
-    python bench.py --steps 2 --warmup 1 --skip-cpu --skip-e2e > gpurun_out/${R}_ncu_bench.log 2>&1
+    python bench.py --steps 2 --warmup 1 --skip-cpu --skip-e2e --skip-large > gpurun_out/${R}_ncu_bench.log 2>&1
 # cluster engine (configs 0/1 share the sweep shape): adjoint, and the trial forward (2nd forward)
 python tools/prof_case.py --config 0 > gpurun_out/${R}_case_plain.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:cluster_adj -c 1 \
