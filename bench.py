@@ -516,7 +516,7 @@ def run_ours(args, rank: int, world: int) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 arithmetic / f32 storage",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded inclusion phantoms; random-init update nets)",
             "config": {"workload": f"config{args.config}: DUFWI K={K} on the config-0 geometry",
                        "grid": [grid.nx, grid.nz], "pml": wl.spec.pml, "nt": grid.nt,

@@ -59,6 +59,20 @@ extern "C" {
 #define DUFWI_ENGINE_STEPWISE 1/* one launch per time step over all units                    */
 #define DUFWI_ENGINE_CLUSTER 2 /* one launch per sweep, one thread-block cluster per unit    */
 
+/* Arithmetic of the sweep kernels (dufwi_geometry_t.arith).  Fields, traces and
+ * strips are f32 in HBM either way.
+ *   F32: every update in f32, in the increment form
+ *        u[t] = u1 + ((u1 - u2) + (A-2) u1 + (B+1) u2 + E L(u1)),
+ *        L by differences (u_j - u_c): the error of "f64 arithmetic, f32 storage"
+ *        (traces ~5e-7, fixed-observation gradients ~5e-6 against the reference),
+ *        inside the 1e-4 / 1e-3 bars at every BASELINE size.  The fast path.
+ *   F64: every update in f64 in the reference's operation order (forward.py:301-308);
+ *        on the cluster engine the whole sweep is then a float64 computation
+ *        (traces ~3e-8).  For callers that difference misfits (fd_gradient_oracle)
+ *        or iterate to convergence on a shrinking residual (ADMM-TV FWI). */
+#define DUFWI_ARITH_F32 0
+#define DUFWI_ARITH_F64 1
+
 typedef struct dufwi_geometry {
   int32_t nx, nz, nt;       /* grid and time axis (grid.py:42-84)                 */
   int32_t n_phantoms;       /* B                                                  */
@@ -67,7 +81,7 @@ typedef struct dufwi_geometry {
   int32_t n_elements;       /* E element nodes (for the gradient guard mask)      */
   int32_t has_rho;          /* 1: variable density model         */
   int32_t engine;           /* DUFWI_ENGINE_*                                     */
-  int32_t reserved;
+  int32_t arith;            /* DUFWI_ARITH_* (0 = f32, the default)               */
   double dx, dt;
   const int32_t* tx_host;       /* [S][2]   transmit node (ix, iz) per shot       */
   const int32_t* rx_host;       /* [S][R][2] receiver nodes per shot              */

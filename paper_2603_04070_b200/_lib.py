@@ -53,7 +53,7 @@ class Geometry(ctypes.Structure):
         ("nx", ctypes.c_int32), ("nz", ctypes.c_int32), ("nt", ctypes.c_int32),
         ("n_phantoms", ctypes.c_int32), ("n_shots", ctypes.c_int32), ("n_rx", ctypes.c_int32),
         ("n_elements", ctypes.c_int32), ("has_rho", ctypes.c_int32), ("engine", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("arith", ctypes.c_int32),
         ("dx", ctypes.c_double), ("dt", ctypes.c_double),
         ("tx_host", ctypes.POINTER(ctypes.c_int32)),
         ("rx_host", ctypes.POINTER(ctypes.c_int32)),

@@ -169,7 +169,7 @@ def fd_gradient_oracle(sos: SosMap, m_obs: ChannelData, pulse: SourcePulse, cell
     rho = _density_values(density, sos.grid)
     B = len(maps)
     eng = get_engine(sos.grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
-                     pulse.samples, damping, n_phantoms=B, has_rho=rho is not None)
+                     pulse.samples, damping, n_phantoms=B, has_rho=rho is not None, arith="f64")
     eng.set_model(np.stack(maps), None if rho is None else np.broadcast_to(rho, (B,) + rho.shape))
     obs = torch.as_tensor(np.ascontiguousarray(m_obs.traces), dtype=torch.float64).to(eng.device)
     obs = obs.repeat(B, 1, 1)

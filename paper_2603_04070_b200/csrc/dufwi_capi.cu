@@ -77,6 +77,7 @@ struct dufwi_plan {
   ClusterCfg ccfg{};                // the forward's shape for all units at once (plan_info)
   ClusterCfg ccfg_adj{};            // the adjoint's
   bool cluster_ok = false;
+  int arith = DUFWI_ARITH_F32;  // arithmetic of the sweep kernels (dufwi_geometry_t.arith)
   int lean_tx = 0;      // rows per warp override (DUFWI_LEAN_TX, experiments)
   bool lean_on = true;  // lean stepwise kernels (DUFWI_LEAN=0: the first vec/stream kernels)
   double *Er = nullptr, *fxe = nullptr, *fz = nullptr, *fz0 = nullptr;  // density tables
@@ -263,6 +264,7 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   p->E = geo->n_elements;
   p->has_rho = geo->has_rho ? 1 : 0;
   p->engine = geo->engine;
+  p->arith = geo->arith == DUFWI_ARITH_F64 ? DUFWI_ARITH_F64 : DUFWI_ARITH_F32;
   p->dx = geo->dx;
   p->dt = geo->dt;
   Geo& g = p->geo;
@@ -427,7 +429,8 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
     big((const void*)img_lean_kernel<1, true>, sizeof(LeanImgRing<true>));
     big((const void*)img_lean_kernel<2, true>, sizeof(LeanImgRing<true>));
   }
-  p->cluster_ok = cluster_candidates(g, p->has_rho != 0, rx_nodes, p->ccands);
+  p->cluster_ok = cluster_candidates(g, p->has_rho != 0, p->arith == DUFWI_ARITH_F64, rx_nodes,
+                                      p->ccands);
   if (p->cluster_ok) {
     p->ccfg = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots);
     p->ccfg_adj = pick_cluster(p->ccands, geo->n_phantoms * geo->n_shots, true);

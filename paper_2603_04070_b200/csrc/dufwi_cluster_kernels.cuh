@@ -61,6 +61,7 @@ struct ClusterCfg {
   int maxrec = 0;   // receiver stage entries per CTA: RPT per thread holding receivers
   int maxring = 0;  // ring-strip cells per CTA (upper bound) staged in shared memory
   int maxc = 0;     // clusters co-resident on the device (one wave)
+  int per_sm = 1;   // CTAs of the sweep kernels that fit one SM (registers / shared memory)
   size_t smem_fwd = 0, smem_adj = 0;
   size_t smem_lap = 0;     // adjoint over the L(u) history (DUFWI_STORE_LAP)
   size_t smem_fwdlap = 0;  // forward storing it (staging slots)
@@ -150,7 +151,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 
 // ------------------------------------------------------------ smem layout
-// [nbufs exchange buffers] [nz x nseg*RPT double2 (A, B)] [2 mbarriers] [IO stage]
+// [nbufs exchange buffers] [nz x nseg*RPT float2 (A, B)] [2 mbarriers] [IO stage]
 // An exchange buffer is column-major: cell (buffer row r, column z) at
 // (z + 1) * RS + r, r = local row + 1 (r = 0 / rows + 1: halo rows from the
 // neighbouring CTAs), z = -1 / nz: zero pad columns.  RS >= nseg * RPT + 2 is
@@ -174,20 +175,21 @@ __host__ __device__ inline int ab_col_stride(int rows, int rpt) {
 }
 template <class T>
 __host__ __device__ inline size_t bar_offset(int rows, int rpt, int nz, int nbufs) {
-  return ab_offset<T>(rows, rpt, nz, nbufs) + (size_t)ab_col_stride(rows, rpt) * nz * sizeof(double2);
+  return ab_offset<T>(rows, rpt, nz, nbufs) + (size_t)ab_col_stride(rows, rpt) * nz * sizeof(pair_t<T>);
 }
 // IO stage after the mbarriers: [n_rec, n_ring, pad] [rec_g[maxrec]] [ring_g[maxring]]
-// [rec_b[maxrec]] [ring_b[maxring]] [double stage_rec[kStage][maxrec]]
+// [rec_b[maxrec]] [ring_b[maxring]] [float stage_rec[kStage][maxrec]]
 // [float stage_ring[kStage][maxring]].  *_g: HBM slot, *_b: exchange-buffer index.
+template <class T>
 struct IoStage {
   int* counts;
   int* rec_g;
   int* ring_g;
   int* rec_b;
   int* ring_b;
-  double* srec;
+  T* srec;
   float* sring;
-  double* spulse;  // pulse samples of the stage's steps (adjoint)
+  T* spulse;  // pulse samples of the stage's steps (adjoint)
   int maxrec, maxring;
 };
 
@@ -198,19 +200,22 @@ __host__ __device__ inline size_t io_offset(int rows, int rpt, int nz, int nbufs
   return al16(bar_offset<T>(rows, rpt, nz, nbufs) + 2 * sizeof(uint64_t));
 }
 
+template <class T>
 __host__ __device__ inline size_t io_bytes(int maxrec, int maxring) {
   return 16 + 2 * al16((size_t)maxrec * 4) + 2 * al16((size_t)maxring * 4) +
-         al16((size_t)kStage * maxrec * 8) + al16((size_t)kStage * maxring * 4) + kStage * 8;
+         al16((size_t)kStage * maxrec * sizeof(T)) + al16((size_t)kStage * maxring * 4) +
+         al16((size_t)kStage * sizeof(T));
 }
 
 template <class T>
 __host__ __device__ inline size_t cluster_smem_bytes(int rows, int rpt, int nz, int nbufs,
                                                      int maxrec, int maxring) {
-  return io_offset<T>(rows, rpt, nz, nbufs) + io_bytes(maxrec, maxring);
+  return io_offset<T>(rows, rpt, nz, nbufs) + io_bytes<T>(maxrec, maxring);
 }
 
-__device__ __forceinline__ IoStage io_stage(unsigned char* base, int maxrec, int maxring) {
-  IoStage io;
+template <class T>
+__device__ __forceinline__ IoStage<T> io_stage(unsigned char* base, int maxrec, int maxring) {
+  IoStage<T> io;
   io.counts = reinterpret_cast<int*>(base);
   size_t o = 16;
   io.rec_g = reinterpret_cast<int*>(base + o);
@@ -221,11 +226,11 @@ __device__ __forceinline__ IoStage io_stage(unsigned char* base, int maxrec, int
   o += al16((size_t)maxrec * 4);
   io.ring_b = reinterpret_cast<int*>(base + o);
   o += al16((size_t)maxring * 4);
-  io.srec = reinterpret_cast<double*>(base + o);
-  o += al16((size_t)kStage * maxrec * 8);
+  io.srec = reinterpret_cast<T*>(base + o);
+  o += al16((size_t)kStage * maxrec * sizeof(T));
   io.sring = reinterpret_cast<float*>(base + o);
   o += al16((size_t)kStage * maxring * 4);
-  io.spulse = reinterpret_cast<double*>(base + o);
+  io.spulse = reinterpret_cast<T*>(base + o);
   io.maxrec = maxrec;
   io.maxring = maxring;
   return io;
@@ -368,9 +373,9 @@ __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx,
 }
 
 // Static per-cell data loaded once per sweep.
-template <int RPT>
+template <int RPT, class T>
 struct CellStatic {
-  double ed[RPT];
+  T ed[RPT];
   // receiver / ring rows (bit j = row j) and their first IO-stage index.  A
   // thread holding receivers owns RPT consecutive receiver entries (row j at
   // base + j; slot -1 where row j has none), ring row j's entry is
@@ -388,14 +393,14 @@ struct CellStatic {
   bool full;                  // whole warp: every row slot active
   bool unif;                  // whole warp: full, and one (A, B) per thread for all its rows
   bool pml;                   // whole warp: full, and no cell in the undamped box
-  const double2* ab;          // this thread's (A, B) column: ab[j] for row j
+  const pair_t<T>* ab;          // this thread's (A, B) column: ab[j] for row j
 };
 
-template <int RPT>
+template <int RPT, class T>
 __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const CellCtx& c,
-                                            size_t pb, int txx, int txz, double2* ab_table,
-                                            const IoStage& io, bool allow_fast,
-                                            CellStatic<RPT>& st) {
+                                            size_t pb, int txx, int txz, pair_t<T>* ab_table,
+                                            const IoStage<T>& io, bool allow_fast,
+                                            CellStatic<RPT, T>& st) {
   st.active = st.src = st.interior = 0u;
   st.ab = ab_table + (size_t)c.z * ab_col_stride(c.rows, RPT) + c.lrow0;
   st.pushes_up = c.has_up && c.lrow0 == 0;
@@ -405,14 +410,12 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const int lr = c.lrow0 + j;
-    st.ed[j] = 0.0;
+    st.ed[j] = T(0);
     if (lr < c.nr) {
       const int x = c.r0 + lr;
       st.active |= 1u << j;
-      st.ed[j] = m.Ed[pb + (size_t)x * g.nz + c.z];
-      double A, B;
-      ab_coeffs(damping_at(g, x, c.z), g.dt, A, B);
-      const_cast<double2*>(st.ab)[j] = make_double2(A, B);
+      st.ed[j] = (T)m.Ed[pb + (size_t)x * g.nz + c.z];
+      const_cast<pair_t<T>*>(st.ab)[j] = ab_pair<T>(damping_at(g, x, c.z), g.dt);
       if (g.row_flag[x] && g.node_slot[(size_t)x * g.nz + c.z] >= 0) st.rmask |= 1u << j;
       if (io.maxring > 0 && ring_index(g, x, c.z) >= 0) st.gmask |= 1u << j;
       if (x == txx && c.z == txz) st.src |= 1u << j;
@@ -469,8 +472,8 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
 // xb: byte offset of the written buffer from the CTA's shared-memory base
 // (uniform), bb: same for the mbarrier completing the step.
 template <int RPT, class T>
-__device__ __forceinline__ void push_edges(const CellCtx& c, const CellStatic<RPT>& s, uint32_t xb,
-                                           uint32_t bb, const double (&v)[RPT], bool full) {
+__device__ __forceinline__ void push_edges(const CellCtx& c, const CellStatic<RPT, T>& s, uint32_t xb,
+                                           uint32_t bb, const T (&v)[RPT], bool full) {
   if (s.pushes_up) push_async(c.rup + xb + c.off_up, (T)v[0], c.rup + bb);
   if (s.pushes_dn) {
     const uint32_t ra = c.rdn + xb + c.off_dn;
@@ -553,7 +556,7 @@ __device__ __forceinline__ BoxRows box_rows(const Geo& g, const CellCtx& c) {
 template <class T>
 __host__ __device__ inline size_t lap_stage_offset(int rows, int rpt, int nz, int maxrec,
                                                    int maxring) {
-  return al16(io_offset<T>(rows, rpt, nz, 2) + io_bytes(maxrec, maxring));
+  return al16(io_offset<T>(rows, rpt, nz, 2) + io_bytes<T>(maxrec, maxring));
 }
 template <class T>
 __host__ __device__ inline size_t cluster_fwdlap_smem_bytes(int rows, int rpt, int nz, int maxrec,
@@ -563,7 +566,7 @@ __host__ __device__ inline size_t cluster_fwdlap_smem_bytes(int rows, int rpt, i
 // Adjoint ring: kLapDepth mbarriers (32 B) then kLapDepth slots of rows x nz floats.
 template <class T>
 __host__ __device__ inline size_t lap_ring_offset(int rows, int rpt, int nz, int maxrec) {
-  return al16(io_offset<T>(rows, rpt, nz, 2) + io_bytes(maxrec, 0));
+  return al16(io_offset<T>(rows, rpt, nz, 2) + io_bytes<T>(maxrec, 0));
 }
 template <class T>
 __host__ __device__ inline size_t cluster_lap_smem_bytes(int rows, int rpt, int nz, int maxrec) {
@@ -613,37 +616,37 @@ struct LapFwd {
 // gathered separately).  All warp-uniform, chosen once per sweep.
 // Receiver / ring samples are gathered from the exchange buffer by io_gather.
 template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF, bool IO>
-__device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
-                                         double (&u1)[RPT], double (&u2)[RPT], int t, int U,
-                                         int lu, const StepBufs<T>& B, double pulse_t,
+__device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const CellStatic<RPT, T>& s,
+                                         T (&u1)[RPT], T (&u2)[RPT], int t, int U,
+                                         int lu, const StepBufs<T>& B, T pulse_t,
                                          float* __restrict__ hist, size_t N2) {
   const T* pc = B.r + c.xo;
   const T* pm = pc - c.RS;
   const T* pp = pc + c.RS;
-  double v[RPT];
-  const double2 ab0 = (!PLAIN && UNIF) ? s.ab[0] : make_double2(2.0, -1.0);
+  T v[RPT];
+  const pair_t<T> ab0 = (!PLAIN && UNIF) ? s.ab[0] : free_pair<T>();
   // MODE 3: the step's L(u[t-1]) (5-point sum, f32) of the box cells into the
   // shared-memory staging slot of step t (`hist`: the thread's first cell there),
   // written to history slot t-1 by one bulk copy after the next step barrier
   float* hl = hist;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    const double xm = j > 0 ? u1[j - 1] : (double)pc[-1];
+    const T xm = j > 0 ? u1[j - 1] : (T)pc[-1];
     const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
-    const double xp = own_next ? u1[j + 1] : (double)pc[j + 1];
-    const double lap = lap5(u1[j], xm, xp, (double)pm[j], (double)pp[j]);
+    const T xp = own_next ? u1[j + 1] : (T)pc[j + 1];
+    const T lap = lap_s(u1[j], xm, xp, (T)pm[j], (T)pp[j]);
     if (MODE == 3 && t >= 1 && (PLAIN || ((s.interior >> j) & 1u))) hl[j * g.nz] = (float)lap;
     if (PLAIN) {
-      v[j] = fwd_update_free(u1[j], u2[j], s.ed[j], lap);
+      v[j] = step_free(u1[j], u2[j], s.ed[j], lap);
     } else {
-      const double2 ab = UNIF ? ab0 : s.ab[j];
-      v[j] = fwd_update(ab.x, ab.y, u1[j], u2[j], s.ed[j], lap);
+      const pair_t<T> ab = UNIF ? ab0 : s.ab[j];
+      v[j] = step_ab(ab, u1[j], u2[j], s.ed[j], lap);
     }
   }
   if ((!PLAIN || IO) && s.src) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
-      if (s.src & (1u << j)) v[j] = __dadd_rn(v[j], pulse_t);
+      if (s.src & (1u << j)) v[j] = add_s(v[j], pulse_t);
   }
   T* q = B.w + c.xo;
 #pragma unroll
@@ -676,12 +679,12 @@ __device__ __forceinline__ int gather_rank() {
 }
 
 template <class T, int MODE>
-__device__ __forceinline__ void io_gather(const IoStage& io, int nrec, int nio, const T* X, int t,
+__device__ __forceinline__ void io_gather(const IoStage<T>& io, int nrec, int nio, const T* X, int t,
                                           int rank) {
   const int k = t % kStage;
   for (int i = rank; i < nio; i += blockDim.x) {
     if (i < nrec) {
-      io.srec[k * io.maxrec + i] = (double)(float)X[io.rec_b[i]];
+      io.srec[k * io.maxrec + i] = (T)(float)X[io.rec_b[i]];
     } else if (MODE == 2) {
       const int r = i - nrec;
       io.sring[k * io.maxring + r] = (float)X[io.ring_b[r]];
@@ -690,8 +693,8 @@ __device__ __forceinline__ void io_gather(const IoStage& io, int nrec, int nio, 
 }
 
 // Write the staged receiver samples / ring strips of steps [t0, t0+nk) to HBM.
-template <int MODE>
-__device__ __forceinline__ void flush_stage(const Geo& g, const IoStage& io, int t0, int nk, int U,
+template <class T, int MODE>
+__device__ __forceinline__ void flush_stage(const Geo& g, const IoStage<T>& io, int t0, int nk, int U,
                                             int lu, float* __restrict__ rec,
                                             float* __restrict__ strips) {
   __syncthreads();
@@ -710,10 +713,10 @@ __device__ __forceinline__ void flush_stage(const Geo& g, const IoStage& io, int
 }
 
 template <int RPT, class T, int MODE>
-__device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
-                                         double (&u1)[RPT], double (&u2)[RPT], int t, int U,
+__device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const CellStatic<RPT, T>& s,
+                                         T (&u1)[RPT], T (&u2)[RPT], int t, int U,
                                          int lu, const StepBufs<T>& B, uint32_t tx_bytes,
-                                         double pulse_t, const IoStage& io, int nrec, int nio,
+                                         T pulse_t, const IoStage<T>& io, int nrec, int nio,
                                          float* __restrict__ rec, float* __restrict__ strips,
                                          float* __restrict__ hist, size_t N2, int grank,
                                          const LapFwd& lap) {
@@ -724,7 +727,7 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
   if (MODE == 3) lap_store(g, lap.br, c.rows, t, lap.stage_sa, lap.hbox, lap.hstep);
   if (t >= 1) {
     io_gather<T, MODE>(io, nrec, nio, B.r, t - 1, grank);
-    if (t % kStage == 0) flush_stage<MODE>(g, io, t - kStage, kStage, U, lu, rec, strips);
+    if (t % kStage == 0) flush_stage<T, MODE>(g, io, t - kStage, kStage, U, lu, rec, strips);
   }
 #ifdef DUFWI_EXP_TIMING
   const long long T1 = clock64();
@@ -764,7 +767,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
   order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem), RPT, DUFWI_PLACE_FWD);
   for (size_t i = threadIdx.x; i < 2 * xe; i += blockDim.x) X[0][i] = T(0);
-  const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 2), maxrec, maxring);
+  const IoStage<T> io = io_stage<T>(smem + io_offset<T>(rows, RPT, g.nz, 2), maxrec, maxring);
   if (threadIdx.x == 0) {
     mbar_init(bar[0], 1);
     mbar_init(bar[1], 1);
@@ -772,18 +775,18 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
     io.counts[0] = io.counts[1] = 0;
   }
   __syncthreads();
-  CellStatic<RPT> st;
-  load_static<RPT>(g, m, c, pb, txx, txz,
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)),
+  CellStatic<RPT, T> st;
+  load_static<RPT, T>(g, m, c, pb, txx, txz,
+                   reinterpret_cast<pair_t<T>*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)),
                    io,
                    true, st);  // (FULL too: the history store is in every step variant)
   const uint32_t tx_bytes =
       (uint32_t)((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T);
-  double ua[RPT], ub[RPT];
+  T ua[RPT], ub[RPT];
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) ua[j] = ub[j] = 0.0;
+  for (int j = 0; j < RPT; ++j) ua[j] = ub[j] = T(0);
   const bool owns_src = st.src != 0u;
-  double p_next = owns_src ? g.pulse[0] : 0.0;
+  T p_next = owns_src ? (T)g.pulse[0] : T(0);
   cluster_sync_all();  // barriers initialised, buffers zeroed, IO lists complete cluster-wide
   const int nrec = io.counts[0];
   const int nio = nrec + (MODE == 2 ? io.counts[1] : 0);
@@ -811,12 +814,12 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
 #define DUFWI_HS(t) (MODE == 3 ? stage + (size_t)(((t) + kLapStage - 1) % kLapStage) * slotf + lofs : hist)
   int t = 0;
   for (; t + 1 < g.nt; t += 2) {
-    double p = p_next;
-    if (owns_src) p_next = g.pulse[t + 1];
+    T p = p_next;
+    if (owns_src) p_next = (T)g.pulse[t + 1];
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p, io, nrec, nio, rec,
                            strips, DUFWI_HS(t), N2, grank, lap);
     p = p_next;
-    if (owns_src && t + 2 < g.nt) p_next = g.pulse[t + 2];
+    if (owns_src && t + 2 < g.nt) p_next = (T)g.pulse[t + 2];
     fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, B1, tx_bytes, p, io, nrec, nio, rec,
                            strips, DUFWI_HS(t + 1), N2, grank, lap);
   }
@@ -833,7 +836,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   io_gather<T, MODE>(io, nrec, nio, X[(g.nt - 1) & 1], g.nt - 1, gather_rank());
   {
     const int t0 = (g.nt - 1) / kStage * kStage;
-    flush_stage<MODE>(g, io, t0, g.nt - t0, U, lu, rec, strips);
+    flush_stage<T, MODE>(g, io, t0, g.nt - t0, U, lu, rec, strips);
   }
   // drain the last step's incoming pushes before any CTA of the cluster exits
   if (c.has_up || c.has_dn) mbar_wait(bar[(g.nt - 1) & 1], ((g.nt - 1) >> 1) & 1);
@@ -851,6 +854,22 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
       d_last[cell] = (float)(last_odd ? ua[j] : ub[j]);
       d_prev[cell] = (float)(last_odd ? ub[j] : ua[j]);
     }
+  }
+}
+
+// The imaging sums run in f32 over blocks of kAccBlock steps and are folded
+// into f64 totals between blocks: a block's partial sum carries ~sqrt(16) f32
+// roundings, the sum over the sweep's thousands of (cancelling) terms none.
+constexpr int kAccBlock = 16;
+static_assert(kAccBlock % 2 == 0, "flushed between step pairs");
+template <int RPT>
+__device__ __forceinline__ void acc_flush(double (&)[RPT], double (&)[RPT]) {}  // f64 sums: nothing to fold
+template <int RPT>
+__device__ __forceinline__ void acc_flush(float (&acc)[RPT], double (&accd)[RPT]) {
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    accd[j] += (double)acc[j];
+    acc[j] = 0.f;
   }
 }
 
@@ -872,101 +891,101 @@ struct AdjBufs {
 // no imaging and no reconstruction; only ring cells carry u (from the strips).
 template <int RPT, class T, int MODE, bool FULL, bool PLAIN, bool UNIF, bool IO, bool NOIMG,
           bool T2>
-__device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
-                                         double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
-                                         double (&ub)[RPT], double (&acc)[RPT], int i, int U,
-                                         int lu, const AdjBufs<T>& B, const IoStage& io,
+__device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const CellStatic<RPT, T>& s,
+                                         T (&l1)[RPT], T (&l2)[RPT], T (&ua)[RPT],
+                                         T (&ub)[RPT], T (&acc)[RPT], int i, int U,
+                                         int lu, const AdjBufs<T>& B, const IoStage<T>& io,
                                          const float* __restrict__ hist, size_t N2) {
   const int RS = c.RS, z = c.z;
   const int t = g.nt - 1 - i;
   const int k = i % kStage;
   // lam[t] = A lam1 + L^T(E lam1) + B lam2 (+ residual at receivers)
-  double el[RPT], lam[RPT];
-  const double2 ab0 = (!PLAIN && UNIF) ? s.ab[0] : make_double2(2.0, -1.0);
+  T el[RPT], lam[RPT];
+  const pair_t<T> ab0 = (!PLAIN && UNIF) ? s.ab[0] : free_pair<T>();
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
+  for (int j = 0; j < RPT; ++j) el[j] = mul_s(s.ed[j], l1[j]);
   {
     const T* pc = B.lr + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-      const double xm = j > 0 ? el[j - 1] : (double)pc[-1];
+      const T xm = j > 0 ? el[j - 1] : (T)pc[-1];
       const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
-      const double xp = own_next ? el[j + 1] : (double)pc[j + 1];
-      const double adj = lap5(el[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
+      const T xp = own_next ? el[j + 1] : (T)pc[j + 1];
+      const T adj = lap_s(el[j], xm, xp, (T)pc[j - RS], (T)pc[j + RS]);
       if (PLAIN) {
-        lam[j] = adj_update_free(l1[j], l2[j], adj);
+        lam[j] = adjs_free(l1[j], l2[j], adj);
       } else {
-        const double2 ab = UNIF ? ab0 : s.ab[j];
-        lam[j] = adj_update(ab.x, ab.y, l1[j], l2[j], adj);
+        const pair_t<T> ab = UNIF ? ab0 : s.ab[j];
+        lam[j] = adjs_ab(ab, l1[j], l2[j], adj);
       }
     }
   }
   if ((!PLAIN || IO) && !NOIMG && s.rmask) {
     // one entry per row (0 where the row has no receiver: adding it is exact)
-    const double* r = io.srec + (size_t)k * io.maxrec + s.rbase;
+    const T* r = io.srec + (size_t)k * io.maxrec + s.rbase;
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) lam[j] = __dadd_rn(lam[j], r[j]);
+    for (int j = 0; j < RPT; ++j) lam[j] = add_s(lam[j], r[j]);
   }
   // imaging with L(u[t-1]) and reconstruction of u[t-2]
   const bool img = T2 || t >= 1;
-  double lapu[RPT];
+  T lapu[RPT];
   if (MODE == 2 && !NOIMG) {
     const T* pc = B.ur + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-      const double xm = j > 0 ? ub[j - 1] : (double)pc[-1];
+      const T xm = j > 0 ? ub[j - 1] : (T)pc[-1];
       const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
-      const double xp = own_next ? ub[j + 1] : (double)pc[j + 1];
-      lapu[j] = lap5(ub[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
+      const T xp = own_next ? ub[j + 1] : (T)pc[j + 1];
+      lapu[j] = lap_s(ub[j], xm, xp, (T)pc[j - RS], (T)pc[j + RS]);
     }
   } else if (MODE == 1) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-      lapu[j] = 0.0;
+      lapu[j] = T(0);
       if (img && (FULL || (s.active & (1u << j)))) {
         const float* F = hist + ((size_t)(t - 1) * U + lu) * N2;
         const int x = c.r0 + c.lrow0 + j;
         const size_t cell = (size_t)x * g.nz + z;
-        const double fxm = x > 0 ? (double)F[cell - g.nz] : 0.0;
-        const double fxp = x < g.nx - 1 ? (double)F[cell + g.nz] : 0.0;
-        const double fzm = z > 0 ? (double)F[cell - 1] : 0.0;
-        const double fzp = z < g.nz - 1 ? (double)F[cell + 1] : 0.0;
-        lapu[j] = lap5((double)F[cell], fxm, fxp, fzm, fzp);
+        const T fxm = x > 0 ? (T)F[cell - g.nz] : T(0);
+        const T fxp = x < g.nx - 1 ? (T)F[cell + g.nz] : T(0);
+        const T fzm = z > 0 ? (T)F[cell - 1] : T(0);
+        const T fzp = z < g.nz - 1 ? (T)F[cell + 1] : T(0);
+        lapu[j] = lap_s((T)F[cell], fxm, fxp, fzm, fzp);
       }
     }
   }
   T* ql = B.lw + c.xo;
   T* qu = B.uw + c.xo;
-  double elw[RPT];
+  T elw[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    elw[j] = __dmul_rn(s.ed[j], lam[j]);
+    elw[j] = mul_s(s.ed[j], lam[j]);
     if (!FULL && !(s.active & (1u << j))) continue;
     l2[j] = lam[j];
     ql[j] = (T)elw[j];
     if (MODE == 2 && NOIMG) {
       if (s.gmask & (1u << j)) {
         if (T2 || t >= 2)
-          ua[j] = (double)lds_f32(s.gsa + 4u * (uint32_t)(k * io.maxring + __popc(s.gmask & ((1u << j) - 1u))));
+          ua[j] = (T)lds_f32(s.gsa + 4u * (uint32_t)(k * io.maxring + __popc(s.gmask & ((1u << j) - 1u))));
         qu[j] = (T)ua[j];
       }
       continue;
     }
     if (img) {
       if (MODE == 1) {
-        acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
+        acc[j] = fma_s(lapu[j], lam[j], acc[j]);
       } else if (PLAIN || (s.interior & (1u << j))) {
-        acc[j] = __fma_rn(lapu[j], lam[j], acc[j]);
+        acc[j] = fma_s(lapu[j], lam[j], acc[j]);
         if (T2 || t >= 2) {
-          double prev = recon(ub[j], ua[j], s.ed[j], lapu[j]);
+          T prev = recon_s(ub[j], ua[j], s.ed[j], lapu[j]);
           // source sample s[t] from the shared-memory stage (a global load here
           // would sit on the step's critical path)
-          if ((!PLAIN || IO) && (s.src & (1u << j))) prev = __dadd_rn(prev, io.spulse[k]);
+          if ((!PLAIN || IO) && (s.src & (1u << j))) prev = add_s(prev, io.spulse[k]);
           ua[j] = prev;
         }
       } else if ((s.gmask & (1u << j)) && (T2 || t >= 2)) {
         // ring cell: the saved strip stands in for the reconstruction
-        ua[j] = (double)lds_f32(s.gsa + 4u * (uint32_t)(k * io.maxring + __popc(s.gmask & ((1u << j) - 1u))));
+        ua[j] = (T)lds_f32(s.gsa + 4u * (uint32_t)(k * io.maxring + __popc(s.gmask & ((1u << j) - 1u))));
       }
     }
     if (MODE == 2) qu[j] = (T)ua[j];
@@ -977,8 +996,8 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
 
 // Load residuals of steps [i0, i0+kStage) (t = nt-1-i) and the ring strips they
 // reconstruct from (t-2) into the shared-memory stage, one coalesced pass.
-template <int MODE>
-__device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, int i0, int U,
+template <class T, int MODE>
+__device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage<T>& io, int i0, int U,
                                                int lu, const double* __restrict__ rres,
                                                const float* __restrict__ strips) {
   __syncthreads();  // the previous block's readers are done with the stage
@@ -988,7 +1007,7 @@ __device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, 
     const int k = idx / nrec, r = idx - k * nrec;
     const int t = g.nt - 1 - (i0 + k);
     const int slot = io.rec_g[r];
-    io.srec[k * io.maxrec + r] = slot >= 0 ? rres[((size_t)t * U + lu) * g.M + slot] : 0.0;
+    io.srec[k * io.maxrec + r] = slot >= 0 ? (T)rres[((size_t)t * U + lu) * g.M + slot] : T(0);
   }
   if (MODE == 2) {
     for (int idx = threadIdx.x; idx < nk * nring; idx += blockDim.x) {
@@ -997,16 +1016,16 @@ __device__ __forceinline__ void prefetch_stage(const Geo& g, const IoStage& io, 
       io.sring[k * io.maxring + r] = t >= 2 ? strips[((size_t)(t - 2) * U + lu) * g.SL + io.ring_g[r]] : 0.f;
     }
     // (a strided loop: a small grid's CTA can have fewer threads than kStage)
-    for (int k = threadIdx.x; k < nk; k += blockDim.x) io.spulse[k] = g.pulse[g.nt - 1 - (i0 + k)];
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) io.spulse[k] = (T)g.pulse[g.nt - 1 - (i0 + k)];
   }
 }
 
 template <int RPT, class T, int MODE, bool T2>
-__device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const CellStatic<RPT>& s,
-                                         double (&l1)[RPT], double (&l2)[RPT], double (&ua)[RPT],
-                                         double (&ub)[RPT], double (&acc)[RPT], int i, int U,
+__device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const CellStatic<RPT, T>& s,
+                                         T (&l1)[RPT], T (&l2)[RPT], T (&ua)[RPT],
+                                         T (&ub)[RPT], T (&acc)[RPT], int i, int U,
                                          int lu, const AdjBufs<T>& B, uint32_t tx_bytes,
-                                         const IoStage& io,
+                                         const IoStage<T>& io,
                                          const float* __restrict__ hist, size_t N2) {
 #ifdef DUFWI_EXP_TIMING
   const long long T0 = clock64();
@@ -1069,7 +1088,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
   order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem), RPT, DUFWI_PLACE_ADJ);
   for (size_t k = threadIdx.x; k < 4 * xe; k += blockDim.x) base[k] = T(0);
-  const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 4), maxrec, maxring);
+  const IoStage<T> io = io_stage<T>(smem + io_offset<T>(rows, RPT, g.nz, 4), maxrec, maxring);
   if (threadIdx.x == 0) {
     mbar_init(bar[0], 1);
     mbar_init(bar[1], 1);
@@ -1077,9 +1096,9 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
     io.counts[0] = io.counts[1] = 0;
   }
   __syncthreads();
-  CellStatic<RPT> st;
-  load_static<RPT>(g, m, c, pb, txx, txz,
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 4)),
+  CellStatic<RPT, T> st;
+  load_static<RPT, T>(g, m, c, pb, txx, txz,
+                   reinterpret_cast<pair_t<T>*>(smem + ab_offset<T>(rows, RPT, g.nz, 4)),
                    io,
                    MODE == 2, st);
   const int per = MODE == 2 ? 2 : 1;
@@ -1099,10 +1118,12 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
       if (x >= 0 && x < g.nx) XU[1][(size_t)(zz + 1) * RS + rb] = (T)u_prev[(size_t)x * g.nz + zz];
     }
   }
-  double la[RPT], lb[RPT], ua[RPT], ub[RPT], acc[RPT];
+  T la[RPT], lb[RPT], ua[RPT], ub[RPT], acc[RPT];
+  double accd[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    la[j] = lb[j] = acc[j] = ua[j] = ub[j] = 0.0;
+    la[j] = lb[j] = acc[j] = ua[j] = ub[j] = T(0);
+    accd[j] = 0.0;
     if (MODE == 2 && (st.active & (1u << j))) {
       const size_t cell = (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z;
       ua[j] = u_last[cell];
@@ -1118,14 +1139,15 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   // steps with t >= 2 (i <= nt - 3) in pairs, then the tail
   int i = 0;
   for (; i + 1 < nt - 2; i += 2) {
-    if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
+    if (i % kAccBlock == 0) acc_flush<RPT>(acc, accd);
+    if (i % kStage == 0) prefetch_stage<T, MODE>(g, io, i, U, lu, rres, strips);
     adj_step<RPT, T, MODE, true>(g, c, st, la, lb, ua, ub, acc, i, U, lu, B0, tx_bytes, io, hist,
                                  N2);
     adj_step<RPT, T, MODE, true>(g, c, st, lb, la, ub, ua, acc, i + 1, U, lu, B1, tx_bytes, io,
                                  hist, N2);
   }
   for (; i < nt; ++i) {
-    if (i % kStage == 0) prefetch_stage<MODE>(g, io, i, U, lu, rres, strips);
+    if (i % kStage == 0) prefetch_stage<T, MODE>(g, io, i, U, lu, rres, strips);
     if (i & 1)
       adj_step<RPT, T, MODE, false>(g, c, st, lb, la, ub, ua, acc, i, U, lu, B1, tx_bytes, io, hist,
                                     N2);
@@ -1138,7 +1160,8 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   double* dst = acc_part + (size_t)(lu + acc_off) * N2;
 #pragma unroll
   for (int j = 0; j < RPT; ++j)
-    if (st.active & (1u << j)) dst[(size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = acc[j];
+    if (st.active & (1u << j))
+      dst[(size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = accd[j] + (double)acc[j];
 }
 
 // ---------------------------------------------------------------------------
@@ -1156,55 +1179,55 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
 // kLapDepth steps ahead with cp.async.bulk (global -> shared) completing on a
 // per-slot mbarrier.  No per-thread global address arithmetic in the step.
 template <int RPT, class T, bool FULL, bool PLAIN, bool UNIF, bool IO, bool IMG>
-__device__ __forceinline__ void adjlap_body(const CellCtx& c, const CellStatic<RPT>& s,
-                                            double (&l1)[RPT], double (&l2)[RPT],
-                                            double (&acc)[RPT], int i, const AdjBufs<T>& B,
-                                            const IoStage& io, const float* lr, int nz) {
+__device__ __forceinline__ void adjlap_body(const CellCtx& c, const CellStatic<RPT, T>& s,
+                                            T (&l1)[RPT], T (&l2)[RPT],
+                                            T (&acc)[RPT], int i, const AdjBufs<T>& B,
+                                            const IoStage<T>& io, const float* lr, int nz) {
   const int RS = c.RS;
   const int k = i % kStage;
-  double el[RPT], lam[RPT];
-  const double2 ab0 = (!PLAIN && UNIF) ? s.ab[0] : make_double2(2.0, -1.0);
+  T el[RPT], lam[RPT];
+  const pair_t<T> ab0 = (!PLAIN && UNIF) ? s.ab[0] : free_pair<T>();
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) el[j] = __dmul_rn(s.ed[j], l1[j]);
+  for (int j = 0; j < RPT; ++j) el[j] = mul_s(s.ed[j], l1[j]);
   const T* pc = B.lr + c.xo;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    const double xm = j > 0 ? el[j - 1] : (double)pc[-1];
+    const T xm = j > 0 ? el[j - 1] : (T)pc[-1];
     const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
-    const double xp = own_next ? el[j + 1] : (double)pc[j + 1];
-    const double adj = lap5(el[j], xm, xp, (double)pc[j - RS], (double)pc[j + RS]);
+    const T xp = own_next ? el[j + 1] : (T)pc[j + 1];
+    const T adj = lap_s(el[j], xm, xp, (T)pc[j - RS], (T)pc[j + RS]);
     if (PLAIN) {
-      lam[j] = adj_update_free(l1[j], l2[j], adj);
+      lam[j] = adjs_free(l1[j], l2[j], adj);
     } else {
-      const double2 ab = UNIF ? ab0 : s.ab[j];
-      lam[j] = adj_update(ab.x, ab.y, l1[j], l2[j], adj);
+      const pair_t<T> ab = UNIF ? ab0 : s.ab[j];
+      lam[j] = adjs_ab(ab, l1[j], l2[j], adj);
     }
   }
   if ((!PLAIN || IO) && s.rmask) {
-    const double* r = io.srec + (size_t)k * io.maxrec + s.rbase;
+    const T* r = io.srec + (size_t)k * io.maxrec + s.rbase;
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) lam[j] = __dadd_rn(lam[j], r[j]);
+    for (int j = 0; j < RPT; ++j) lam[j] = add_s(lam[j], r[j]);
   }
   T* ql = B.lw + c.xo;
-  double elw[RPT];
+  T elw[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    elw[j] = __dmul_rn(s.ed[j], lam[j]);
+    elw[j] = mul_s(s.ed[j], lam[j]);
     if (!FULL && !(s.active & (1u << j))) continue;
     l2[j] = lam[j];
     ql[j] = (T)elw[j];
     if (IMG && (PLAIN || ((s.interior >> j) & 1u)))
-      acc[j] = __fma_rn((double)lr[j * nz], lam[j], acc[j]);
+      acc[j] = fma_s((T)lr[j * nz], lam[j], acc[j]);
   }
   push_edges<RPT, T>(c, s, B.lwb, B.bar_wb, elw, FULL);
 }
 
 template <int RPT, class T, bool IMG>
 __device__ __forceinline__ void adjlap_step(const Geo& g, const CellCtx& c,
-                                            const CellStatic<RPT>& s, double (&l1)[RPT],
-                                            double (&l2)[RPT], double (&acc)[RPT], int i,
+                                            const CellStatic<RPT, T>& s, T (&l1)[RPT],
+                                            T (&l2)[RPT], T (&acc)[RPT], int i,
                                             const AdjBufs<T>& B, uint32_t tx_bytes,
-                                            const IoStage& io, const BoxRows& br, int rows,
+                                            const IoStage<T>& io, const BoxRows& br, int rows,
                                             const float* ring, uint32_t ring_sa, uint32_t ringbar,
                                             const float* hbox, size_t hstep, int lofs) {
 #ifdef DUFWI_EXP_TIMING
@@ -1255,7 +1278,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const uint32_t bar[2] = {smem_addr(&bars[0]), smem_addr(&bars[1])};
   order_columns<T>(g, c, txx, txz, reinterpret_cast<int*>(smem), RPT, DUFWI_PLACE_ADJ);
   for (size_t k = threadIdx.x; k < 2 * xe; k += blockDim.x) XL[0][k] = T(0);
-  const IoStage io = io_stage(smem + io_offset<T>(rows, RPT, g.nz, 2), maxrec, 0);
+  const IoStage<T> io = io_stage<T>(smem + io_offset<T>(rows, RPT, g.nz, 2), maxrec, 0);
   unsigned char* rbase = smem + lap_ring_offset<T>(rows, RPT, g.nz, maxrec);
   const uint32_t ringbar = smem_addr(rbase);
   const float* ring = reinterpret_cast<const float*>(rbase + 32);
@@ -1272,17 +1295,21 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
     for (int d = 0; d < kLapDepth; ++d) lap_load(g, br, rows, d, ring_sa, ringbar, hbox, hstep);
   }
   __syncthreads();
-  CellStatic<RPT> st;
-  load_static<RPT>(g, m, c, pb, txx, txz,
-                   reinterpret_cast<double2*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)), io, true,
+  CellStatic<RPT, T> st;
+  load_static<RPT, T>(g, m, c, pb, txx, txz,
+                   reinterpret_cast<pair_t<T>*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)), io, true,
                    st);
   const uint32_t tx_bytes = (uint32_t)(((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T));
   const int nt = g.nt;
   // the thread's first cell in a ring slot (slots hold the box rows from b0)
   const int lofs = (c.r0 + c.lrow0 - br.b0) * g.nz + c.z;
-  double la[RPT], lb[RPT], acc[RPT];
+  T la[RPT], lb[RPT], acc[RPT];
+  double accd[RPT];
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) la[j] = lb[j] = acc[j] = 0.0;
+  for (int j = 0; j < RPT; ++j) {
+    la[j] = lb[j] = acc[j] = T(0);
+    accd[j] = 0.0;
+  }
   cluster_sync_all();
 
   const uint32_t xsz = (uint32_t)(xe * sizeof(T));
@@ -1293,12 +1320,13 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
                            ringbar, hbox, hstep, lofs)
   int i = 0;
   for (; i + 1 < nt - 1; i += 2) {  // steps with t >= 1: imaging
-    if (i % kStage == 0) prefetch_stage<1>(g, io, i, U, lu, rres, nullptr);
+    if (i % kAccBlock == 0) acc_flush<RPT>(acc, accd);
+    if (i % kStage == 0) prefetch_stage<T, 1>(g, io, i, U, lu, rres, nullptr);
     DUFWI_ADJLAP(true, la, lb, B0, i);
     DUFWI_ADJLAP(true, lb, la, B1, i + 1);
   }
   for (; i < nt; ++i) {
-    if (i % kStage == 0) prefetch_stage<1>(g, io, i, U, lu, rres, nullptr);
+    if (i % kStage == 0) prefetch_stage<T, 1>(g, io, i, U, lu, rres, nullptr);
     const bool img = nt - 1 - i >= 1;
     if (i & 1) {
       if (img) DUFWI_ADJLAP(true, lb, la, B1, i); else DUFWI_ADJLAP(false, lb, la, B1, i);
@@ -1312,7 +1340,8 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   double* dst = acc_part + (size_t)(lu + acc_off) * N2;
 #pragma unroll
   for (int j = 0; j < RPT; ++j)
-    if (st.active & (1u << j)) dst[(size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = acc[j];
+    if (st.active & (1u << j))
+      dst[(size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = accd[j] + (double)acc[j];
 }
 
 // ------------------------------------------------------------------ host side
@@ -1403,6 +1432,13 @@ inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, 
   n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 2>, cs, threads, sa));
   n = std::min(n, max_active_clusters(cluster_adjlap_kernel<RPT, T>, cs, threads, sl));
   if (n <= 0) return false;
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cluster_adj_kernel<RPT, T, 2>, threads,
+                                                    sa) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  out->per_sm = std::max(1, per_sm);
   out->cs = cs;
   out->rows = rows;
   out->rpt = RPT;
@@ -1428,10 +1464,11 @@ inline bool try_cluster_rpt(const Geo& g, int cs, int rpt, const std::vector<int
   switch (rpt) {
     case 2: return try_cluster_cfg<2, T>(g, cs, rxn, out);
     case 4: return try_cluster_cfg<4, T>(g, cs, rxn, out);
-    case 5: return sizeof(T) == 8 && try_cluster_cfg<5, double>(g, cs, rxn, out);
-    case 6: return sizeof(T) == 8 && try_cluster_cfg<6, double>(g, cs, rxn, out);
-    case 7: return sizeof(T) == 8 && try_cluster_cfg<7, double>(g, cs, rxn, out);
-    case 8: return sizeof(T) == 8 && try_cluster_cfg<8, double>(g, cs, rxn, out);
+    case 8: return try_cluster_cfg<8, T>(g, cs, rxn, out);
+    // (f64 arithmetic, the precise variant: 2 / 4 / 8 rows per thread only)
+    case 5: return sizeof(T) == 4 && try_cluster_cfg<5, float>(g, cs, rxn, out);
+    case 6: return sizeof(T) == 4 && try_cluster_cfg<6, float>(g, cs, rxn, out);
+    case 7: return sizeof(T) == 4 && try_cluster_cfg<7, float>(g, cs, rxn, out);
     default: return false;
   }
 }
@@ -1439,7 +1476,7 @@ inline bool try_cluster_rpt(const Geo& g, int cs, int rpt, const std::vector<int
 // Every launch shape that fits: cluster sizes 16 .. 2, each with the fewest
 // rows per thread that fit the thread budget and any larger count that splits
 // the slab exactly.  DUFWI_CLUSTER_CS / DUFWI_CLUSTER_RPT pin them (experiments).
-inline bool cluster_candidates(const Geo& g, bool rho, const std::vector<int2>& rxn,
+inline bool cluster_candidates(const Geo& g, bool rho, bool f64, const std::vector<int2>& rxn,
                                std::vector<ClusterCfg>& out) {
   out.clear();
   if (rho) return false;  // density runs on the stepwise engine
@@ -1466,10 +1503,8 @@ inline bool cluster_candidates(const Geo& g, bool rho, const std::vector<int2>& 
       first = false;
       if (!take) continue;
       ClusterCfg c;
-#ifndef DUFWI_EXCHANGE_F32
-      if (try_cluster_rpt<double>(g, cs, r, rxn, &c)) { out.push_back(c); continue; }
-#endif
-      if (try_cluster_rpt<float>(g, cs, r, rxn, &c)) out.push_back(c);
+      if (f64 ? try_cluster_rpt<double>(g, cs, r, rxn, &c) : try_cluster_rpt<float>(g, cs, r, rxn, &c))
+        out.push_back(c);
     }
   }
   return !out.empty();
@@ -1480,11 +1515,18 @@ inline bool cluster_candidates(const Geo& g, bool rho, const std::vector<int2>& 
 // run fewer warps with more register pressure (x1.05).  Measured on config 1
 // (forward + adjoint ms): 16 rows as 2 x 8 (0.84 + 1.71) < 18 as 3 x 6
 // (0.87 + 1.82) < 18 slots as 3 x 6 with 16 rows used.
-inline double cluster_cost(const ClusterCfg& c) {
+inline double cluster_cost(const ClusterCfg& c, int U) {
   double cost = (double)c.nseg * c.rpt;
   if (c.rows % c.rpt) cost *= 1.3;
   if (c.rpt >= 7) cost *= 1.05;
-  return cost;
+  // Co-residency counts clusters that SHARE SMs (several CTAs per SM): only
+  // maxc / per_sm clusters get SMs of their own, and a step is as slow as the
+  // busiest SM.  Measured (f32, config 1, 8 units, fwd / adj ms with the L(u)
+  // store): 10 CTAs x 16 rows, 11 resident at 1 CTA/SM: 0.81 / 0.78; 16 CTAs x
+  // 10 rows, 14 resident at 2 CTAs/SM (7 GPCs hold a 16-CTA cluster): 0.90 / 0.93.
+  const int own = std::max(1, c.maxc / std::max(1, c.per_sm));
+  const int share = std::min(c.per_sm, (U + own - 1) / own);
+  return cost * std::max(1, share);
 }
 
 // Launch shape for U units: the fewest waves of co-resident clusters (a unit's
@@ -1502,12 +1544,13 @@ inline const ClusterCfg& pick_cluster(const std::vector<ClusterCfg>& c, int U,
   long best_w = -1;
   double best_c = 0.0;
   bool any = false;
+  // (f64 forward: the <= 512-thread shapes measured faster; f32: 640 threads as well)
   for (size_t i = 0; i < c.size(); ++i)
-    if (adjoint || c[i].threads <= 512) any = true;
+    if (adjoint || !c[i].dbl || c[i].threads <= 512) any = true;
   for (size_t i = 0; i < c.size(); ++i) {
-    if (any && !adjoint && c[i].threads > 512) continue;
+    if (any && !adjoint && c[i].dbl && c[i].threads > 512) continue;
     const long w = (U + c[i].maxc - 1) / c[i].maxc;
-    double k = cluster_cost(c[i]);
+    double k = cluster_cost(c[i], U);
     if (adjoint) {
       const int W = (c[i].threads + 31) / 32;
       k *= (double)((W + 3) / 4) / (W / 4.0);
@@ -1578,11 +1621,13 @@ inline cudaError_t cluster_adjoint_t(const Geo& g, const Model& m, const Cluster
 #define DUFWI_CLUSTER_DISPATCH(FN, ...)                                        \
   (c.dbl ? (c.rpt == 2   ? FN<2, double>(__VA_ARGS__)                          \
             : c.rpt == 4 ? FN<4, double>(__VA_ARGS__)                          \
-            : c.rpt == 5 ? FN<5, double>(__VA_ARGS__)                          \
-            : c.rpt == 6 ? FN<6, double>(__VA_ARGS__)                          \
-            : c.rpt == 7 ? FN<7, double>(__VA_ARGS__)                          \
                          : FN<8, double>(__VA_ARGS__))                         \
-         : (c.rpt == 2 ? FN<2, float>(__VA_ARGS__) : FN<4, float>(__VA_ARGS__)))
+         : (c.rpt == 2   ? FN<2, float>(__VA_ARGS__)                           \
+            : c.rpt == 4 ? FN<4, float>(__VA_ARGS__)                           \
+            : c.rpt == 5 ? FN<5, float>(__VA_ARGS__)                           \
+            : c.rpt == 6 ? FN<6, float>(__VA_ARGS__)                           \
+            : c.rpt == 7 ? FN<7, float>(__VA_ARGS__)                           \
+                         : FN<8, float>(__VA_ARGS__)))
 
 inline int cluster_forward(const Geo& g, const Model& m, const ClusterCfg& c, int mode,
                            int unit_begin, int U, float* rec, float* hist, float* strips,

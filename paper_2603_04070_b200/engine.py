@@ -32,6 +32,8 @@ __all__ = ["PhysicsEngine", "shard_range", "NonFiniteResult", "STORE_NONE", "STO
 
 _ENGINES = {"auto": _lib.ENGINE_AUTO, "stepwise": _lib.ENGINE_STEPWISE,
             "cluster": _lib.ENGINE_CLUSTER}
+#: include/dufwi.h DUFWI_ARITH_*: arithmetic of the sweep kernels
+_ARITH = {"f32": 0, "f64": 1}
 
 
 class NonFiniteResult(FloatingPointError):
@@ -98,7 +100,7 @@ class PhysicsEngine:
     def __init__(self, *, nx: int, nz: int, nt: int, dx: float, dt: float,
                  tx_nodes, rx_nodes, pulse, element_nodes=None,
                  damping_values=None, damping_profiles=None, n_phantoms: int = 1,
-                 has_rho: bool = False, engine: str = "auto", device=None,
+                 has_rho: bool = False, engine: str = "auto", arith: str = "f32", device=None,
                  max_chunk_units: int | None = None, memory_fraction: float = 0.55):
         self._plan = None
         so = _lib.lib()
@@ -127,6 +129,10 @@ class PhysicsEngine:
         geo.n_phantoms, geo.n_shots, geo.n_rx, geo.n_elements = self.B, self.S, self.R, el.shape[0]
         geo.has_rho = int(self.has_rho)
         geo.engine = _ENGINES[engine]
+        if arith not in _ARITH:
+            raise ValueError(f"arith must be one of {sorted(_ARITH)}")
+        self.arith = arith
+        geo.arith = _ARITH[arith]
         geo.dx, geo.dt = self.dx, self.dt
         keep = [tx, rx, el, pulse]
         I32P, F64P = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)

@@ -275,15 +275,19 @@ def _digest(*parts) -> str:
 
 def get_engine(grid: Grid2D, tx_nodes, rx_nodes, element_nodes, pulse: np.ndarray,
                damping: DampingProfile, n_phantoms: int = 1, has_rho: bool = False,
-               engine: str = "auto"):
-    """Cached :class:`~paper_2603_04070_b200.engine.PhysicsEngine` for an acquisition."""
+               engine: str = "auto", arith: str = "f32"):
+    """Cached :class:`~paper_2603_04070_b200.engine.PhysicsEngine` for an acquisition.
+
+    ``arith``: "f32" (default; the increment-form f32 kernels, inside the north-star
+    tolerances) or "f64" (the reference's operation order in f64; misfit differencing
+    and convergence studies, include/dufwi.h DUFWI_ARITH_*)."""
     import torch
 
     from .engine import PhysicsEngine
 
     dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
     key = _digest(grid, np.asarray(tx_nodes), np.asarray(rx_nodes), np.asarray(element_nodes),
-                  np.asarray(pulse), damping.values, n_phantoms, has_rho, engine, dev)
+                  np.asarray(pulse), damping.values, n_phantoms, has_rho, engine, arith, dev)
     eng = _ENGINE_CACHE.get(key)
     if eng is None:
         prof = damping.profiles
@@ -291,7 +295,7 @@ def get_engine(grid: Grid2D, tx_nodes, rx_nodes, element_nodes, pulse: np.ndarra
                             tx_nodes=tx_nodes, rx_nodes=rx_nodes, element_nodes=element_nodes,
                             pulse=pulse, damping_profiles=prof,
                             damping_values=None if prof is not None else damping.values,
-                            n_phantoms=n_phantoms, has_rho=has_rho, engine=engine)
+                            n_phantoms=n_phantoms, has_rho=has_rho, engine=engine, arith=arith)
         _ENGINE_CACHE[key] = eng
         while len(_ENGINE_CACHE) > _ENGINE_CACHE_SIZE:
             _ENGINE_CACHE.popitem(last=False)

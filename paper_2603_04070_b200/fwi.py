@@ -222,7 +222,7 @@ class _DataTerm:
                 raise ValueError("batched FWI needs one acquisition geometry")
         self.grid = grid
         self.eng = get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes,
-                              pulse.samples, damping, n_phantoms=len(m_obs_list))
+                              pulse.samples, damping, n_phantoms=len(m_obs_list), arith="f64")
         self.obs = torch.from_numpy(np.concatenate(
             [np.require(m.traces, np.float64, ["C", "W"]) for m in m_obs_list])).to(self.eng.device)
         self.limit = grid.dx / (grid.dt * np.sqrt(2.0))  # check_cfl bound (grid.py:242-251)
