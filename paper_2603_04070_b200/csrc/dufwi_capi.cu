@@ -14,6 +14,7 @@
 #include "dufwi_step_kernels.cuh"
 #include "dufwi_vec_kernels.cuh"
 #include "dufwi_lean_kernels.cuh"
+#include "dufwi_tile_kernels.cuh"
 
 using namespace dufwi;
 
@@ -82,6 +83,11 @@ struct dufwi_plan {
   bool lean_on = true;  // lean stepwise kernels (DUFWI_LEAN=0: the first vec/stream kernels)
   double *Er = nullptr, *fxe = nullptr, *fz = nullptr, *fz0 = nullptr;  // density tables
   float *Edf = nullptr, *Erf = nullptr, *qf = nullptr;  // f32 coefficient streams (lean kernels)
+  // f32 tile kernels (DUFWI_ARITH_F32 stepwise path, dufwi_tile_kernels.cuh)
+  TileTabs tile{};       // f32 damping tables, receiver-tile flags
+  float* hq = nullptr;   // q / 2, replicate-padded [B][nx+2][nz+8]
+  bool tile_ok = false;  // tensor maps can be encoded and the tables exist
+  bool tile_on = true;   // DUFWI_TILE=0: the f64 lean kernels instead (A/B timing)
 };
 
 namespace {
@@ -149,8 +155,17 @@ Groups fwd_groups(const Geo& g, int unit_begin, int U) { return make_groups(g, u
 // Adjoint: as many shots per group as the warp target allows (one f64
 // accumulator read-modify-write per cell, group and step).
 Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec, bool lean,
-                  int sms) {
+                  int sms, bool tile = false) {
   if (per_unit) return make_groups(g, unit_begin, U, 1);
+  if (tile) {
+    // tile imaging kernel: a CTA per (box tile, group) walks the group's shots;
+    // enough groups for ~8 CTAs per SM, at most 64 shots per group (f32 partial
+    // sums), at least 4 (the accumulator costs 16 B / gs per cell update)
+    const long tiles = (long)((g.Lz + 2 + kTZ - 1) / kTZ + 1) * ((g.Lx + 2 + kTX - 1) / kTX + 1);
+    const long want = std::max(1L, ((long)sms * 8 + tiles - 1) / tiles);
+    const int gs = (int)std::min(64L, std::max(4L, (long)U / want));
+    return make_groups(g, unit_begin, U, gs);
+  }
   // lean imaging kernel: ~8 groups, enough CTAs for several waves; the
   // accumulator read-modify-write costs 16 B / gs per cell update
   if (lean) return make_groups(g, unit_begin, U, std::max(1, (U + 7) / 8));
@@ -172,9 +187,66 @@ bool use_vec(const dufwi_plan_t* p) { return !p->has_rho && p->geo.nz % 4 == 0; 
 bool use_lean(const dufwi_plan_t* p) {
   return p->geo.nz % 4 == 0 && p->ab.px && p->box_ok && p->lean_on;
 }
+// f32 tile kernels: the lean kernels' domain (nz % 4 == 0 makes every row a
+// multiple of 16 bytes for the tensor maps), f32 arithmetic
+bool use_tile(const dufwi_plan_t* p) {
+  return p->arith == DUFWI_ARITH_F32 && use_lean(p) && p->tile_ok && p->tile_on;
+}
+
+// Tensor maps of one sweep call: a workspace region [slots][U][nx][nz] gets a
+// halo'd and a plain map, valid for every step and unit of the call; the
+// coefficient maps cover the plan's per-phantom arrays.
+struct TileRegion {
+  const float* base = nullptr;
+  size_t slots = 0;
+  CUtensorMap halo, plain;
+};
+struct TileCtx {
+  TileRegion ubuf, lbuf, hist, snap;
+  CUtensorMap e_plain, e_halo, h_halo;
+  size_t fieldU = 0;
+  bool ok = false;
+  // region and slot of a field pointer handed to a step launch
+  const TileRegion* find(const float* ptr, int* slot) const {
+    for (const TileRegion* r : {&ubuf, &lbuf, &hist, &snap}) {
+      if (!r->base || ptr < r->base || ptr >= r->base + r->slots * fieldU) continue;
+      *slot = (int)((ptr - r->base) / fieldU);
+      return r;
+    }
+    return nullptr;
+  }
+};
+
+bool tile_region(const dufwi_plan_t* p, TileRegion& r, const float* base, size_t slots, int U) {
+  const Geo& g = p->geo;
+  r.base = base;
+  r.slots = slots;
+  if (!base || !slots) { r.base = nullptr; return true; }
+  return make_tile_map(&r.halo, base, g.nz, g.nx, (size_t)U, slots, true) &&
+         make_tile_map(&r.plain, base, g.nz, g.nx, (size_t)U, slots, false);
+}
+
+void tile_ctx_build(const dufwi_plan_t* p, int U, const float* ubuf, const float* lbuf,
+                    const float* hist, size_t hist_slots, const float* snap, size_t snap_slots,
+                    TileCtx& c) {
+  const Geo& g = p->geo;
+  c.ok = false;
+  if (!use_tile(p)) return;
+  c.fieldU = (size_t)U * g.nx * g.nz;
+  const float* E = p->has_rho ? p->Erf : p->Edf;
+  bool ok = tile_region(p, c.ubuf, ubuf, 2, U) && tile_region(p, c.lbuf, lbuf, lbuf ? 2 : 0, U) &&
+            tile_region(p, c.hist, hist, hist_slots, U) && tile_region(p, c.snap, snap, snap_slots, U);
+  ok = ok && make_tile_map(&c.e_plain, E, g.nz, g.nx, (size_t)g.B, 0, false) &&
+       make_tile_map(&c.e_halo, E, g.nz, g.nx, (size_t)g.B, 0, true);
+  if (p->has_rho)
+    ok = ok && make_tile_map(&c.h_halo, p->hq, g.nz + 8, g.nx + 2, (size_t)g.B, 0, true);
+  else
+    c.h_halo = c.e_halo;  // never dereferenced without density
+  c.ok = ok;
+}
 
 Groups groups_for(const dufwi_plan_t* p, int unit_begin, int U, bool per_unit) {
-  return adj_groups(p->geo, unit_begin, U, per_unit, use_vec(p), use_lean(p), p->sms);
+  return adj_groups(p->geo, unit_begin, U, per_unit, use_vec(p), use_lean(p), p->sms, use_tile(p));
 }
 
 // Upper bound of the group count over every placement of U units.
@@ -370,6 +442,46 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
       if (!rc) { p->ab.A2 = dA2; p->ab.B2 = dB2; }
     }
   }
+  if (geo->px_host) {
+    // f32 increment-form tables: ramps and (A - 2, B + 1) per axis, rounded once from f64
+    auto inc_host = [&](const double* prof, int n, std::vector<float>& pf, std::vector<float>& a2,
+                        std::vector<float>& b1) {
+      pf.resize(n); a2.resize(n); b1.resize(n);
+      for (int i = 0; i < n; ++i) {
+        const double D = prof[i];
+        double A = 2.0, B = -1.0;
+        if (D != 0.0) {
+          const double ddt = D * geo->dt, den = 1.0 + ddt;
+          A = (2.0 - ddt * ddt) / den;
+          B = (ddt - 1.0) / den;
+        }
+        pf[i] = (float)D;
+        if (D != 0.0 && pf[i] == 0.f) pf[i] = 1e-30f;  // keep "damped" distinguishable after rounding
+        a2[i] = (float)(A - 2.0);
+        b1[i] = (float)(B + 1.0);
+      }
+    };
+    std::vector<float> pf, a2, b1;
+    float *dp, *da, *db;
+    inc_host(geo->px_host, nx, pf, a2, b1);
+    rc = rc ? rc : upload(p, &dp, pf.data(), nx);
+    rc = rc ? rc : upload(p, &da, a2.data(), nx);
+    rc = rc ? rc : upload(p, &db, b1.data(), nx);
+    if (!rc) { p->tile.px = dp; p->tile.a2x = da; p->tile.b1x = db; }
+    inc_host(geo->pz_host, nz, pf, a2, b1);
+    rc = rc ? rc : upload(p, &dp, pf.data(), nz);
+    rc = rc ? rc : upload(p, &da, a2.data(), nz);
+    rc = rc ? rc : upload(p, &db, b1.data(), nz);
+    if (!rc) { p->tile.pz = dp; p->tile.a2z = da; p->tile.b1z = db; }
+    // tiles holding a receiver node
+    const int tzn = (nz + kTZ - 1) / kTZ, txn = (nx + kTX - 1) / kTX;
+    std::vector<unsigned char> trx((size_t)tzn * txn, 0);
+    for (int i = 0; i < S * R; ++i)
+      trx[(size_t)(geo->rx_host[2 * i] / kTX) * tzn + geo->rx_host[2 * i + 1] / kTZ] = 1;
+    unsigned char* dt_ = nullptr;
+    rc = rc ? rc : upload(p, &dt_, trx.data(), trx.size());
+    if (!rc) p->tile.tile_rx = dt_;
+  }
   rc = rc ? rc : upload(p, &p->pulse, geo->pulse_host, geo->nt);
   rc = rc ? rc : upload(p, &p->tx, geo->tx_host, 2 * (size_t)S);
   rc = rc ? rc : upload(p, &p->rx_slot, rx_slot.data(), rx_slot.size());
@@ -392,6 +504,7 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
     rc = rc ? rc : dev_alloc(p, &p->fxe, (size_t)g.B * (nx + 1) * nz);
     rc = rc ? rc : dev_alloc(p, &p->fz, BN2);
     rc = rc ? rc : dev_alloc(p, &p->fz0, (size_t)g.B * nx);
+    rc = rc ? rc : dev_alloc(p, &p->hq, (size_t)g.B * (nx + 2) * (nz + 8));
   }
   rc = rc ? rc : dev_alloc(p, &p->flag, 4);
   if (!rc && cudaMemset(p->flag, 0, 4 * sizeof(int)) != cudaSuccess)
@@ -412,6 +525,17 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   g.col_flag = p->col_flag;
   if (const char* e = getenv("DUFWI_LEAN")) p->lean_on = atoi(e) != 0;
   if (const char* e = getenv("DUFWI_LEAN_TX")) p->lean_tx = std::max(0, atoi(e));
+  if (const char* e = getenv("DUFWI_TILE")) p->tile_on = atoi(e) != 0;
+  p->tile_ok = p->tile.px && encode_tiled_fn() != nullptr;
+  {
+    auto big = [](const void* f, size_t bytes) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    };
+    big((const void*)tile_img_kernel<false, 1>, TileImgSmem::bytes(false));
+    big((const void*)tile_img_kernel<false, 2>, TileImgSmem::bytes(false));
+    big((const void*)tile_img_kernel<true, 1>, TileImgSmem::bytes(true));
+    big((const void*)tile_img_kernel<true, 2>, TileImgSmem::bytes(true));
+  }
   {  // lean rings may exceed the 48 KB default of dynamic shared memory
     auto big = [](const void* f, size_t bytes) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -463,6 +587,10 @@ extern "C" int dufwi_set_model(dufwi_plan_t* p, const double* c_dev, const doubl
     const int b2 = (int)std::min<size_t>((te + threads - 1) / threads, (size_t)p->sms * 16);
     rho_faces_kernel<<<b2, threads, 0, (cudaStream_t)stream>>>(g, g.B, p->Ed, p->rho, p->q, p->Er,
                                                                p->fxe, p->fz, p->fz0, p->Erf);
+    LAUNCH_CHECK(p);
+    const size_t th = (size_t)g.B * (g.nx + 2) * (g.nz + 8);
+    const int b3 = (int)std::min<size_t>((th + threads - 1) / threads, (size_t)p->sms * 16);
+    hq_pad_kernel<<<b3, threads, 0, (cudaStream_t)stream>>>(g, g.B, p->qf, p->hq);
     LAUNCH_CHECK(p);
   }
   return DUFWI_OK;
@@ -516,8 +644,28 @@ int stepwise_tx(const dufwi_plan_t* p, int U) {
 // exist), receiver samples -> rec_t, ring strips -> st_t (kmode 2).
 int fwd_step_launch(dufwi_plan_t* p, const Model& m, int kmode, int t, int unit_begin, int U,
                     const float* u1, const float* u2, float* uo, float* rec_t, float* st_t,
-                    int has1, int has2, cudaStream_t st) {
+                    int has1, int has2, cudaStream_t st, const TileCtx* tc = nullptr) {
   const Geo& g = p->geo;
+  if (tc && tc->ok) {
+    // f32 tile kernels: operands by tensor map (region + slot), output by pointer
+    int s1 = 0, s2 = 0;
+    const TileRegion* r1 = tc->find(u1, &s1);
+    const TileRegion* r2 = tc->find(u2, &s2);
+    if (!r1 || !r2) return fail(DUFWI_EINVAL, "tile forward: operand outside the mapped regions");
+    const dim3 tgrid((g.nz + kTZ - 1) / kTZ, (g.nx + kTX - 1) / kTX, U);
+#define DUFWI_TILE_FWD(R, M)                                                                     \
+  tile_fwd_kernel<R, M><<<tgrid, kTT, TileFwdSmem::bytes(R), st>>>(                              \
+      r1->halo, r2->plain, tc->e_plain, tc->h_halo, g, p->tile, t, unit_begin, s1, s2, has1, has2, \
+      uo, rec_t, st_t)
+    if (p->has_rho) {
+      if (kmode == 2) DUFWI_TILE_FWD(true, 2); else DUFWI_TILE_FWD(true, 0);
+    } else {
+      if (kmode == 2) DUFWI_TILE_FWD(false, 2); else DUFWI_TILE_FWD(false, 0);
+    }
+#undef DUFWI_TILE_FWD
+    LAUNCH_CHECK(p);
+    return 0;
+  }
   const Groups G = fwd_groups(g, unit_begin, U);
   const int vtx = stepwise_tx(p, U);
   const dim3 vgrid((g.nz + 127) / 128, (g.nx + kPipeWarps * vtx - 1) / (kPipeWarps * vtx), U);
@@ -561,10 +709,55 @@ int fwd_step_launch(dufwi_plan_t* p, const Model& m, int kmode, int t, int unit_
 int adj_step_launch(dufwi_plan_t* p, const Model& m, int kmode, int t, int unit_begin, int U,
                     const Groups& G, const float* l1, float* l2o, const double* rres_t,
                     const float* F, float* ut, const float* utm1, const float* st_tm1,
-                    const float* st_tm2, double* acc_part, cudaStream_t st) {
+                    const float* st_tm2, double* acc_part, cudaStream_t st,
+                    const TileCtx* tc = nullptr) {
   const Geo& g = p->geo;
   const int has1 = t <= g.nt - 2, has2 = t <= g.nt - 3;
   const int do_img = t >= 1, do_recon = t >= 2;
+  if (tc && tc->ok) {
+    int s1 = 0, s2 = 0;
+    const TileRegion* r1 = tc->find(l1, &s1);
+    const TileRegion* r2 = tc->find(l2o, &s2);
+    if (!r1 || !r2) return fail(DUFWI_EINVAL, "tile adjoint: operand outside the mapped regions");
+    const dim3 tgrid((g.nz + kTZ - 1) / kTZ, (g.nx + kTX - 1) / kTX, U);
+    if (p->has_rho)
+      tile_adj_kernel<true><<<tgrid, kTT, TileAdjSmem::bytes(true), st>>>(
+          r1->halo, r2->plain, tc->e_halo, tc->h_halo, g, p->tile, unit_begin, s1, s2, has1, has2,
+          l2o, rres_t);
+    else
+      tile_adj_kernel<false><<<tgrid, kTT, TileAdjSmem::bytes(false), st>>>(
+          r1->halo, r2->plain, tc->e_halo, tc->h_halo, g, p->tile, unit_begin, s1, s2, has1, has2,
+          l2o, rres_t);
+    LAUNCH_CHECK(p);
+    if (do_img) {
+      // imaging operand u[t-1]: the full history (kmode 1) or the field buffer
+      int su = 0, sut = 0;
+      const TileRegion* ru = tc->find(kmode == 1 ? F : utm1, &su);
+      const TileRegion* rt = tc->find(ut, &sut);
+      if (!ru || !rt) return fail(DUFWI_EINVAL, "tile imaging: operand outside the mapped regions");
+      // tiles touching the undamped box and its 1-cell ring (kmode 2) / the whole grid
+      int tx0 = 0, tx1 = (g.nx - 1) / kTX, tz0 = 0, tz1 = (g.nz - 1) / kTZ;
+      if (kmode == 2) {
+        tx0 = std::max(0, g.x_lo - 1) / kTX;
+        tx1 = std::min(g.nx - 1, g.x_hi + 1) / kTX;
+        tz0 = std::max(0, g.z_lo - 1) / kTZ;
+        tz1 = std::min(g.nz - 1, g.z_hi + 1) / kTZ;
+      }
+      const dim3 igrid(tz1 - tz0 + 1, tx1 - tx0 + 1, G.ngroups);
+#define DUFWI_TILE_IMG(R, M)                                                                    \
+  tile_img_kernel<R, M><<<igrid, kTT, TileImgSmem::bytes(R), st>>>(                             \
+      ru->halo, r2->plain, rt->plain, tc->e_plain, tc->h_halo, g, t, unit_begin, U, G.gs, su, s2, \
+      sut, tx0, tz0, ut, st_tm2, acc_part, do_recon)
+      if (kmode == 1) {
+        if (p->has_rho) DUFWI_TILE_IMG(true, 1); else DUFWI_TILE_IMG(false, 1);
+      } else {
+        if (p->has_rho) DUFWI_TILE_IMG(true, 2); else DUFWI_TILE_IMG(false, 2);
+      }
+#undef DUFWI_TILE_IMG
+      LAUNCH_CHECK(p);
+    }
+    return 0;
+  }
   const int vtx = stepwise_tx(p, U);
   if (use_lean(p)) {
     // split adjoint: lam update (12 B/update) then imaging + reconstruction
@@ -670,6 +863,9 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   } else {
     p->last_engine = DUFWI_ENGINE_STEPWISE;
     const int K = ck_len(g.nt);
+    TileCtx tc;
+    tile_ctx_build(p, U, ubuf, nullptr, mode == DUFWI_STORE_FULL ? hist : nullptr, (size_t)g.nt,
+                   nullptr, 0, tc);
     for (int t = 0; t < g.nt; ++t) {
       float* rec_t = rec + (size_t)t * U * g.M;
       const int has1 = t >= 1, has2 = t >= 2;
@@ -697,7 +893,7 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
         }
       }
       rc = fwd_step_launch(p, m, mode == DUFWI_STORE_STRIPS ? 2 : 0, t, unit_begin, U, u1, u2, uo,
-                           rec_t, st_t, has1, has2, st);
+                           rec_t, st_t, has1, has2, st, &tc);
       if (rc) return rc;
     }
   }
@@ -778,6 +974,13 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
   } else {
     p->last_engine = DUFWI_ENGINE_STEPWISE;
     CUDA_TRY(cudaMemsetAsync(acc_part, 0, (size_t)G.ngroups * N2 * sizeof(double), st));
+    TileCtx tc;
+    {
+      const bool ck = mode == DUFWI_STORE_CHECKPOINT;
+      const bool hh = mode == DUFWI_STORE_FULL || ck;
+      tile_ctx_build(p, U, ubuf, lbuf, hh ? hist : nullptr, ck ? (size_t)ck_len(g.nt) : (size_t)g.nt,
+                     ck ? snap : nullptr, ck ? (size_t)ck_segments(g.nt) * 2 : 0, tc);
+    }
     auto adj_step = [&](int t, const float* F) {
       const float* l1 = lbuf + (size_t)((t + 1) & 1) * fieldU;
       float* l2o = lbuf + (size_t)(t & 1) * fieldU;
@@ -788,7 +991,7 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
       const float* st_tm1 = (strip && t >= 1) ? strips + (size_t)(t - 1) * U * g.SL : nullptr;
       const float* st_tm2 = (strip && t >= 2) ? strips + (size_t)(t - 2) * U * g.SL : nullptr;
       return adj_step_launch(p, m, strip ? 2 : 1, t, unit_begin, U, G, l1, l2o, rres_t,
-                             t >= 1 ? F : nullptr, ut, utm1, st_tm1, st_tm2, acc_part, st);
+                             t >= 1 ? F : nullptr, ut, utm1, st_tm1, st_tm2, acc_part, st, &tc);
     };
     if (mode == DUFWI_STORE_CHECKPOINT) {
       // segments last to first: recompute the segment's fields u[s0-1 .. s1-2]
@@ -803,7 +1006,7 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
           const float* u1 = hist + (size_t)(t - s0) * fieldU;
           const float* u2 = t == s0 ? sp + fieldU : hist + (size_t)(t - s0 - 1) * fieldU;
           rc = fwd_step_launch(p, m, 0, t, unit_begin, U, u1, u2, hist + (size_t)(t - s0 + 1) * fieldU,
-                               rec + (size_t)t * U * g.M, nullptr, t >= 1, t >= 2, st);
+                               rec + (size_t)t * U * g.M, nullptr, t >= 1, t >= 2, st, &tc);
           if (rc) return rc;
         }
         for (int t = s1 - 1; t >= s0; --t) {
