@@ -1057,7 +1057,7 @@ extern "C" int32_t dufwi_plan_info(const dufwi_plan_t* p, int64_t* out, int32_t 
                          p->ccfg.threads, p->ccfg.dbl, (int64_t)p->ccfg.smem_fwd,
                          (int64_t)p->ccfg_adj.smem_adj, p->ccfg.maxc, p->ccfg_adj.cs,
                          p->ccfg_adj.rpt, p->ccfg_adj.threads,
-                         use_lean(p) ? 0 : use_vec(p) ? 1 : 2};
+                         use_tile(p) ? 3 : use_lean(p) ? 0 : use_vec(p) ? 1 : 2};
   const int k = n < 13 ? n : 13;
   for (int i = 0; i < k; ++i) out[i] = v[i];
   return k;

@@ -485,9 +485,14 @@ __global__ void __launch_bounds__(kTT)
 // with halo, lam[t], u[t]); the coefficient tiles E (and h) are loaded once
 // per CTA, the imaging sums stay in f32 registers for the group (gs terms) and
 // are added to the group's f64 accumulator once.
+#ifndef DUFWI_IMG_STAGES
+#define DUFWI_IMG_STAGES 2
+#endif
+constexpr int kImgStages = DUFWI_IMG_STAGES;  // 1: latency hidden across CTAs only; 2: next shot prefetched
+static_assert(kImgStages == 1 || kImgStages == 2, "imaging pipeline depth");
 struct TileImgSmem {
   static constexpr uint32_t stage = kHaloSlot + 2 * kPlainSlot;  // u1, lam, ut
-  static constexpr uint32_t e = 2 * stage, h = e + kPlainSlot;
+  static constexpr uint32_t e = kImgStages * stage, h = e + kPlainSlot;
   __host__ __device__ static constexpr uint32_t bar(bool rho) { return h + (rho ? kHaloSlot : 0u); }
   __host__ __device__ static constexpr uint32_t bytes(bool rho) { return bar(rho) + 32u; }
 };
@@ -590,8 +595,8 @@ __global__ void __launch_bounds__(kTT)
   const size_t N2 = (size_t)g.nx * g.nz;
   const uint32_t stage_bytes = kHaloBytes + kPlainBytes + (recon_on ? kPlainBytes : 0u);
   auto issue = [&](int k) {  // thread 0: the operands of the group's k-th shot
-    unsigned char* sb = tsm + (k & 1) * TileImgSmem::stage;
-    const uint32_t bk = bar + 8u * (k & 1);
+    unsigned char* sb = tsm + (k % kImgStages) * TileImgSmem::stage;
+    const uint32_t bk = bar + 8u * (k % kImgStages);
     const int lu = sg.lu0 + k;
     mbar_expect_tx(bk, stage_bytes);
     tma_load_4d(smem_addr(sb), &mU1, z0 - 4, x0 - 1, lu, su1, bk);
@@ -619,9 +624,9 @@ __global__ void __launch_bounds__(kTT)
   __syncthreads();
   if (recon_on || RHO) mbar_wait(bar + 16u, 0);
   for (int k = 0; k < sg.n; ++k) {
-    if (threadIdx.x == 0 && k + 1 < sg.n) issue(k + 1);
-    mbar_wait(bar + 8u * (k & 1), (uint32_t)(k >> 1) & 1u);
-    const unsigned char* sb = tsm + (k & 1) * TileImgSmem::stage;
+    if (kImgStages == 2 && threadIdx.x == 0 && k + 1 < sg.n) issue(k + 1);
+    mbar_wait(bar + 8u * (k % kImgStages), (uint32_t)(k / kImgStages) & 1u);
+    const unsigned char* sb = tsm + (k % kImgStages) * TileImgSmem::stage;
     const float* sU1 = reinterpret_cast<const float*>(sb);
     const float* sLam = reinterpret_cast<const float*>(sb + kHaloSlot);
     const float* sUt = reinterpret_cast<const float*>(sb + kHaloSlot + kPlainSlot);
@@ -636,7 +641,8 @@ __global__ void __launch_bounds__(kTT)
     else
       tile_img_shot<RHO, MODE, false>(g, tt, sU1, sLam, sUt, sE, sH, txx, txz, pulse_t, recon_on,
                                       uo, st, acc);
-    __syncthreads();  // the stage is free for the shot after next
+    __syncthreads();  // every thread is done with the stage: it may be refilled
+    if (kImgStages == 1 && threadIdx.x == 0 && k + 1 < sg.n) issue(k + 1);
   }
   if (tt.zact) {
     double* dst = acc_part + (size_t)blockIdx.z * N2 + tt.z4;

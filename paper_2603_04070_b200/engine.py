@@ -208,7 +208,7 @@ class PhysicsEngine:
                 "adjoint_threads_per_cta", "stepwise_kernels")
         out = {k: int(buf[i]) for i, k in enumerate(keys[:n])}
         if "stepwise_kernels" in out:
-            out["stepwise_kernels"] = ("lean", "vec", "stream")[out["stepwise_kernels"]]
+            out["stepwise_kernels"] = ("lean", "vec", "stream", "tile")[out["stepwise_kernels"]]
         return out
 
     def _stream(self) -> int:

@@ -1,8 +1,9 @@
 """Every stepwise kernel family and history store against the float64 oracle.
 
-The lean kernels cover nz % 4 == 0 grids with separable damping and a
-rectangular undamped box (all BASELINE configs).  The others are reached by
-inputs a user of the reference can hand over:
+The f32 tile kernels (default arithmetic) and the f64 lean kernels (arith="f64")
+cover nz % 4 == 0 grids with separable damping and a rectangular undamped box
+(all BASELINE configs).  The others are reached by inputs a user of the
+reference can hand over:
   * nz % 4 != 0                       -> stream kernels (with and without density)
   * a damping map that is not max(px, pz) (DampingProfile(grid, values) from disk)
                                        -> vec kernels (constant density), stream (density)
@@ -48,7 +49,10 @@ CASES = {
     "sum_damping_rho": (dict(n=40, rho=True), "sum", "stream", ("full", "strips")),
     "island": (dict(n=40), "island", "vec", ("full", "checkpoint")),
     "island_rho": (dict(n=40, rho=True), "island", "stream", ("full", "checkpoint")),
-    "lean_checkpoint": (dict(n=40), None, "lean", ("strips", "checkpoint", "full")),
+    "tile": (dict(n=40), None, "tile", ("strips", "checkpoint", "full")),
+    "tile_rho": (dict(n=40, rho=True), None, "tile", ("strips", "checkpoint", "full")),
+    "lean_f64": (dict(n=40), None, "lean", ("strips", "checkpoint", "full")),
+    "lean_f64_rho": (dict(n=40, rho=True), None, "lean", ("strips", "full")),
 }
 
 
@@ -69,7 +73,8 @@ def test_stepwise_family_vs_oracle(gpu, name):
     m_ref, g_ref, tr_ref = oracle.misfit_gradient(c0, damp.values, grid.dx, grid.dt, pulse.samples,
                                                   tx, rx, obs, geom.element_nodes, rho=rho)
     eng = fwd.get_engine(grid, tx, rx, geom.element_nodes, pulse.samples, damp,
-                         has_rho=rho is not None, engine="stepwise")
+                         has_rho=rho is not None, engine="stepwise",
+                         arith="f64" if name.startswith("lean_f64") else "f32")
     assert eng.info()["stepwise_kernels"] == family
     assert (eng.box is None) == (dkind == "island")
     eng.set_model(wl.c_true, None if rho is None else rho[None])
@@ -102,7 +107,10 @@ def test_pml_values_without_profiles_take_the_lean_kernels(gpu):
     assert np.array_equal(a.traces, b.traces)
     eng = fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes,
                          pulse.samples, plain, engine="stepwise")
-    assert eng.info()["stepwise_kernels"] == "lean"
+    assert eng.info()["stepwise_kernels"] == "tile"
+    eng64 = fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes,
+                           pulse.samples, plain, engine="stepwise", arith="f64")
+    assert eng64.info()["stepwise_kernels"] == "lean"
 
 
 def test_checkpoint_auto_when_full_history_does_not_fit(gpu):

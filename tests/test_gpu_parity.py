@@ -268,3 +268,29 @@ def test_cluster_lap_store_vs_reference(gpu, golden_dir):
                                   geom.tx_nodes(), geom.rx_nodes())
     _, g = eng.misfit_and_gradient(torch.as_tensor(obs).to(gpu), store="lap")
     assert rel_l2(g[0].cpu().numpy(), zc["grad"]) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_arith_option_f32_default_f64_precise(gpu, engine):
+    """dufwi_geometry_t.arith: the default f32 increment form sits at the f32-storage
+    error level (~5e-7 on traces); arith="f64" evaluates the reference's operation
+    order in f64 — on the cluster engine the whole sweep, so only the final f32
+    rounding of the samples remains (<= 1e-7)."""
+    z, grid, geom, pulse, damp = ring48()
+    errs = {}
+    for arith in ("f32", "f64"):
+        eng = fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes,
+                             pulse.samples, damp, engine=engine, arith=arith)
+        assert eng.arith == arith
+        eng.set_model(z["c_true"][None])
+        errs[arith] = rel_l2(eng.forward().cpu().numpy(), z["obs"])
+        eng.set_model(z["c0"][None])
+        mis, g = eng.misfit_and_gradient(torch.as_tensor(z["obs"]).to(gpu))
+        assert rel_l2(g[0].cpu().numpy(), z["grad"]) <= GRAD_TOL
+    assert errs["f32"] <= 2e-6
+    assert errs["f64"] <= (1e-7 if engine == "cluster" else 2e-6)
+    if engine == "cluster":
+        assert errs["f64"] < errs["f32"]
+    with pytest.raises(ValueError, match="arith"):
+        fwd.get_engine(grid, geom.tx_nodes(), geom.rx_nodes(), geom.element_nodes,
+                       pulse.samples, damp, engine=engine, arith="f16")

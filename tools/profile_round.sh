@@ -15,11 +15,11 @@ ncu --set full --clock-control none --import-source on -k regex:cluster_adj -c 1
     -o gpurun_out/${R}_cluster_adj python tools/prof_case.py --config 0 > gpurun_out/${R}_ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:cluster_fwd -s 1 -c 1 \
     -o gpurun_out/${R}_cluster_fwd python tools/prof_case.py --config 0 >> gpurun_out/${R}_ncu_full.log 2>&1
-# stepwise engine (lean kernels) on config 4 (64 units, short nt) and on config 3
+# stepwise engine (f32 tile kernels) on config 4 (64 units, short nt) and on config 3
 # (variable density): one launch of each step kernel
 for cfg in 4 3; do
   python tools/time_config.py --config $cfg --units 64 --nt 12 --reps 1 > gpurun_out/${R}_step_plain_c$cfg.log 2>&1
-  for k in fwd_lean_kernel adjlam_lean_kernel img_lean_kernel; do
+  for k in tile_fwd_kernel tile_adj_kernel tile_img_kernel; do
     ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 \
         -o gpurun_out/${R}_step_c${cfg}_$k python tools/time_config.py --config $cfg --units 64 --nt 12 --reps 1 >> gpurun_out/${R}_ncu_full.log 2>&1
   done
