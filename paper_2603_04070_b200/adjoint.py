@@ -139,8 +139,9 @@ def fd_gradient_oracle(sos: SosMap, m_obs: ChannelData, pulse: SourcePulse, cell
     """Central-difference misfit derivatives at selected cells (adjoint.py:154-186).
 
     All 2*len(cells) perturbed models run as phantoms of ONE batched forward
-    sweep on the device; each misfit sum((obs - sim)^2) is reduced in f64 by
-    the residual kernel.  Noise floor: the receiver samples leave the sweep as
+    sweep on the device with arith="f64" (the sweep itself in f64: a misfit
+    difference needs more than the f32 kernels' 5e-7 trace error); each misfit
+    sum((obs - sim)^2) is reduced in f64 by the residual kernel.  Noise floor: the receiver samples leave the sweep as
     f32 (the ChannelData format of the engine), so each misfit carries a
     relative rounding error of order 1e-7 * (trace/residual energy ratio);
     choose ``eps`` so that the misfit change 2*eps*|g| stays well above it
