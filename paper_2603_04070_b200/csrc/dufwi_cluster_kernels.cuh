@@ -49,6 +49,15 @@ __device__ __forceinline__ void dbg_step(int sweep, long long T0, long long T1, 
     atomicAdd(d + 2, (unsigned long long)path);
   }
 }
+// slot 3: cycles in the step's __syncthreads (low 32 bits) and in its halo wait (high 32 bits)
+__device__ long long g_dbg_tb, g_dbg_tm;  // unused placeholders keep the symbol table stable
+__device__ __forceinline__ void dbg_sync(int sweep, long long T0, long long Tb, long long Tm) {
+  if ((blockIdx.x == 0 || blockIdx.x == 4) && (threadIdx.x & 31) == 0) {
+    const int w = threadIdx.x >> 5;
+    unsigned long long* d = g_dbg + ((sweep * 2 + (blockIdx.x ? 1 : 0)) * 32 + w) * 4;
+    atomicAdd(d + 3, (unsigned long long)(Tb - T0) + ((unsigned long long)(Tm - Tb) << 32));
+  }
+}
 #endif
 
 struct ClusterCfg {
@@ -62,6 +71,7 @@ struct ClusterCfg {
   int maxring = 0;  // ring-strip cells per CTA (upper bound) staged in shared memory
   int maxc = 0;     // clusters co-resident on the device (one wave)
   int per_sm = 1;   // CTAs of the sweep kernels that fit one SM (registers / shared memory)
+  int xthreads = 0; // extra warp of the L(u)-storing forward: issues its bulk stores (0: thread 0 does)
   size_t smem_fwd = 0, smem_adj = 0;
   size_t smem_lap = 0;     // adjoint over the L(u) history (DUFWI_STORE_LAP)
   size_t smem_fwdlap = 0;  // forward storing it (staging slots)
@@ -87,6 +97,20 @@ __host__ __device__ constexpr int cluster_max_threads(int rpt) {
 // registers come from one SM sub-partition, 16384 each, so 15 warps cap at 128)
 __host__ __device__ constexpr int cluster_max_regs(int rpt) {
   return (65536 / cluster_max_threads(rpt)) / 8 * 8;
+}
+
+// The forward that stores the L(u) history runs one warp more than the compute
+// threads (ClusterCfg::xthreads, its bulk-copy issuer): 21 warps put 6 on one
+// SM sub-partition, 16384 / (6 * 32) = 85 registers per thread.  (The adjoint
+// over that history measured slower with the extra warp and the 80-register
+// cap: 0.80 vs 0.77 ms on config 1; it keeps thread 0 as the issuer.)
+// (f32 only: the f64 instances spill at 80 and keep thread 0 as the issuer)
+__host__ __device__ constexpr int cluster_lap_regs(int rpt, int scalar_bytes) {
+  return rpt <= 5 && scalar_bytes == 4 ? 80 : cluster_max_regs(rpt);
+}
+// an extra warp fits: warps per sub-partition x registers within its 16384
+__host__ __device__ constexpr bool cluster_extra_warp_fits(int threads, int regs) {
+  return threads + 32 <= 1024 && ((threads + 32 + 127) / 128) * 32 * regs <= 16384;
 }
 
 // ------------------------------------------------------------- PTX helpers
@@ -393,6 +417,7 @@ struct CellStatic {
   bool full;                  // whole warp: every row slot active
   bool unif;                  // whole warp: full, and one (A, B) per thread for all its rows
   bool pml;                   // whole warp: full, and no cell in the undamped box
+  bool idle;                  // whole warp: no active row (the bulk-copy issuer's warp)
   const pair_t<T>* ab;          // this thread's (A, B) column: ab[j] for row j
 };
 
@@ -463,6 +488,7 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
       same = false;
   st.unif = __all_sync(__activemask(), st.active == full && same);
   st.pml = __all_sync(__activemask(), st.active == full && st.interior == 0u);
+  st.idle = __all_sync(__activemask(), st.active == 0u);
 }
 
 // Exchange-row pushes to the neighbouring CTAs (DSMEM st.async completing on
@@ -494,9 +520,18 @@ __device__ __forceinline__ void push_edges(const CellCtx& c, const CellStatic<RP
 // halo rows of step i-1 have landed (mbarrier phase of bar_r); bar_w is armed
 // for the bytes the neighbours push during step i.
 __device__ __forceinline__ void step_sync(const CellCtx& c, int i, uint32_t bar_r, uint32_t bar_w,
-                                          uint32_t tx_bytes) {
+                                          uint32_t tx_bytes, int sweep = 0) {
+#ifdef DUFWI_EXP_TIMING
+  const long long T0 = clock64();
+#endif
   __syncthreads();
+#ifdef DUFWI_EXP_TIMING
+  const long long Tb = clock64();
+#endif
   if (i >= 1 && (c.has_up || c.has_dn)) mbar_wait(bar_r, ((i - 1) >> 1) & 1);
+#ifdef DUFWI_EXP_TIMING
+  dbg_sync(sweep, T0, Tb, clock64());
+#endif
   if (threadIdx.x == 0 && (c.has_up || c.has_dn)) mbar_expect_tx(bar_w, tx_bytes);
 }
 
@@ -511,7 +546,7 @@ struct StepBufs {
 
 // ---- L(u) history transport (DUFWI_STORE_LAP; the adjoint kernel is below)
 constexpr int kLapDepth = 4;  // adjoint ring slots
-constexpr int kLapStage = 3;  // forward staging slots
+constexpr int kLapStage = 4;  // forward staging slots
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint32_t bar) {
@@ -574,16 +609,22 @@ __host__ __device__ inline size_t cluster_lap_smem_bytes(int rows, int rpt, int 
 }
 
 // Forward, thread 0 after the step barrier of step t: write the staging slot of
-// step t-1 (slot (t-2) % 3, holding L(u[t-2])) to history slot t-2.  Slot
-// reuse: step t writes slot (t-1) % 3, whose last bulk read was issued at step
-// t-2 and completed by this thread's wait_group.read<1> at step t-1.
+// step t-1 (slot (t-2) % 4, holding L(u[t-2])) to history slot t-2.  Slot
+// reuse: step t writes slot (t-1) % 4, whose last bulk read was issued at step
+// t-3 and completed by this thread's wait_group.read<2> at step t-1 (it passed
+// that wait before the barrier of step t).  A store therefore has two full
+// steps to read its slot: with 3 slots and wait_group.read<1> thread 0 waited
+// ~800 cycles per step for the previous step's store, its warp's halo push
+// arrived late and every neighbour CTA sat ~600 cycles in its halo wait
+// (per-warp clock64 timing, profiles/r02_phase_dbg_f32.log).
 __device__ __forceinline__ void lap_store(const Geo& g, const BoxRows& br, int rows, int t,
-                                          uint32_t stage_sa, float* hbox, size_t hstep) {
-  if (threadIdx.x == 0 && br.nb > 0 && t >= 2) {
+                                          uint32_t stage_sa, float* hbox, size_t hstep,
+                                          bool issuer) {
+  if (issuer && br.nb > 0 && t >= 2) {
     const uint32_t slot = stage_sa + (uint32_t)(((t - 2) % kLapStage) * rows * g.nz) * 4u;
     bulk_s2g(hbox + (size_t)(t - 2) * hstep, slot, (uint32_t)(br.nb * g.nz) * 4u);
     bulk_commit();
-    bulk_wait_read<1>();
+    bulk_wait_read<2>();
   }
 }
 
@@ -608,7 +649,20 @@ struct LapFwd {
   uint32_t stage_sa;
   float* hbox;
   size_t hstep;
+  bool issuer;  // this thread issues the CTA's bulk stores
 };
+
+// The thread that issues a CTA's bulk copies.  Issuing and waiting on them
+// costs the thread ~500-800 cycles per step (per-warp clock64 timing): in a
+// compute warp that delays the warp's step body and with it its halo pushes,
+// and the neighbouring CTAs wait for those.  When the register file allows a
+// 21st warp (ClusterCfg::xthreads) the first thread past the compute threads —
+// in the virtual thread order of order_columns — takes the job; its warp owns
+// no cells.
+__device__ __forceinline__ bool bulk_issuer(const CellCtx& c, int nz, int rows, int rpt) {
+  const int nthr = nz * ((rows + rpt - 1) / rpt);
+  return (int)blockDim.x > nthr ? c.seg * nz + c.zi == nthr : threadIdx.x == 0;
+}
 
 // One forward step of a thread's cells (u1 = u[t-1] -> u2 := u[t]).  FULL:
 // every row slot active (no per-row predicates); PLAIN: undamped cells of the
@@ -724,7 +778,7 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
   const long long T0 = clock64();
 #endif
   step_sync(c, t, B.bar_r, B.bar_w, tx_bytes);
-  if (MODE == 3) lap_store(g, lap.br, c.rows, t, lap.stage_sa, lap.hbox, lap.hstep);
+  if (MODE == 3) lap_store(g, lap.br, c.rows, t, lap.stage_sa, lap.hbox, lap.hstep, lap.issuer);
   if (t >= 1) {
     io_gather<T, MODE>(io, nrec, nio, B.r, t - 1, grank);
     if (t % kStage == 0) flush_stage<T, MODE>(g, io, t - kStage, kStage, U, lu, rec, strips);
@@ -733,7 +787,8 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
   const long long T1 = clock64();
 #endif
   // (the forward's FULL step is measured faster than the single-(A, B) one)
-  if (s.fast)
+  if (s.idle) {
+  } else if (s.fast)
     fwd_body<RPT, T, MODE, true, true, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else if (s.plainio)
     fwd_body<RPT, T, MODE, true, true, false, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
@@ -747,7 +802,7 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
 }
 
 template <int RPT, class T, int MODE>
-__global__ void __maxnreg__(cluster_max_regs(RPT))
+__global__ void __maxnreg__(MODE == 3 ? cluster_lap_regs(RPT, (int)sizeof(T)) : cluster_max_regs(RPT))
     cluster_fwd_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
                        int unit_begin, int U, float* __restrict__ rec, float* __restrict__ hist,
                        float* __restrict__ strips, float* __restrict__ ubuf) {
@@ -803,6 +858,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const int slotf = rows * g.nz;
   if (MODE == 3) {
     lap.br = box_rows(g, c);
+    lap.issuer = bulk_issuer(c, g.nz, rows, RPT);
     const size_t so = lap_stage_offset<T>(rows, RPT, g.nz, maxrec, maxring);
     stage = reinterpret_cast<float*>(smem + so);
     lap.stage_sa = smem_addr(stage);
@@ -830,8 +886,8 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   // the last step's samples, then the partial stage
   __syncthreads();
   if (MODE == 3) {  // the last step's L(u[nt-2]); every store complete before exit
-    lap_store(g, lap.br, rows, g.nt, lap.stage_sa, lap.hbox, lap.hstep);
-    if (threadIdx.x == 0) bulk_wait<0>();
+    lap_store(g, lap.br, rows, g.nt, lap.stage_sa, lap.hbox, lap.hstep, lap.issuer);
+    if (lap.issuer) bulk_wait<0>();
   }
   io_gather<T, MODE>(io, nrec, nio, X[(g.nt - 1) & 1], g.nt - 1, gather_rank());
   {
@@ -1030,7 +1086,7 @@ __device__ __forceinline__ void adj_step(const Geo& g, const CellCtx& c, const C
 #ifdef DUFWI_EXP_TIMING
   const long long T0 = clock64();
 #endif
-  step_sync(c, i, B.bar_r, B.bar_w, tx_bytes);
+  step_sync(c, i, B.bar_r, B.bar_w, tx_bytes, 1);
 #ifdef DUFWI_EXP_TIMING
   const long long T1 = clock64();
 #endif
@@ -1229,20 +1285,22 @@ __device__ __forceinline__ void adjlap_step(const Geo& g, const CellCtx& c,
                                             const AdjBufs<T>& B, uint32_t tx_bytes,
                                             const IoStage<T>& io, const BoxRows& br, int rows,
                                             const float* ring, uint32_t ring_sa, uint32_t ringbar,
-                                            const float* hbox, size_t hstep, int lofs) {
+                                            const float* hbox, size_t hstep, int lofs,
+                                            bool issuer) {
 #ifdef DUFWI_EXP_TIMING
   const long long T0 = clock64();
 #endif
-  step_sync(c, i, B.bar_r, B.bar_w, tx_bytes);
+  step_sync(c, i, B.bar_r, B.bar_w, tx_bytes, 1);
   // every thread is past step i-1: its ring slot is free for step i-1+depth
-  if (threadIdx.x == 0 && i >= 1) lap_load(g, br, rows, i - 1 + kLapDepth, ring_sa, ringbar, hbox, hstep);
+  if (issuer && i >= 1) lap_load(g, br, rows, i - 1 + kLapDepth, ring_sa, ringbar, hbox, hstep);
   const int sl = i % kLapDepth;
-  if (IMG && br.nb > 0) mbar_wait(ringbar + 8u * (uint32_t)sl, (uint32_t)(i / kLapDepth) & 1u);
+  if (IMG && br.nb > 0 && !s.idle) mbar_wait(ringbar + 8u * (uint32_t)sl, (uint32_t)(i / kLapDepth) & 1u);
 #ifdef DUFWI_EXP_TIMING
   const long long T1 = clock64();
 #endif
   const float* lr = ring + (size_t)sl * rows * g.nz + lofs;
-  if (s.fast)
+  if (s.idle) {
+  } else if (s.fast)
     adjlap_body<RPT, T, true, true, false, false, IMG>(c, s, l1, l2, acc, i, B, io, lr, g.nz);
   else if (s.plainio)
     adjlap_body<RPT, T, true, true, false, true, IMG>(c, s, l1, l2, acc, i, B, io, lr, g.nz);
@@ -1303,6 +1361,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const int nt = g.nt;
   // the thread's first cell in a ring slot (slots hold the box rows from b0)
   const int lofs = (c.r0 + c.lrow0 - br.b0) * g.nz + c.z;
+  const bool issuer = bulk_issuer(c, g.nz, rows, RPT);
   T la[RPT], lb[RPT], acc[RPT];
   double accd[RPT];
 #pragma unroll
@@ -1317,7 +1376,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const AdjBufs<T> B1{XL[0], XL[1], nullptr, nullptr, xsz, 0u, bar[0], bar[1], bar_off + 8u};
 #define DUFWI_ADJLAP(IMG, L1, L2, BB, I)                                                          \
   adjlap_step<RPT, T, IMG>(g, c, st, L1, L2, acc, I, BB, tx_bytes, io, br, rows, ring, ring_sa,   \
-                           ringbar, hbox, hstep, lofs)
+                           ringbar, hbox, hstep, lofs, issuer)
   int i = 0;
   for (; i + 1 < nt - 1; i += 2) {  // steps with t >= 1: imaging
     if (i % kAccBlock == 0) acc_flush<RPT>(acc, accd);
@@ -1427,7 +1486,9 @@ inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, 
   int n = max_active_clusters(cluster_fwd_kernel<RPT, T, 0>, cs, threads, sf);
   n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 1>, cs, threads, sf));
   n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 2>, cs, threads, sf));
-  n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 3>, cs, threads, sf3));
+  // the L(u)-storing forward runs a 21st warp for its bulk stores when the register file allows
+  const int xt = cluster_extra_warp_fits(threads, cluster_lap_regs(RPT, (int)sizeof(T))) ? 32 : 0;
+  n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 3>, cs, threads + xt, sf3));
   n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 1>, cs, threads, sa));
   n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 2>, cs, threads, sa));
   n = std::min(n, max_active_clusters(cluster_adjlap_kernel<RPT, T>, cs, threads, sl));
@@ -1439,6 +1500,7 @@ inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, 
     per_sm = 1;
   }
   out->per_sm = std::max(1, per_sm);
+  out->xthreads = xt;
   out->cs = cs;
   out->rows = rows;
   out->rpt = RPT;
@@ -1596,9 +1658,12 @@ inline cudaError_t cluster_forward_t(const Geo& g, const Model& m, const Cluster
   if (mode == 1)
     return launch_cluster(cluster_fwd_kernel<RPT, T, 1>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
                           c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
-  if (mode == 4)  // DUFWI_STORE_LAP: hist receives L(u[t]) (kernel MODE 3)
-    return launch_cluster(cluster_fwd_kernel<RPT, T, 3>, c, U, c.smem_fwdlap, st, g, m, c.cs, c.rows,
+  if (mode == 4) {  // DUFWI_STORE_LAP: hist receives L(u[t]) (kernel MODE 3)
+    ClusterCfg cx = c;
+    cx.threads += c.xthreads;
+    return launch_cluster(cluster_fwd_kernel<RPT, T, 3>, cx, U, c.smem_fwdlap, st, g, m, c.cs, c.rows,
                           c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
+  }
   return launch_cluster(cluster_fwd_kernel<RPT, T, 2>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
                         c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
 }

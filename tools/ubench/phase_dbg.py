@@ -27,11 +27,12 @@ so.dufwi_debug_counters(buf, 512)
 nt = grid.nt
 paths = {0: "plain", 1: "full", 2: "generic", 3: "unif", 4: "xpml", 5: "io-plain"}
 for sweep in (0, 1):
-    print(["forward", "adjoint"][sweep], "cycles per step: sync/body(halo wait inside the body) path")
+    print(["forward", "adjoint"][sweep], "cycles per step: before the body [of which __syncthreads, halo wait] / body, path")
     for cta in (0, 1):
         row = []
         for w in range(32):
             d = ((sweep * 2 + cta) * 32 + w) * 4
             p = round(buf[d + 2] / nt)
-            row.append(f"{buf[d] // nt}/{buf[d + 1] // nt}({buf[d + 3] // nt}){paths.get(p, '?')[0]}")
+            bar_c, halo_c = (buf[d + 3] & 0xffffffff) // nt, (buf[d + 3] >> 32) // nt
+            row.append(f"{buf[d] // nt}[bar {bar_c} halo {halo_c}]/{buf[d + 1] // nt}{paths.get(p, '?')[0]}")
         print("  cta", [0, 4][cta], " ".join(row))
