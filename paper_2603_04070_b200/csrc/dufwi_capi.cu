@@ -162,8 +162,16 @@ Groups adj_groups(const Geo& g, int unit_begin, int U, bool per_unit, bool vec, 
     // enough groups for ~8 CTAs per SM, at most 64 shots per group (f32 partial
     // sums), at least 4 (the accumulator costs 16 B / gs per cell update)
     const long tiles = (long)((g.Lz + 2 + kTZ - 1) / kTZ + 1) * ((g.Lx + 2 + kTX - 1) / kTX + 1);
-    const long want = std::max(1L, ((long)sms * 8 + tiles - 1) / tiles);
-    const int gs = (int)std::min(64L, std::max(4L, (long)U / want));
+    static const long per_sm = [] {
+      const char* e = getenv("DUFWI_IMG_CTAS_PER_SM");
+      return e ? std::max(1L, atol(e)) : 8L;
+    }();
+    const long want = std::max(1L, ((long)sms * per_sm + tiles - 1) / tiles);
+    // groups never span phantoms: balance the shots of a phantom over its groups
+    const long nb = std::max(1L, ((long)U + g.S - 1) / g.S);
+    const long gpp = std::max(1L, (want + nb - 1) / nb);
+    const long shots = std::min((long)U, (long)g.S);
+    const int gs = (int)std::min(64L, std::max(4L, (shots + gpp - 1) / gpp));
     return make_groups(g, unit_begin, U, gs);
   }
   // lean imaging kernel: ~8 groups, enough CTAs for several waves; the

@@ -488,13 +488,13 @@ __global__ void __launch_bounds__(kTT)
 #ifndef DUFWI_IMG_STAGES
 #define DUFWI_IMG_STAGES 2
 #endif
-constexpr int kImgStages = DUFWI_IMG_STAGES;  // 1: latency hidden across CTAs only; 2: next shot prefetched
-static_assert(kImgStages == 1 || kImgStages == 2, "imaging pipeline depth");
+constexpr int kImgStages = DUFWI_IMG_STAGES;  // 1: latency hidden across CTAs only; N: N-1 shots prefetched
+static_assert(kImgStages >= 1 && kImgStages <= 4, "imaging pipeline depth");
 struct TileImgSmem {
   static constexpr uint32_t stage = kHaloSlot + 2 * kPlainSlot;  // u1, lam, ut
   static constexpr uint32_t e = kImgStages * stage, h = e + kPlainSlot;
   __host__ __device__ static constexpr uint32_t bar(bool rho) { return h + (rho ? kHaloSlot : 0u); }
-  __host__ __device__ static constexpr uint32_t bytes(bool rho) { return bar(rho) + 32u; }
+  __host__ __device__ static constexpr uint32_t bytes(bool rho) { return bar(rho) + 48u; }
 };
 
 template <bool RHO, int MODE, bool BORDER>
@@ -589,7 +589,8 @@ __global__ void __launch_bounds__(kTT)
   if (sg.n == 0) return;
   float* sE = reinterpret_cast<float*>(tsm + TileImgSmem::e);
   float* sH = reinterpret_cast<float*>(tsm + TileImgSmem::h);
-  const uint32_t bar = smem_addr(tsm + TileImgSmem::bar(RHO));  // [0], [1]: stages, [2]: coefficients
+  const uint32_t bar = smem_addr(tsm + TileImgSmem::bar(RHO));  // [0 .. 3]: stages, [4]: coefficients
+  const uint32_t cbar = bar + 32u;
   const int z0 = (tz0 + blockIdx.x) * kTZ, x0 = (tx0 + blockIdx.y) * kTX;
   const bool recon_on = MODE == 2 && do_recon;
   const size_t N2 = (size_t)g.nx * g.nz;
@@ -604,14 +605,15 @@ __global__ void __launch_bounds__(kTT)
     if (recon_on) tma_load_4d(smem_addr(sb + kHaloSlot + kPlainSlot), &mUt, z0, x0, lu, sut, bk);
   };
   if (threadIdx.x == 0) {
-    tile_bar_init(bar, 3);
+    tile_bar_init(bar, 5);
     const uint32_t cb = (recon_on ? kPlainBytes : 0u) + (RHO ? kHaloBytes : 0u);
     if (cb) {
-      mbar_expect_tx(bar + 16u, cb);
-      if (recon_on) tma_load_3d(smem_addr(sE), &mE, z0, x0, sg.b, bar + 16u);
-      if (RHO) tma_load_3d(smem_addr(sH), &mH, z0, x0, sg.b, bar + 16u);
+      mbar_expect_tx(cbar, cb);
+      if (recon_on) tma_load_3d(smem_addr(sE), &mE, z0, x0, sg.b, cbar);
+      if (RHO) tma_load_3d(smem_addr(sH), &mH, z0, x0, sg.b, cbar);
     }
     issue(0);
+    for (int k = 1; k < kImgStages - 1 && k < sg.n; ++k) issue(k);
   }
   const TileThread tt = tile_thread(g, z0, x0);
   const bool border = MODE == 2 && !tile_in_box(g, z0, x0);
@@ -622,9 +624,10 @@ __global__ void __launch_bounds__(kTT)
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[j][k] = 0.f;
   __syncthreads();
-  if (recon_on || RHO) mbar_wait(bar + 16u, 0);
+  if (recon_on || RHO) mbar_wait(cbar, 0);
   for (int k = 0; k < sg.n; ++k) {
-    if (kImgStages == 2 && threadIdx.x == 0 && k + 1 < sg.n) issue(k + 1);
+    // shot k + N - 1 goes into the stage shot k - 1 used (free since the last barrier)
+    if (kImgStages >= 2 && threadIdx.x == 0 && k + kImgStages - 1 < sg.n) issue(k + kImgStages - 1);
     mbar_wait(bar + 8u * (k % kImgStages), (uint32_t)(k / kImgStages) & 1u);
     const unsigned char* sb = tsm + (k % kImgStages) * TileImgSmem::stage;
     const float* sU1 = reinterpret_cast<const float*>(sb);

@@ -215,3 +215,31 @@ def test_sos_stack_checked_applies_the_map_rules():
     for bad in (np.full((2, 8, 8), np.nan), np.full((2, 8, 8), -1.0), np.full((2, 7, 8), 1500.0)):
         with pytest.raises(ValueError):
             pk.SosMap.stack_checked(g, bad)
+
+
+def test_ctypes_geometry_matches_the_header_layout(tmp_path):
+    """_lib.Geometry mirrors dufwi_geometry_t field by field (gcc on include/dufwi.h),
+    including the `arith` selector, and the DUFWI_ARITH_* values match engine._ARITH."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    from paper_2603_04070_b200 import _lib, engine
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    fields = [f[0] for f in _lib.Geometry._fields_]
+    assert "arith" in fields and "reserved" not in fields
+    src = tmp_path / "layout.c"
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{ROOT / "include" / "dufwi.h"}"',
+             'int main(void) {', '  printf("%zu\\n", sizeof(dufwi_geometry_t));']
+    lines += [f'  printf("%zu\\n", offsetof(dufwi_geometry_t, {f}));' for f in fields]
+    lines += ['  printf("%d %d\\n", DUFWI_ARITH_F32, DUFWI_ARITH_F64);', '  return 0;', '}']
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    assert int(out[0]) == ctypes.sizeof(_lib.Geometry)
+    for f, off in zip(fields, out[1:1 + len(fields)]):
+        assert getattr(_lib.Geometry, f).offset == int(off), f
+    assert engine._ARITH == {"f32": int(out[-2]), "f64": int(out[-1])}

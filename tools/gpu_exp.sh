@@ -1,10 +1,14 @@
 #!/bin/bash
-# Cluster engine: parity of the cluster tests, sweep times per store, per-warp phase timing.
+# Imaging kernel: shot-group size (CTAs per SM target) on the stepwise configs.
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dufwi.py -m gpu -q -x > gpurun_out/pytest_cl.log 2>&1
-echo "pytest exit $?" >> gpurun_out/pytest_cl.log
-CSS="10" RPTS="4 8" bash tools/cluster_shape_sweep.sh > /dev/null 2>&1
-DUFWI_CLUSTER_CS=10 DUFWI_CLUSTER_RPT=4 timeout 300 python tools/ubench/phase_dbg.py > gpurun_out/phase_dbg.log 2>&1
-tail -3 gpurun_out/pytest_cl.log
-cat gpurun_out/shape_sweep.log
-cut -c1-700 gpurun_out/phase_dbg.log
+O=gpurun_out/exp.log
+: > $O
+for ps in 4 8 16 24 40; do
+for c in "3 --units 128 --nt 300" "2 --units 256 --nt 300" "4 --units 256 --nt 200"; do
+  DUFWI_IMG_CTAS_PER_SM=$ps timeout 300 python tools/time_config.py --config $c --reps 2 2>&1 | tail -1 | python -c '
+import sys,json
+d=json.loads(sys.stdin.read())
+print("cfg %d units %3d adj %8.3f ms %.3e upd/s" % (d["config"], d["units"], d["adjoint_ms"], d["adj_updates_per_s"]))' | sed "s/^/per_sm $ps: /" >> $O
+done
+done
+cat $O
