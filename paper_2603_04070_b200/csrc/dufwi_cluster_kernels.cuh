@@ -419,9 +419,14 @@ struct CellStatic {
   bool pml;                   // whole warp: full, and no cell in the undamped box
   bool idle;                  // whole warp: no active row (the bulk-copy issuer's warp)
   const pair_t<T>* ab;          // this thread's (A, B) column: ab[j] for row j
+  // f32, L(u)-history kernels: the pairs also live in registers (2 per row; the
+  // f64 pairs would cost 4, and the strips adjoint has no registers to spare:
+  // 1.10 -> 1.15 ms) — the damped CTAs at both ends of a cluster, whose every
+  // warp runs the FULL path, set the cluster's pace (adjoint 0.77 -> 0.74 ms)
+  pair_t<T> abr[sizeof(T) == 4 ? RPT : 1];
 };
 
-template <int RPT, class T>
+template <int RPT, class T, bool ABR = false>
 __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const CellCtx& c,
                                             size_t pb, int txx, int txz, pair_t<T>* ab_table,
                                             const IoStage<T>& io, bool allow_fast,
@@ -436,11 +441,14 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
   for (int j = 0; j < RPT; ++j) {
     const int lr = c.lrow0 + j;
     st.ed[j] = T(0);
+    if (ABR) st.abr[j] = free_pair<T>();
     if (lr < c.nr) {
       const int x = c.r0 + lr;
       st.active |= 1u << j;
       st.ed[j] = (T)m.Ed[pb + (size_t)x * g.nz + c.z];
-      const_cast<pair_t<T>*>(st.ab)[j] = ab_pair<T>(damping_at(g, x, c.z), g.dt);
+      const pair_t<T> abv = ab_pair<T>(damping_at(g, x, c.z), g.dt);
+      const_cast<pair_t<T>*>(st.ab)[j] = abv;
+      if (ABR) st.abr[j] = abv;
       if (g.row_flag[x] && g.node_slot[(size_t)x * g.nz + c.z] >= 0) st.rmask |= 1u << j;
       if (io.maxring > 0 && ring_index(g, x, c.z) >= 0) st.gmask |= 1u << j;
       if (x == txx && c.z == txz) st.src |= 1u << j;
@@ -693,7 +701,7 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
     if (PLAIN) {
       v[j] = step_free(u1[j], u2[j], s.ed[j], lap);
     } else {
-      const pair_t<T> ab = UNIF ? ab0 : s.ab[j];
+      const pair_t<T> ab = UNIF ? ab0 : ((sizeof(T) == 4 && MODE == 3) ? s.abr[sizeof(T) == 4 ? j : 0] : s.ab[j]);
       v[j] = step_ab(ab, u1[j], u2[j], s.ed[j], lap);
     }
   }
@@ -831,7 +839,7 @@ __global__ void __maxnreg__(MODE == 3 ? cluster_lap_regs(RPT, (int)sizeof(T)) : 
   }
   __syncthreads();
   CellStatic<RPT, T> st;
-  load_static<RPT, T>(g, m, c, pb, txx, txz,
+  load_static<RPT, T, (MODE == 3 && sizeof(T) == 4)>(g, m, c, pb, txx, txz,
                    reinterpret_cast<pair_t<T>*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)),
                    io,
                    true, st);  // (FULL too: the history store is in every step variant)
@@ -1255,7 +1263,7 @@ __device__ __forceinline__ void adjlap_body(const CellCtx& c, const CellStatic<R
     if (PLAIN) {
       lam[j] = adjs_free(l1[j], l2[j], adj);
     } else {
-      const pair_t<T> ab = UNIF ? ab0 : s.ab[j];
+      const pair_t<T> ab = UNIF ? ab0 : (sizeof(T) == 4 ? s.abr[sizeof(T) == 4 ? j : 0] : s.ab[j]);
       lam[j] = adjs_ab(ab, l1[j], l2[j], adj);
     }
   }
@@ -1354,7 +1362,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   }
   __syncthreads();
   CellStatic<RPT, T> st;
-  load_static<RPT, T>(g, m, c, pb, txx, txz,
+  load_static<RPT, T, sizeof(T) == 4>(g, m, c, pb, txx, txz,
                    reinterpret_cast<pair_t<T>*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)), io, true,
                    st);
   const uint32_t tx_bytes = (uint32_t)(((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T));
