@@ -1,12 +1,15 @@
 // Shared device-side types and helpers for the DUFWI sm_100a kernels.
 //
-// Arithmetic model: wavefields are stored in f32 in HBM, every
-// per-cell update is evaluated in f64 registers from the f32 inputs and rounded
-// once when stored.  The cluster engine and the first-generation stepwise
-// kernels read f64 coefficients (E/dx^2, dE/dc, density); the lean stepwise
-// kernels stream f32 copies of E/dx^2, rho E/dx^2 and 1/rho (Model::Edf/Erf/qf,
-// half the bytes) and widen them to f64 before the arithmetic.  Damping
-// profiles, (A, B) tables and the pulse are f64 everywhere.
+// Arithmetic model: wavefields are stored in f32 in HBM.  The
+// default sweep kernels (cluster engine with T = float, dufwi_tile_kernels.cuh)
+// evaluate every update in f32 in the increment form defined below, which has
+// the error of "f64 arithmetic, f32 storage"; imaging sums are folded into f64.
+// DUFWI_ARITH_F64 plans (cluster engine with T = double, the lean / vec / stream
+// stepwise kernels) evaluate every update in f64 registers in the reference's
+// operation order and round once when storing; they read f64 coefficients
+// (E/dx^2, dE/dc, density) or, the lean kernels, f32 copies widened to f64.
+// Damping profiles and the pulse are f64 on the device; the f32 kernels use
+// pairs / tables rounded once from f64.
 #pragma once
 
 #include <cuda_runtime.h>
