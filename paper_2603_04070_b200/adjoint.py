@@ -69,8 +69,12 @@ def gradient_mask(geometry, damping: DampingProfile, guard_radius: int = 2) -> n
 def misfit_and_gradient(sos: SosMap, m_obs: ChannelData, pulse: SourcePulse,
                         damping: DampingProfile | None = None, mask: bool = True,
                         guard_radius: int = 2, *, density=None,
-                        store: str = "auto") -> tuple[float, GradientMap]:
-    """Misfit and its adjoint-state gradient in one forward pass (adjoint.py:94-138)."""
+                        store: str = "auto", arith: str = "f32") -> tuple[float, GradientMap]:
+    """Misfit and its adjoint-state gradient in one forward pass (adjoint.py:94-138).
+
+    ``arith``: "f32" (default) or "f64" — the arithmetic of the sweep kernels
+    (include/dufwi.h DUFWI_ARITH_*); "f64" evaluates the reference's operation
+    order in float64."""
     import torch
 
     geometry = m_obs.geometry
@@ -78,7 +82,7 @@ def misfit_and_gradient(sos: SosMap, m_obs: ChannelData, pulse: SourcePulse,
     _check_simulation_inputs(sos, geometry, pulse, damping)
     rho = _density_values(density, sos.grid)
     eng = get_engine(sos.grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
-                     pulse.samples, damping, has_rho=rho is not None)
+                     pulse.samples, damping, has_rho=rho is not None, arith=arith)
     eng.set_model(sos.values[None], None if rho is None else rho[None])
     obs = torch.as_tensor(m_obs.traces, dtype=torch.float64).to(eng.device)
     try:
@@ -91,14 +95,15 @@ def misfit_and_gradient(sos: SosMap, m_obs: ChannelData, pulse: SourcePulse,
 
 def compute_gradient(sos: SosMap, m_obs: ChannelData, pulse: SourcePulse,
                      damping: DampingProfile | None = None, mask: bool = True,
-                     guard_radius: int = 2, *, density=None) -> GradientMap:
+                     guard_radius: int = 2, *, density=None, arith: str = "f32") -> GradientMap:
     """Adjoint-state gradient of :func:`data_misfit` (adjoint.py:141-151)."""
-    return misfit_and_gradient(sos, m_obs, pulse, damping, mask, guard_radius, density=density)[1]
+    return misfit_and_gradient(sos, m_obs, pulse, damping, mask, guard_radius, density=density,
+                               arith=arith)[1]
 
 
 def misfit_and_gradient_batch(sos_list, obs_list, pulse: SourcePulse,
                               damping: DampingProfile | None = None, mask: bool = True,
-                              guard_radius: int = 2, *, density_list=None):
+                              guard_radius: int = 2, *, density_list=None, arith: str = "f32"):
     """Batched extension: B phantoms sharing one acquisition, one engine launch set.
 
     Under torch.distributed the (phantom, shot) units are sharded across ranks
@@ -122,7 +127,7 @@ def misfit_and_gradient_batch(sos_list, obs_list, pulse: SourcePulse,
     if density_list is not None:
         rho = np.stack([_density_values(d, grid) for d in density_list])
     eng = get_engine(grid, geometry.tx_nodes(), geometry.rx_nodes(), geometry.element_nodes,
-                     pulse.samples, damping, n_phantoms=B, has_rho=rho is not None)
+                     pulse.samples, damping, n_phantoms=B, has_rho=rho is not None, arith=arith)
     eng.set_model(np.stack([s.values for s in sos_list]), rho)
     obs = torch.as_tensor(np.concatenate([o.traces for o in obs_list]), dtype=torch.float64)
     try:

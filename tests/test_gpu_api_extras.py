@@ -108,3 +108,21 @@ def test_shape_checks_of_engine_and_batch(gpu):
     mis, gs = pk.misfit_and_gradient_batch([c, c], [o, o], pulse, damp)
     m1, g1 = pk.misfit_and_gradient(c, o, pulse, damp)
     assert mis[0] == m1 and np.array_equal(gs[1].values, g1.values)
+
+
+def test_public_api_arith_keyword(gpu):
+    """simulate_all / misfit_and_gradient take arith="f64": the float64 sweep sits an
+    order of magnitude closer to the reference than the default f32 one, both inside
+    the parity bars; an unknown value raises."""
+    z, grid, geom, pulse, damp = ring48()
+    c_true, c0 = pk.SosMap(grid, z["c_true"]), pk.SosMap(grid, z["c0"])
+    obs = pk.ChannelData(z["obs"], geom, grid.dt)
+    e32 = rel_l2(pk.simulate_all(c_true, geom, pulse, damp).traces, z["obs"])
+    e64 = rel_l2(pk.simulate_all(c_true, geom, pulse, damp, arith="f64").traces, z["obs"])
+    assert e64 < 1e-7 < e32 <= 1e-4
+    for arith in ("f32", "f64"):
+        m, g = pk.misfit_and_gradient(c0, obs, pulse, damp, arith=arith)
+        assert rel_l2(g.values, z["grad"]) <= 1e-4
+        assert abs(m - float(z["misfit"])) <= 1e-4 * float(z["misfit"])
+    with pytest.raises(ValueError, match="arith"):
+        pk.compute_gradient(c0, obs, pulse, damp, arith="bf16")
