@@ -38,10 +38,13 @@ namespace dufwi {
 
 namespace cg = cooperative_groups;
 #ifdef DUFWI_EXP_TIMING
-// per-warp step timing of CTA ranks 0 and 4 of cluster 0: [sweep][cta][warp < 32][sync, body, path, -]
+#ifndef DUFWI_DBG_RANK
+#define DUFWI_DBG_RANK 4
+#endif
+// per-warp step timing of CTA ranks 0 and DUFWI_DBG_RANK of cluster 0: [sweep][cta][warp < 32][sync, body, path, -]
 __device__ unsigned long long g_dbg[2 * 2 * 32 * 4];
 __device__ __forceinline__ void dbg_step(int sweep, long long T0, long long T1, int path) {
-  if ((blockIdx.x == 0 || blockIdx.x == 4) && (threadIdx.x & 31) == 0) {
+  if ((blockIdx.x == 0 || blockIdx.x == DUFWI_DBG_RANK) && (threadIdx.x & 31) == 0) {
     const int w = threadIdx.x >> 5;
     unsigned long long* d = g_dbg + ((sweep * 2 + (blockIdx.x ? 1 : 0)) * 32 + w) * 4;
     atomicAdd(d + 0, (unsigned long long)(T1 - T0));
@@ -52,7 +55,7 @@ __device__ __forceinline__ void dbg_step(int sweep, long long T0, long long T1, 
 // slot 3: cycles in the step's __syncthreads (low 32 bits) and in its halo wait (high 32 bits)
 __device__ long long g_dbg_tb, g_dbg_tm;  // unused placeholders keep the symbol table stable
 __device__ __forceinline__ void dbg_sync(int sweep, long long T0, long long Tb, long long Tm) {
-  if ((blockIdx.x == 0 || blockIdx.x == 4) && (threadIdx.x & 31) == 0) {
+  if ((blockIdx.x == 0 || blockIdx.x == DUFWI_DBG_RANK) && (threadIdx.x & 31) == 0) {
     const int w = threadIdx.x >> 5;
     unsigned long long* d = g_dbg + ((sweep * 2 + (blockIdx.x ? 1 : 0)) * 32 + w) * 4;
     atomicAdd(d + 3, (unsigned long long)(Tb - T0) + ((unsigned long long)(Tm - Tb) << 32));

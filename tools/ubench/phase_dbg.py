@@ -1,5 +1,6 @@
 """Per-warp step timing of the cluster sweeps (library built with -DDUFWI_EXP_TIMING):
-CTA rank 0 (x damping band) and rank 4 (interior) of the first cluster."""
+CTA rank 0 (x damping band) and rank DUFWI_DBG_RANK (default 4, interior; the library must be
+built with the same -DDUFWI_DBG_RANK) of the first cluster."""
 import ctypes
 import os
 import sys
@@ -35,4 +36,4 @@ for sweep in (0, 1):
             p = round(buf[d + 2] / nt)
             bar_c, halo_c = (buf[d + 3] & 0xffffffff) // nt, (buf[d + 3] >> 32) // nt
             row.append(f"{buf[d] // nt}[bar {bar_c} halo {halo_c}]/{buf[d + 1] // nt}{paths.get(p, '?')[0]}")
-        print("  cta", [0, 4][cta], " ".join(row))
+        print("  cta", [0, int(os.environ.get("DUFWI_DBG_RANK", "4"))][cta], " ".join(row))
