@@ -26,7 +26,7 @@ c0 = pk.SosMap(grid, np.full(grid.shape, 1540.0))
 setup = pk.InversionSetup(pulse, damp, bounds)
 for _ in range(3):
     pk.unfold_infer(obs_host, c0, nets, setup)
-rec = uf._reconstructor(eng, nets, setup.bounds, None)
+rec = uf._reconstructor(eng, nets, setup.bounds, None, False, grid)
 sync = torch.cuda.synchronize
 for k in range(5):
     sync()
