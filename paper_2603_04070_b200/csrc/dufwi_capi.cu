@@ -874,6 +874,9 @@ extern "C" int dufwi_forward(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
     TileCtx tc;
     tile_ctx_build(p, U, ubuf, nullptr, mode == DUFWI_STORE_FULL ? hist : nullptr, (size_t)g.nt,
                    nullptr, 0, tc);
+    // no silent change of kernels (and arithmetic) under a plan that reports "tile"
+    if (use_tile(p) && !tc.ok)
+      return fail(DUFWI_ECUDA, "tensor map encoding failed (workspace not 16-byte aligned?)");
     for (int t = 0; t < g.nt; ++t) {
       float* rec_t = rec + (size_t)t * U * g.M;
       const int has1 = t >= 1, has2 = t >= 2;
@@ -988,6 +991,8 @@ extern "C" int dufwi_adjoint(dufwi_plan_t* p, int32_t mode, int32_t unit_begin, 
       const bool hh = mode == DUFWI_STORE_FULL || ck;
       tile_ctx_build(p, U, ubuf, lbuf, hh ? hist : nullptr, ck ? (size_t)ck_len(g.nt) : (size_t)g.nt,
                      ck ? snap : nullptr, ck ? (size_t)ck_segments(g.nt) * 2 : 0, tc);
+      if (use_tile(p) && !tc.ok)
+        return fail(DUFWI_ECUDA, "tensor map encoding failed (workspace not 16-byte aligned?)");
     }
     auto adj_step = [&](int t, const float* F) {
       const float* l1 = lbuf + (size_t)((t + 1) & 1) * fieldU;
