@@ -180,16 +180,24 @@ __device__ __forceinline__ void cluster_sync_all() {
 // ------------------------------------------------------------ smem layout
 // [nbufs exchange buffers] [nz x nseg*RPT float2 (A, B)] [2 mbarriers] [IO stage]
 // An exchange buffer is column-major: cell (buffer row r, column z) at
-// (z + 1) * RS + r, r = local row + 1 (r = 0 / rows + 1: halo rows from the
-// neighbouring CTAs), z = -1 / nz: zero pad columns.  RS >= nseg * RPT + 2 is
-// odd, so 32 lanes on consecutive columns hit 32 distinct 8-byte bank pairs,
-// and a thread's own rows sit at compile-time offsets from one base address.
+// (z + 1) * RS + r, r = local row + 1 (r = 0 / rows + 1: never written, zero),
+// z = -1 / nz: zero pad columns.  RS >= nseg * RPT + 2 is odd, so 32 lanes on
+// consecutive columns hit 32 distinct banks, and a thread's own rows sit at
+// compile-time offsets from one base address.  The halo rows pushed by the
+// neighbouring CTAs are ROW-major side rows after the column-major part (top
+// halo at xmain + z, bottom halo at xmain + nzp + z): a warp's st.async then
+// covers 128 contiguous bytes of the neighbour's shared memory instead of 32
+// scattered words.
 __host__ __device__ inline int xcol_stride(int rows, int rpt) {
   const int nseg = (rows + rpt - 1) / rpt;
   return (nseg * rpt + 2) | 1;
 }
+__host__ __device__ inline size_t xbuf_main(int rows, int rpt, int nz) {
+  return (((size_t)(nz + 2) * xcol_stride(rows, rpt)) + 3) & ~(size_t)3;
+}
+__host__ __device__ inline int xhalo_pitch(int nz) { return (nz + 3) & ~3; }
 __host__ __device__ inline size_t xbuf_elems(int rows, int rpt, int nz) {
-  return (size_t)(nz + 2) * xcol_stride(rows, rpt);
+  return xbuf_main(rows, rpt, nz) + 2 * (size_t)xhalo_pitch(nz);
 }
 template <class T>
 __host__ __device__ inline size_t ab_offset(int rows, int rpt, int nz, int nbufs) {
@@ -270,6 +278,7 @@ struct CellCtx {
   int RS;                      // exchange column stride
   int xo;                      // buffer offset of the thread's first cell
   uint32_t off_up, off_dn;     // byte offsets of this column's halo cells in a buffer
+  int o_xm, o_xp;              // buffer offsets of the x neighbours of the thread's first / last row
   bool has_up, has_dn;         // CTA rank-1 / rank+1 exist with rows
   uint32_t lbase, rup, rdn;    // shared-window base: own, rank-1, rank+1
 };
@@ -394,8 +403,18 @@ __device__ __forceinline__ void order_columns(const Geo& g, CellCtx& c, int txx,
   }
   c.z = order[c.zi];
   c.xo = (c.z + 1) * c.RS + c.lrow0 + 1;
-  c.off_dn = (uint32_t)((c.z + 1) * c.RS) * (uint32_t)sizeof(T);        // top halo of rank+1
-  c.off_up = c.off_dn + (uint32_t)(c.rows + 1) * (uint32_t)sizeof(T);  // bottom halo of rank-1
+  {
+    const int xm = (int)xbuf_main(c.rows, rpt, nz), hp = xhalo_pitch(nz);
+    c.off_dn = (uint32_t)(xm + c.z) * (uint32_t)sizeof(T);       // top halo row of rank+1
+    c.off_up = (uint32_t)(xm + hp + c.z) * (uint32_t)sizeof(T);  // bottom halo row of rank-1
+    // x neighbours across the slab's edges come from the side rows, inside the
+    // slab from the adjacent segment's cell (a missing neighbour: a zero cell)
+    // (o_xp: of the thread's last ACTIVE row — the slab's last row may sit
+    // anywhere in a partial last segment)
+    const bool holds_last = c.lrow0 < c.nr && c.lrow0 + rpt >= c.nr;
+    c.o_xm = (c.lrow0 == 0 && c.has_up) ? xm + c.z : c.xo - 1;
+    c.o_xp = !holds_last ? c.xo + rpt : c.has_dn ? xm + hp + c.z : c.xo + (c.nr - c.lrow0);
+  }
   __syncthreads();  // scratch is reused as exchange buffer afterwards
 }
 
@@ -422,10 +441,10 @@ struct CellStatic {
   bool pml;                   // whole warp: full, and no cell in the undamped box
   bool idle;                  // whole warp: no active row (the bulk-copy issuer's warp)
   const pair_t<T>* ab;          // this thread's (A, B) column: ab[j] for row j
-  // f32, L(u)-history kernels: the pairs also live in registers (2 per row; the
-  // f64 pairs would cost 4, and the strips adjoint has no registers to spare:
-  // 1.10 -> 1.15 ms) — the damped CTAs at both ends of a cluster, whose every
-  // warp runs the FULL path, set the cluster's pace (adjoint 0.77 -> 0.74 ms)
+  // f32, L(u)-storing forward: the pairs also live in registers (2 per row; the
+  // f64 pairs would cost 4).  The adjoint kernels have no registers to spare
+  // (strips adjoint 1.10 -> 1.15 ms; the adjoint over the history gained 4% with
+  // them until the side-row offsets took the registers: 0.79 vs 0.72 ms).
   pair_t<T> abr[sizeof(T) == 4 ? RPT : 1];
 };
 
@@ -696,9 +715,10 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
   float* hl = hist;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    const T xm = j > 0 ? u1[j - 1] : (T)pc[-1];
+    const T xm = j > 0 ? u1[j - 1] : (T)B.r[c.o_xm];
     const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
-    const T xp = own_next ? u1[j + 1] : (T)pc[j + 1];
+    const T xp = own_next ? u1[j + 1]
+                          : ((FULL ? j == RPT - 1 : c.lrow0 + j + 1 >= c.nr) ? (T)B.r[c.o_xp] : (T)pc[j + 1]);
     const T lap = lap_s(u1[j], xm, xp, (T)pm[j], (T)pp[j]);
     if (MODE == 3 && t >= 1 && (PLAIN || ((s.interior >> j) & 1u))) hl[j * g.nz] = (float)lap;
     if (PLAIN) {
@@ -975,9 +995,10 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
     const T* pc = B.lr + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-      const T xm = j > 0 ? el[j - 1] : (T)pc[-1];
+      const T xm = j > 0 ? el[j - 1] : (T)B.lr[c.o_xm];
       const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
-      const T xp = own_next ? el[j + 1] : (T)pc[j + 1];
+      const T xp = own_next ? el[j + 1]
+                          : ((FULL ? j == RPT - 1 : c.lrow0 + j + 1 >= c.nr) ? (T)B.lr[c.o_xp] : (T)pc[j + 1]);
       const T adj = lap_s(el[j], xm, xp, (T)pc[j - RS], (T)pc[j + RS]);
       if (PLAIN) {
         lam[j] = adjs_free(l1[j], l2[j], adj);
@@ -1000,9 +1021,10 @@ __device__ __forceinline__ void adj_body(const Geo& g, const CellCtx& c, const C
     const T* pc = B.ur + c.xo;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-      const T xm = j > 0 ? ub[j - 1] : (T)pc[-1];
+      const T xm = j > 0 ? ub[j - 1] : (T)B.ur[c.o_xm];
       const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
-      const T xp = own_next ? ub[j + 1] : (T)pc[j + 1];
+      const T xp = own_next ? ub[j + 1]
+                          : ((FULL ? j == RPT - 1 : c.lrow0 + j + 1 >= c.nr) ? (T)B.ur[c.o_xp] : (T)pc[j + 1]);
       lapu[j] = lap_s(ub[j], xm, xp, (T)pc[j - RS], (T)pc[j + RS]);
     }
   } else if (MODE == 1) {
@@ -1180,9 +1202,12 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
     for (int k = threadIdx.x; k < (c.nr + 2) * g.nz; k += blockDim.x) {
       const int r = k / g.nz, zz = k - r * g.nz;
       const int x = c.r0 - 1 + r;
-      // buffer row r (0: top halo, nr + 1: bottom halo at rows + 1)
-      const int rb = r == c.nr + 1 ? c.rows + 1 : r;
-      if (x >= 0 && x < g.nx) XU[1][(size_t)(zz + 1) * RS + rb] = (T)u_prev[(size_t)x * g.nz + zz];
+      // own rows: column-major cell r; the halo rows: the row-major side rows
+      const size_t xm = xbuf_main(rows, RPT, g.nz);
+      const size_t cell = r == 0 ? xm + zz
+                          : r == c.nr + 1 ? xm + xhalo_pitch(g.nz) + zz
+                                          : (size_t)(zz + 1) * RS + r;
+      if (x >= 0 && x < g.nx) XU[1][cell] = (T)u_prev[(size_t)x * g.nz + zz];
     }
   }
   T la[RPT], lb[RPT], ua[RPT], ub[RPT], acc[RPT];
@@ -1259,14 +1284,15 @@ __device__ __forceinline__ void adjlap_body(const CellCtx& c, const CellStatic<R
   const T* pc = B.lr + c.xo;
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    const T xm = j > 0 ? el[j - 1] : (T)pc[-1];
+    const T xm = j > 0 ? el[j - 1] : (T)B.lr[c.o_xm];
     const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
-    const T xp = own_next ? el[j + 1] : (T)pc[j + 1];
+    const T xp = own_next ? el[j + 1]
+                          : ((FULL ? j == RPT - 1 : c.lrow0 + j + 1 >= c.nr) ? (T)B.lr[c.o_xp] : (T)pc[j + 1]);
     const T adj = lap_s(el[j], xm, xp, (T)pc[j - RS], (T)pc[j + RS]);
     if (PLAIN) {
       lam[j] = adjs_free(l1[j], l2[j], adj);
     } else {
-      const pair_t<T> ab = UNIF ? ab0 : (sizeof(T) == 4 ? s.abr[sizeof(T) == 4 ? j : 0] : s.ab[j]);
+      const pair_t<T> ab = UNIF ? ab0 : s.ab[j];
       lam[j] = adjs_ab(ab, l1[j], l2[j], adj);
     }
   }
@@ -1365,7 +1391,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   }
   __syncthreads();
   CellStatic<RPT, T> st;
-  load_static<RPT, T, sizeof(T) == 4>(g, m, c, pb, txx, txz,
+  load_static<RPT, T, false>(g, m, c, pb, txx, txz,
                    reinterpret_cast<pair_t<T>*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)), io, true,
                    st);
   const uint32_t tx_bytes = (uint32_t)(((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T));
