@@ -689,9 +689,17 @@ struct LapFwd {
 // 21st warp (ClusterCfg::xthreads) the first thread past the compute threads —
 // in the virtual thread order of order_columns — takes the job; its warp owns
 // no cells.
+// Without an extra warp the job goes to the first thread of a middle segment:
+// its warp pushes no halo row, so its late start delays no neighbour, and
+// inside the CTA it is hidden behind the halo wait.
 __device__ __forceinline__ bool bulk_issuer(const CellCtx& c, int nz, int rows, int rpt) {
   const int nthr = nz * ((rows + rpt - 1) / rpt);
   return (int)blockDim.x > nthr ? c.seg * nz + c.zi == nthr : threadIdx.x == 0;
+}
+// (the adjoint over the L(u) history; adjoint 0.721 -> 0.697 ms on config 1)
+__device__ __forceinline__ bool bulk_issuer_mid(const CellCtx& c, int nz, int rows, int rpt) {
+  const int nseg = (rows + rpt - 1) / rpt;
+  return c.seg * nz + c.zi == (nseg >= 3 ? (nseg / 2) * nz : 0);
 }
 
 // One forward step of a thread's cells (u1 = u[t-1] -> u2 := u[t]).  FULL:
@@ -1398,7 +1406,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   const int nt = g.nt;
   // the thread's first cell in a ring slot (slots hold the box rows from b0)
   const int lofs = (c.r0 + c.lrow0 - br.b0) * g.nz + c.z;
-  const bool issuer = bulk_issuer(c, g.nz, rows, RPT);
+  const bool issuer = bulk_issuer_mid(c, g.nz, rows, RPT);
   T la[RPT], lb[RPT], acc[RPT];
   double accd[RPT];
 #pragma unroll
