@@ -702,6 +702,20 @@ __device__ __forceinline__ bool bulk_issuer_mid(const CellCtx& c, int nz, int ro
   return c.seg * nz + c.zi == (nseg >= 3 ? (nseg / 2) * nz : 0);
 }
 
+// Edge rows first: a thread computes its first and last row before the others
+// and pushes them to the neighbouring CTAs at once, so the DSMEM transfer of
+// the halo rows overlaps the rest of the step body instead of following it.  A
+// thread still reads its halo inputs before it pushes (the edge rows are the
+// only ones that read them), which is what orders the neighbour's next
+// overwrite of that halo row after this read.  Full slabs only.
+#ifndef DUFWI_EDGE_FIRST
+#define DUFWI_EDGE_FIRST 1
+#endif
+constexpr bool kEdgeFirst = DUFWI_EDGE_FIRST != 0;
+__host__ __device__ constexpr int edge_order(int i, int rpt) {
+  return i == 0 ? 0 : i == 1 ? rpt - 1 : i - 1;
+}
+
 // One forward step of a thread's cells (u1 = u[t-1] -> u2 := u[t]).  FULL:
 // every row slot active (no per-row predicates); PLAIN: undamped cells of the
 // box (A = 2, B = -1); IO: a PLAIN thread may hold the source (receivers are
@@ -721,8 +735,10 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
   // shared-memory staging slot of step t (`hist`: the thread's first cell there),
   // written to history slot t-1 by one bulk copy after the next step barrier
   float* hl = hist;
+  constexpr bool EARLY = FULL && kEdgeFirst;
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) {
+  for (int i = 0; i < RPT; ++i) {
+    const int j = EARLY ? edge_order(i, RPT) : i;
     const T xm = j > 0 ? u1[j - 1] : (T)B.r[c.o_xm];
     const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
     const T xp = own_next ? u1[j + 1]
@@ -735,11 +751,8 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
       const pair_t<T> ab = UNIF ? ab0 : ((sizeof(T) == 4 && MODE == 3) ? s.abr[sizeof(T) == 4 ? j : 0] : s.ab[j]);
       v[j] = step_ab(ab, u1[j], u2[j], s.ed[j], lap);
     }
-  }
-  if ((!PLAIN || IO) && s.src) {
-#pragma unroll
-    for (int j = 0; j < RPT; ++j)
-      if (s.src & (1u << j)) v[j] = add_s(v[j], pulse_t);
+    if ((!PLAIN || IO) && (s.src & (1u << j))) v[j] = add_s(v[j], pulse_t);
+    if (EARLY && i == (RPT > 1 ? 1 : 0)) push_edges<RPT, T>(c, s, B.wb, B.bar_wb, v, FULL);
   }
   T* q = B.w + c.xo;
 #pragma unroll
@@ -749,7 +762,7 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
     q[j] = (T)v[j];
     if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = (float)v[j];
   }
-  push_edges<RPT, T>(c, s, B.wb, B.bar_wb, v, FULL);
+  if (!EARLY) push_edges<RPT, T>(c, s, B.wb, B.bar_wb, v, FULL);
   if (MODE == 3) fence_proxy_async();  // the staged values are read by the bulk copy
 }
 
@@ -1290,8 +1303,13 @@ __device__ __forceinline__ void adjlap_body(const CellCtx& c, const CellStatic<R
 #pragma unroll
   for (int j = 0; j < RPT; ++j) el[j] = mul_s(s.ed[j], l1[j]);
   const T* pc = B.lr + c.xo;
+  constexpr bool EARLY = FULL && kEdgeFirst;
+  const bool rx = (!PLAIN || IO) && s.rmask;  // one stage entry per row (0: no receiver)
+  const T* r = io.srec + (size_t)k * io.maxrec + s.rbase;
+  T elw[RPT];
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) {
+  for (int i = 0; i < RPT; ++i) {
+    const int j = EARLY ? edge_order(i, RPT) : i;
     const T xm = j > 0 ? el[j - 1] : (T)B.lr[c.o_xm];
     const bool own_next = j + 1 < RPT && (FULL || c.lrow0 + j + 1 < c.nr);
     const T xp = own_next ? el[j + 1]
@@ -1303,24 +1321,20 @@ __device__ __forceinline__ void adjlap_body(const CellCtx& c, const CellStatic<R
       const pair_t<T> ab = UNIF ? ab0 : s.ab[j];
       lam[j] = adjs_ab(ab, l1[j], l2[j], adj);
     }
-  }
-  if ((!PLAIN || IO) && s.rmask) {
-    const T* r = io.srec + (size_t)k * io.maxrec + s.rbase;
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) lam[j] = add_s(lam[j], r[j]);
+    if (rx) lam[j] = add_s(lam[j], r[j]);
+    elw[j] = mul_s(s.ed[j], lam[j]);
+    if (EARLY && i == (RPT > 1 ? 1 : 0)) push_edges<RPT, T>(c, s, B.lwb, B.bar_wb, elw, FULL);
   }
   T* ql = B.lw + c.xo;
-  T elw[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
-    elw[j] = mul_s(s.ed[j], lam[j]);
     if (!FULL && !(s.active & (1u << j))) continue;
     l2[j] = lam[j];
     ql[j] = (T)elw[j];
     if (IMG && (PLAIN || ((s.interior >> j) & 1u)))
       acc[j] = fma_s((T)lr[j * nz], lam[j], acc[j]);
   }
-  push_edges<RPT, T>(c, s, B.lwb, B.bar_wb, elw, FULL);
+  if (!EARLY) push_edges<RPT, T>(c, s, B.lwb, B.bar_wb, elw, FULL);
 }
 
 template <int RPT, class T, bool IMG>
