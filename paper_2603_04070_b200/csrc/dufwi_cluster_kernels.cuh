@@ -441,14 +441,9 @@ struct CellStatic {
   bool pml;                   // whole warp: full, and no cell in the undamped box
   bool idle;                  // whole warp: no active row (the bulk-copy issuer's warp)
   const pair_t<T>* ab;          // this thread's (A, B) column: ab[j] for row j
-  // f32, L(u)-storing forward: the pairs also live in registers (2 per row; the
-  // f64 pairs would cost 4).  The adjoint kernels have no registers to spare
-  // (strips adjoint 1.10 -> 1.15 ms; the adjoint over the history gained 4% with
-  // them until the side-row offsets took the registers: 0.79 vs 0.72 ms).
-  pair_t<T> abr[sizeof(T) == 4 ? RPT : 1];
 };
 
-template <int RPT, class T, bool ABR = false>
+template <int RPT, class T>
 __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const CellCtx& c,
                                             size_t pb, int txx, int txz, pair_t<T>* ab_table,
                                             const IoStage<T>& io, bool allow_fast,
@@ -463,14 +458,11 @@ __device__ __forceinline__ void load_static(const Geo& g, const Model& m, const 
   for (int j = 0; j < RPT; ++j) {
     const int lr = c.lrow0 + j;
     st.ed[j] = T(0);
-    if (ABR) st.abr[j] = free_pair<T>();
     if (lr < c.nr) {
       const int x = c.r0 + lr;
       st.active |= 1u << j;
       st.ed[j] = (T)m.Ed[pb + (size_t)x * g.nz + c.z];
-      const pair_t<T> abv = ab_pair<T>(damping_at(g, x, c.z), g.dt);
-      const_cast<pair_t<T>*>(st.ab)[j] = abv;
-      if (ABR) st.abr[j] = abv;
+      const_cast<pair_t<T>*>(st.ab)[j] = ab_pair<T>(damping_at(g, x, c.z), g.dt);
       if (g.row_flag[x] && g.node_slot[(size_t)x * g.nz + c.z] >= 0) st.rmask |= 1u << j;
       if (io.maxring > 0 && ring_index(g, x, c.z) >= 0) st.gmask |= 1u << j;
       if (x == txx && c.z == txz) st.src |= 1u << j;
@@ -748,7 +740,7 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
     if (PLAIN) {
       v[j] = step_free(u1[j], u2[j], s.ed[j], lap);
     } else {
-      const pair_t<T> ab = UNIF ? ab0 : ((sizeof(T) == 4 && MODE == 3) ? s.abr[sizeof(T) == 4 ? j : 0] : s.ab[j]);
+      const pair_t<T> ab = UNIF ? ab0 : s.ab[j];
       v[j] = step_ab(ab, u1[j], u2[j], s.ed[j], lap);
     }
     if ((!PLAIN || IO) && (s.src & (1u << j))) v[j] = add_s(v[j], pulse_t);
@@ -883,7 +875,7 @@ __global__ void __maxnreg__(MODE == 3 ? cluster_lap_regs(RPT, (int)sizeof(T)) : 
   }
   __syncthreads();
   CellStatic<RPT, T> st;
-  load_static<RPT, T, (MODE == 3 && sizeof(T) == 4)>(g, m, c, pb, txx, txz,
+  load_static<RPT, T>(g, m, c, pb, txx, txz,
                    reinterpret_cast<pair_t<T>*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)),
                    io,
                    true, st);  // (FULL too: the history store is in every step variant)
@@ -1413,7 +1405,7 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
   }
   __syncthreads();
   CellStatic<RPT, T> st;
-  load_static<RPT, T, false>(g, m, c, pb, txx, txz,
+  load_static<RPT, T>(g, m, c, pb, txx, txz,
                    reinterpret_cast<pair_t<T>*>(smem + ab_offset<T>(rows, RPT, g.nz, 2)), io, true,
                    st);
   const uint32_t tx_bytes = (uint32_t)(((c.has_up ? 1 : 0) + (c.has_dn ? 1 : 0)) * g.nz * sizeof(T));
