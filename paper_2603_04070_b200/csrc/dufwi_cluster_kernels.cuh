@@ -830,12 +830,14 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
 #ifdef DUFWI_EXP_TIMING
   const long long T1 = clock64();
 #endif
-  // (the forward's FULL step is measured faster than the single-(A, B) one)
   if (s.idle) {
   } else if (s.fast)
     fwd_body<RPT, T, MODE, true, true, false, false>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else if (s.plainio)
     fwd_body<RPT, T, MODE, true, true, false, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
+  else if (MODE != 3 && s.unif)  // (0.663 -> 0.636 ms with the strips store; the L(u)-storing
+                                 // forward, at its 80-register cap, loses 3% with it)
+    fwd_body<RPT, T, MODE, true, false, true, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else if (s.full)
     fwd_body<RPT, T, MODE, true, false, false, true>(g, c, s, u1, u2, t, U, lu, B, pulse_t, hist, N2);
   else
