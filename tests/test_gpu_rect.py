@@ -77,3 +77,29 @@ def test_rectangular_grid_vs_oracle(gpu, shape, rho):
             assert rel_l2(tr.cpu().numpy(), tr_ref) <= TOL, (engine, store)
             assert rel_l2(g[0].cpu().numpy(), g_ref) <= TOL, (engine, store)
             assert abs(float(mis[0]) - m_ref) <= TOL * m_ref, (engine, store)
+
+
+def test_rectangular_grid_poisoned_workspace(gpu):
+    """No kernel may read workspace memory it did not write: with the allocator's
+    recycled blocks NaN-filled before the engine takes them (field buffers,
+    strips, receiver samples, accumulators all come from there), the stepwise
+    tile kernels and the cluster engine still match the oracle."""
+    grid, geom, pulse, damp, c_true, r = _rect_case(72, 104, 6, True)
+    tx, rx = geom.tx_nodes(), geom.rx_nodes()
+    obs, _ = oracle.forward_sweep(c_true, damp.values, grid.dx, grid.dt, pulse.samples, tx, rx, rho=r)
+    c0 = np.full(grid.shape, 1520.0)
+    m_ref, g_ref, _ = oracle.misfit_gradient(c0, damp.values, grid.dx, grid.dt, pulse.samples, tx, rx,
+                                             obs, geom.element_nodes, rho=r)
+    for store in ("strips", "full", "checkpoint"):
+        fwd._ENGINE_CACHE.clear()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        junk = torch.full((1 << 27,), float("nan"), device=gpu)  # 512 MiB of NaN
+        del junk
+        eng = fwd.get_engine(grid, tx, rx, geom.element_nodes, pulse.samples, damp, has_rho=True,
+                             engine="stepwise")
+        eng.set_model(c0[None], r[None])
+        mis, g = eng.misfit_and_gradient(torch.as_tensor(obs).to(gpu), store=store)
+        assert torch.isfinite(g).all(), store
+        assert rel_l2(g[0].cpu().numpy(), g_ref) <= TOL, store
+        assert abs(float(mis[0]) - m_ref) <= TOL * m_ref, store
