@@ -74,10 +74,8 @@ struct ClusterCfg {
   int maxring = 0;  // ring-strip cells per CTA (upper bound) staged in shared memory
   int maxc = 0;     // clusters co-resident on the device (one wave)
   int per_sm = 1;   // CTAs of the sweep kernels that fit one SM (registers / shared memory)
-  int xthreads = 0; // extra warp of the L(u)-storing forward: issues its bulk stores (0: thread 0 does)
   size_t smem_fwd = 0, smem_adj = 0;
   size_t smem_lap = 0;     // adjoint over the L(u) history (DUFWI_STORE_LAP)
-  size_t smem_fwdlap = 0;  // forward storing it (staging slots)
 };
 
 // Receiver samples / ring strips / residuals move between HBM and the step loop
@@ -100,20 +98,6 @@ __host__ __device__ constexpr int cluster_max_threads(int rpt) {
 // registers come from one SM sub-partition, 16384 each, so 15 warps cap at 128)
 __host__ __device__ constexpr int cluster_max_regs(int rpt) {
   return (65536 / cluster_max_threads(rpt)) / 8 * 8;
-}
-
-// The forward that stores the L(u) history runs one warp more than the compute
-// threads (ClusterCfg::xthreads, its bulk-copy issuer): 21 warps put 6 on one
-// SM sub-partition, 16384 / (6 * 32) = 85 registers per thread.  (The adjoint
-// over that history measured slower with the extra warp and the 80-register
-// cap: 0.80 vs 0.77 ms on config 1; it keeps thread 0 as the issuer.)
-// (f32 only: the f64 instances spill at 80 and keep thread 0 as the issuer)
-__host__ __device__ constexpr int cluster_lap_regs(int rpt, int scalar_bytes) {
-  return rpt <= 5 && scalar_bytes == 4 ? 80 : cluster_max_regs(rpt);
-}
-// an extra warp fits: warps per sub-partition x registers within its 16384
-__host__ __device__ constexpr bool cluster_extra_warp_fits(int threads, int regs) {
-  return threads + 32 <= 1024 && ((threads + 32 + 127) / 128) * 32 * regs <= 16384;
 }
 
 // ------------------------------------------------------------- PTX helpers
@@ -568,7 +552,6 @@ struct StepBufs {
 
 // ---- L(u) history transport (DUFWI_STORE_LAP; the adjoint kernel is below)
 constexpr int kLapDepth = 4;  // adjoint ring slots
-constexpr int kLapStage = 4;  // forward staging slots
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint32_t bar) {
@@ -577,22 +560,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
           dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -609,17 +576,6 @@ __device__ __forceinline__ BoxRows box_rows(const Geo& g, const CellCtx& c) {
   return r;
 }
 
-// Forward staging (MODE 3): kLapStage slots of rows x nz floats after the IO stage.
-template <class T>
-__host__ __device__ inline size_t lap_stage_offset(int rows, int rpt, int nz, int maxrec,
-                                                   int maxring) {
-  return al16(io_offset<T>(rows, rpt, nz, 2) + io_bytes<T>(maxrec, maxring));
-}
-template <class T>
-__host__ __device__ inline size_t cluster_fwdlap_smem_bytes(int rows, int rpt, int nz, int maxrec,
-                                                            int maxring) {
-  return lap_stage_offset<T>(rows, rpt, nz, maxrec, maxring) + (size_t)kLapStage * rows * nz * 4;
-}
 // Adjoint ring: kLapDepth mbarriers (32 B) then kLapDepth slots of rows x nz floats.
 template <class T>
 __host__ __device__ inline size_t lap_ring_offset(int rows, int rpt, int nz, int maxrec) {
@@ -628,26 +584,6 @@ __host__ __device__ inline size_t lap_ring_offset(int rows, int rpt, int nz, int
 template <class T>
 __host__ __device__ inline size_t cluster_lap_smem_bytes(int rows, int rpt, int nz, int maxrec) {
   return lap_ring_offset<T>(rows, rpt, nz, maxrec) + 32 + (size_t)kLapDepth * rows * nz * 4;
-}
-
-// Forward, thread 0 after the step barrier of step t: write the staging slot of
-// step t-1 (slot (t-2) % 4, holding L(u[t-2])) to history slot t-2.  Slot
-// reuse: step t writes slot (t-1) % 4, whose last bulk read was issued at step
-// t-3 and completed by this thread's wait_group.read<2> at step t-1 (it passed
-// that wait before the barrier of step t).  A store therefore has two full
-// steps to read its slot: with 3 slots and wait_group.read<1> thread 0 waited
-// ~800 cycles per step for the previous step's store, its warp's halo push
-// arrived late and every neighbour CTA sat ~600 cycles in its halo wait
-// (per-warp clock64 timing, profiles/r02_phase_dbg_f32.log).
-__device__ __forceinline__ void lap_store(const Geo& g, const BoxRows& br, int rows, int t,
-                                          uint32_t stage_sa, float* hbox, size_t hstep,
-                                          bool issuer) {
-  if (issuer && br.nb > 0 && t >= 2) {
-    const uint32_t slot = stage_sa + (uint32_t)(((t - 2) % kLapStage) * rows * g.nz) * 4u;
-    bulk_s2g(hbox + (size_t)(t - 2) * hstep, slot, (uint32_t)(br.nb * g.nz) * 4u);
-    bulk_commit();
-    bulk_wait_read<2>();
-  }
 }
 
 // Adjoint, thread 0: bulk load of step j's operand L(u[t-1]) (t = nt-1-j) into
@@ -665,29 +601,12 @@ __device__ __forceinline__ void lap_load(const Geo& g, const BoxRows& br, int ro
   }
 }
 
-// Forward side of a CTA: its box rows, staging slots and history base.
-struct LapFwd {
-  BoxRows br;
-  uint32_t stage_sa;
-  float* hbox;
-  size_t hstep;
-  bool issuer;  // this thread issues the CTA's bulk stores
-};
-
-// The thread that issues a CTA's bulk copies.  Issuing and waiting on them
-// costs the thread ~500-800 cycles per step (per-warp clock64 timing): in a
-// compute warp that delays the warp's step body and with it its halo pushes,
-// and the neighbouring CTAs wait for those.  When the register file allows a
-// 21st warp (ClusterCfg::xthreads) the first thread past the compute threads —
-// in the virtual thread order of order_columns — takes the job; its warp owns
-// no cells.
-// Without an extra warp the job goes to the first thread of a middle segment:
-// its warp pushes no halo row, so its late start delays no neighbour, and
-// inside the CTA it is hidden behind the halo wait.
-__device__ __forceinline__ bool bulk_issuer(const CellCtx& c, int nz, int rows, int rpt) {
-  const int nthr = nz * ((rows + rpt - 1) / rpt);
-  return (int)blockDim.x > nthr ? c.seg * nz + c.zi == nthr : threadIdx.x == 0;
-}
+// The thread that issues the adjoint's bulk loads.  Issuing them costs the
+// thread a few hundred cycles per step (per-warp clock64 timing): in a warp
+// that pushes a halo row that delays the push, and the neighbouring CTAs wait
+// for it.  The job goes to the first thread of a middle segment: its warp
+// pushes no halo row, so its late start delays no neighbour, and inside the
+// CTA it is hidden behind the halo wait.
 // (the adjoint over the L(u) history; adjoint 0.721 -> 0.697 ms on config 1)
 __device__ __forceinline__ bool bulk_issuer_mid(const CellCtx& c, int nz, int rows, int rpt) {
   const int nseg = (rows + rpt - 1) / rpt;
@@ -723,9 +642,9 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
   const T* pp = pc + c.RS;
   T v[RPT];
   const pair_t<T> ab0 = (!PLAIN && UNIF) ? s.ab[0] : free_pair<T>();
-  // MODE 3: the step's L(u[t-1]) (5-point sum, f32) of the box cells into the
-  // shared-memory staging slot of step t (`hist`: the thread's first cell there),
-  // written to history slot t-1 by one bulk copy after the next step barrier
+  // MODE 3: the step's L(u[t-1]) (5-point sum, f32) of the box cells straight
+  // to history slot t-1 (`hist`: the thread's first cell there): a warp's
+  // st.global covers one 128-byte row piece, nothing waits on it
   float* hl = hist;
   constexpr bool EARLY = FULL && kEdgeFirst;
 #pragma unroll
@@ -755,7 +674,6 @@ __device__ __forceinline__ void fwd_body(const Geo& g, const CellCtx& c, const C
     if (MODE == 1) hist[((size_t)t * U + lu) * N2 + (size_t)(c.r0 + c.lrow0 + j) * g.nz + c.z] = (float)v[j];
   }
   if (!EARLY) push_edges<RPT, T>(c, s, B.wb, B.bar_wb, v, FULL);
-  if (MODE == 3) fence_proxy_async();  // the staged values are read by the bulk copy
 }
 
 // Receiver samples / ring cells of step t, read back from the exchange buffer
@@ -816,13 +734,11 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
                                          int lu, const StepBufs<T>& B, uint32_t tx_bytes,
                                          T pulse_t, const IoStage<T>& io, int nrec, int nio,
                                          float* __restrict__ rec, float* __restrict__ strips,
-                                         float* __restrict__ hist, size_t N2, int grank,
-                                         const LapFwd& lap) {
+                                         float* __restrict__ hist, size_t N2, int grank) {
 #ifdef DUFWI_EXP_TIMING
   const long long T0 = clock64();
 #endif
   step_sync(c, t, B.bar_r, B.bar_w, tx_bytes);
-  if (MODE == 3) lap_store(g, lap.br, c.rows, t, lap.stage_sa, lap.hbox, lap.hstep, lap.issuer);
   if (t >= 1) {
     io_gather<T, MODE>(io, nrec, nio, B.r, t - 1, grank);
     if (t % kStage == 0) flush_stage<T, MODE>(g, io, t - kStage, kStage, U, lu, rec, strips);
@@ -848,7 +764,7 @@ __device__ __forceinline__ void fwd_step(const Geo& g, const CellCtx& c, const C
 }
 
 template <int RPT, class T, int MODE>
-__global__ void __maxnreg__(MODE == 3 ? cluster_lap_regs(RPT, (int)sizeof(T)) : cluster_max_regs(RPT))
+__global__ void __maxnreg__(cluster_max_regs(RPT))
     cluster_fwd_kernel(Geo g, Model m, int cs, int rows, int maxrec, int maxring,
                        int unit_begin, int U, float* __restrict__ rec, float* __restrict__ hist,
                        float* __restrict__ strips, float* __restrict__ ubuf) {
@@ -897,44 +813,29 @@ __global__ void __maxnreg__(MODE == 3 ? cluster_lap_regs(RPT, (int)sizeof(T)) : 
   const uint32_t xb1 = (uint32_t)(xe * sizeof(T));
   const StepBufs<T> B0{X[1], X[0], 0u, bar[1], bar[0], bar_off};
   const StepBufs<T> B1{X[0], X[1], xb1, bar[0], bar[1], bar_off + 8u};
-  // MODE 3: staging slots of the box rows' L(u), written out by thread 0
-  LapFwd lap{};
-  float* stage = nullptr;
-  int lofs = 0;
-  const int slotf = rows * g.nz;
-  if (MODE == 3) {
-    lap.br = box_rows(g, c);
-    lap.issuer = bulk_issuer(c, g.nz, rows, RPT);
-    const size_t so = lap_stage_offset<T>(rows, RPT, g.nz, maxrec, maxring);
-    stage = reinterpret_cast<float*>(smem + so);
-    lap.stage_sa = smem_addr(stage);
-    lap.hstep = (size_t)U * N2;
-    lap.hbox = hist + (size_t)lu * N2 + (size_t)max(lap.br.b0, 0) * g.nz;
-    lofs = (c.r0 + c.lrow0 - lap.br.b0) * g.nz + c.z;  // slots start at box row b0
-  }
-  // the thread's cell in the staging slot of step t (MODE 3), else the history
-#define DUFWI_HS(t) (MODE == 3 ? stage + (size_t)(((t) + kLapStage - 1) % kLapStage) * slotf + lofs : hist)
+  // MODE 3: the thread's first cell in history slot 0 (slots hold whole [x][z]
+  // maps per unit; only the undamped box is written and read)
+  const size_t hstep = (size_t)U * N2;
+  float* hcell = MODE == 3 ? hist + (size_t)lu * N2 + (size_t)(c.r0 + c.lrow0) * g.nz + c.z : hist;
+  // step t stores L(u[t-1]) to slot t-1 (t >= 1; never dereferenced at t = 0)
+#define DUFWI_HS(t) (MODE == 3 ? hcell + ((ptrdiff_t)(t) - 1) * (ptrdiff_t)hstep : hist)
   int t = 0;
   for (; t + 1 < g.nt; t += 2) {
     T p = p_next;
     if (owns_src) p_next = (T)g.pulse[t + 1];
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p, io, nrec, nio, rec,
-                           strips, DUFWI_HS(t), N2, grank, lap);
+                           strips, DUFWI_HS(t), N2, grank);
     p = p_next;
     if (owns_src && t + 2 < g.nt) p_next = (T)g.pulse[t + 2];
     fwd_step<RPT, T, MODE>(g, c, st, ub, ua, t + 1, U, lu, B1, tx_bytes, p, io, nrec, nio, rec,
-                           strips, DUFWI_HS(t + 1), N2, grank, lap);
+                           strips, DUFWI_HS(t + 1), N2, grank);
   }
   if (t < g.nt)
     fwd_step<RPT, T, MODE>(g, c, st, ua, ub, t, U, lu, B0, tx_bytes, p_next, io, nrec, nio, rec,
-                           strips, DUFWI_HS(t), N2, grank, lap);
+                           strips, DUFWI_HS(t), N2, grank);
 #undef DUFWI_HS
   // the last step's samples, then the partial stage
   __syncthreads();
-  if (MODE == 3) {  // the last step's L(u[nt-2]); every store complete before exit
-    lap_store(g, lap.br, rows, g.nt, lap.stage_sa, lap.hbox, lap.hstep, lap.issuer);
-    if (lap.issuer) bulk_wait<0>();
-  }
   io_gather<T, MODE>(io, nrec, nio, X[(g.nt - 1) & 1], g.nt - 1, gather_rank());
   {
     const int t0 = (g.nt - 1) / kStage * kStage;
@@ -1279,12 +1180,16 @@ __global__ void __maxnreg__(cluster_max_regs(RPT))
 // receivers, and acc += L(u[t-1]) * lam.  No u state, no backward
 // reconstruction, no second exchange buffer or push.
 //
-// Both directions move a CTA's box rows of a step as ONE contiguous bulk copy
-// issued by one thread (the rows of a slab are contiguous in the [x][z]
-// layout): the forward stages L(u) in shared memory and writes it with
-// cp.async.bulk (shared -> global, bulk groups); the adjoint prefetches
-// kLapDepth steps ahead with cp.async.bulk (global -> shared) completing on a
-// per-slot mbarrier.  No per-thread global address arithmetic in the step.
+// The forward writes its box cells' L(u) with plain st.global from the step
+// body: fire-and-forget, a warp covers 128 contiguous bytes of a row.  (Staging
+// the rows in shared memory and writing them with cp.async.bulk from a 21st
+// warp cost a fence.proxy.async per thread and step and an 80-register cap:
+// 0.682 against 0.637 ms on config 1.)  The adjoint cannot afford the latency
+// of per-thread loads (operand loaded one step ahead into registers: 0.81 ms,
+// in the same step: 0.93 ms, against 0.67 ms): it prefetches a CTA's box rows
+// of a step as ONE contiguous cp.async.bulk (global -> shared, the rows of a
+// slab are contiguous in the [x][z] layout) kLapDepth steps ahead, completing
+// on a per-slot mbarrier, issued by one thread.
 template <int RPT, class T, bool FULL, bool PLAIN, bool UNIF, bool IO, bool IMG>
 __device__ __forceinline__ void adjlap_body(const CellCtx& c, const CellStatic<RPT, T>& s,
                                             T (&l1)[RPT], T (&l2)[RPT],
@@ -1535,13 +1440,10 @@ inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, 
   const size_t sa = cluster_smem_bytes<T>(rows, RPT, g.nz, 4, maxrec, maxring);
   // clusters co-resident on the device: the least over the sweep kernels
   const size_t sl = cluster_lap_smem_bytes<T>(rows, RPT, g.nz, maxrec);
-  const size_t sf3 = cluster_fwdlap_smem_bytes<T>(rows, RPT, g.nz, maxrec, maxring);
   int n = max_active_clusters(cluster_fwd_kernel<RPT, T, 0>, cs, threads, sf);
   n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 1>, cs, threads, sf));
   n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 2>, cs, threads, sf));
-  // the L(u)-storing forward runs a 21st warp for its bulk stores when the register file allows
-  const int xt = cluster_extra_warp_fits(threads, cluster_lap_regs(RPT, (int)sizeof(T))) ? 32 : 0;
-  n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 3>, cs, threads + xt, sf3));
+  n = std::min(n, max_active_clusters(cluster_fwd_kernel<RPT, T, 3>, cs, threads, sf));
   n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 1>, cs, threads, sa));
   n = std::min(n, max_active_clusters(cluster_adj_kernel<RPT, T, 2>, cs, threads, sa));
   n = std::min(n, max_active_clusters(cluster_adjlap_kernel<RPT, T>, cs, threads, sl));
@@ -1553,7 +1455,6 @@ inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, 
     per_sm = 1;
   }
   out->per_sm = std::max(1, per_sm);
-  out->xthreads = xt;
   out->cs = cs;
   out->rows = rows;
   out->rpt = RPT;
@@ -1563,7 +1464,6 @@ inline bool try_cluster_cfg(const Geo& g, int cs, const std::vector<int2>& rxn, 
   out->smem_fwd = sf;
   out->smem_adj = sa;
   out->smem_lap = sl;
-  out->smem_fwdlap = sf3;
   out->maxrec = maxrec;
   out->maxring = maxring;
   out->maxc = n;
@@ -1711,12 +1611,9 @@ inline cudaError_t cluster_forward_t(const Geo& g, const Model& m, const Cluster
   if (mode == 1)
     return launch_cluster(cluster_fwd_kernel<RPT, T, 1>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
                           c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
-  if (mode == 4) {  // DUFWI_STORE_LAP: hist receives L(u[t]) (kernel MODE 3)
-    ClusterCfg cx = c;
-    cx.threads += c.xthreads;
-    return launch_cluster(cluster_fwd_kernel<RPT, T, 3>, cx, U, c.smem_fwdlap, st, g, m, c.cs, c.rows,
+  if (mode == 4)  // DUFWI_STORE_LAP: hist receives L(u[t]) (kernel MODE 3)
+    return launch_cluster(cluster_fwd_kernel<RPT, T, 3>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
                           c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
-  }
   return launch_cluster(cluster_fwd_kernel<RPT, T, 2>, c, U, c.smem_fwd, st, g, m, c.cs, c.rows,
                         c.maxrec, c.maxring, unit_begin, U, rec, hist, strips, ubuf);
 }
