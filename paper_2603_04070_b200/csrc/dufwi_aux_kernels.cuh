@@ -87,7 +87,7 @@ __global__ void gather_traces_kernel(Geo g, int unit_begin, int U, const float* 
 // receiver order, like np.add.at in adjoint.py:127) and per-part partial
 // misfits sum((tr - obs)^2) (adjoint.py:113-114) from fixed-shape block
 // reductions, summed in part order later — results do not depend on scheduling.
-constexpr int kResidualSplit = 16;
+constexpr int kResidualSplit = 64;
 
 template <int NT>
 __global__ void __launch_bounds__(NT) residual_kernel(Geo g, int unit_begin, int U,
@@ -128,14 +128,26 @@ __global__ void __launch_bounds__(NT) residual_kernel(Geo g, int unit_begin, int
   if (threadIdx.x == 0) misfit_unit[(size_t)lu * kResidualSplit + blockIdx.x] = red[0];
 }
 
-// misfit[b] += sum over the chunk's units of phantom b, in unit order.
+// misfit[b] += sum over the chunk's units of phantom b, in unit order.  One warp:
+// lane l sums the parts of units l, l + 32, ... (part order, loads of different
+// units in flight together), lane 0 then adds the unit sums in unit order — the
+// same additions in the same order as a serial loop.
 __global__ void misfit_sum_kernel(Geo g, int unit_begin, int U, const double* __restrict__ mu,
                                   double* __restrict__ misfit) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int lu = 0; lu < U; ++lu) {
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  __shared__ double unit_sum[32];
+  for (int base = 0; base < U; base += 32) {
+    const int lu = base + threadIdx.x;
     double m = 0.0;
-    for (int k = 0; k < kResidualSplit; ++k) m += mu[(size_t)lu * kResidualSplit + k];
-    misfit[(unit_begin + lu) / g.S] += m;
+    if (lu < U)
+      for (int k = 0; k < kResidualSplit; ++k) m += mu[(size_t)lu * kResidualSplit + k];
+    unit_sum[threadIdx.x] = m;
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      const int n = min(32, U - base);
+      for (int j = 0; j < n; ++j) misfit[(unit_begin + base + j) / g.S] += unit_sum[j];
+    }
+    __syncwarp();
   }
 }
 
@@ -163,10 +175,12 @@ __global__ void reduce_groups_kernel(Geo g, int b0, int nb, int first, int gpp,
 
 // grad = keep ? dE/dc * (acc / dx^2) : 0, keep = D == 0 and farther than guard
 // from every element (adjoint.py:75-91, 133-137).
+// (ex0..ez1: bounding box of the elements, so cells farther than guard from the
+// box skip the element loop.)
 __global__ void finalize_kernel(Geo g, const double* __restrict__ acc, const double* __restrict__ dEdc,
-                                const int* __restrict__ elements, int n_el, int apply_mask,
-                                int guard, double dx2, double* __restrict__ grad,
-                                int* __restrict__ flag) {
+                                const int* __restrict__ elements, int n_el, int ex0, int ex1,
+                                int ez0, int ez1, int apply_mask, int guard, double dx2,
+                                double* __restrict__ grad, int* __restrict__ flag) {
   const size_t N2 = (size_t)g.nx * g.nz;
   const size_t total = (size_t)g.B * N2;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
@@ -179,7 +193,8 @@ __global__ void finalize_kernel(Geo g, const double* __restrict__ acc, const dou
     if (apply_mask) {
       keep = damping_at(g, x, z) == 0.0;
       const long g2 = (long)guard * guard;
-      for (int e = 0; e < n_el && keep; ++e) {
+      const bool near = x >= ex0 - guard && x <= ex1 + guard && z >= ez0 - guard && z <= ez1 + guard;
+      for (int e = 0; e < n_el && keep && near; ++e) {
         const long ddx = x - elements[2 * e], ddz = z - elements[2 * e + 1];
         if (ddx * ddx + ddz * ddz <= g2) keep = false;
       }

@@ -67,6 +67,7 @@ struct dufwi_plan {
   double *px = nullptr, *pz = nullptr, *d2d = nullptr, *pulse = nullptr;
   int *tx = nullptr, *rx_slot = nullptr, *rx_next = nullptr, *node_slot = nullptr;
   int* elements = nullptr;
+  int el_box[4] = {0, -1, 0, -1};  // x0, x1, z0, z1 of the elements (gradient mask)
   int* rx_slot_unused = nullptr;
   unsigned char *row_flag = nullptr, *col_flag = nullptr, *rx_head = nullptr;
   double *Ed = nullptr, *dEdc = nullptr, *rho = nullptr, *q = nullptr;
@@ -499,6 +500,12 @@ extern "C" int dufwi_plan_create(const dufwi_geometry_t* geo, dufwi_plan_t** pla
   rc = rc ? rc : upload(p, &p->row_flag, row_flag.data(), row_flag.size());
   rc = rc ? rc : upload(p, &p->col_flag, col_flag.data(), col_flag.size());
   if (p->E > 0) rc = rc ? rc : upload(p, &p->elements, geo->elements_host, 2 * (size_t)p->E);
+  for (int e = 0; e < p->E; ++e) {
+    const int ex = geo->elements_host[2 * e], ez = geo->elements_host[2 * e + 1];
+    if (e == 0) p->el_box[0] = p->el_box[1] = ex, p->el_box[2] = p->el_box[3] = ez;
+    p->el_box[0] = std::min(p->el_box[0], ex), p->el_box[1] = std::max(p->el_box[1], ex);
+    p->el_box[2] = std::min(p->el_box[2], ez), p->el_box[3] = std::max(p->el_box[3], ez);
+  }
   const size_t BN2 = (size_t)g.B * nx * nz;
   rc = rc ? rc : dev_alloc(p, &p->Ed, BN2);
   rc = rc ? rc : dev_alloc(p, &p->dEdc, BN2);
@@ -1056,8 +1063,8 @@ extern "C" int dufwi_finalize_gradient(dufwi_plan_t* p, const double* acc_dev, i
   const size_t total = (size_t)g.B * g.nx * g.nz;
   const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)p->sms * 16);
   finalize_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-      g, acc_dev, p->dEdc, p->elements, p->E, apply_mask, guard, p->dx * p->dx, grad_dev,
-      nonfinite_dev);
+      g, acc_dev, p->dEdc, p->elements, p->E, p->el_box[0], p->el_box[1], p->el_box[2], p->el_box[3],
+      apply_mask, guard, p->dx * p->dx, grad_dev, nonfinite_dev);
   LAUNCH_CHECK(p);
   return DUFWI_OK;
 }
