@@ -149,6 +149,14 @@ def test_graphed_reconstruct_equals_eager(gpu):
     assert rec._g is not first
     assert all(torch.equal(a, b) for a, b in zip(eager, g3))
     assert rec.replayed_launches > 0
+    # the public API's one-round-trip variant: the same maps on the host, from the
+    # replay (graph buffers read without clones) and from eager launches
+    want = torch.stack(eager).cpu().numpy()
+    assert np.array_equal(rec.reconstruct_host(obs, c0), want)
+    assert np.array_equal(rec.reconstruct_host(obs, c0), want)
+    assert np.array_equal(Reconstructor(eng, nets, bounds, graph=False).reconstruct_host(obs, c0), want)
+    want2 = torch.stack(e2).cpu().numpy()
+    assert np.array_equal(rec.reconstruct_host(obs2, c02), want2)
 
 
 def test_stage_device_equals_torch_update_bitwise(gpu):
