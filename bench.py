@@ -398,7 +398,8 @@ def run_ours(args, rank: int, world: int) -> None:
     # the update networks' 3x3 convolutions: let cuDNN pick its fastest fp32 algorithm
     # (measured 0.29 -> 0.26 ms per network at 160^2; TF32 stays off)
     # (single process only: replicated networks stay on cuDNN's deterministic heuristics
-    # under torch.distributed; Reconstructor also broadcasts rank 0's maps)
+    # under torch.distributed; Reconstructor runs each phantom's network on one rank and
+    # combines the stage maps with an all_reduce of exact zeros)
     torch.backends.cudnn.benchmark = world == 1
     dev = torch.device("cuda", local)
     B = world  # weak scaling: one phantom per GPU

@@ -91,10 +91,24 @@ class Reconstructor:
         self._seen = None  # key of the last eager call (capture on the next one)
         self.replayed_launches = 0
 
+    def _update(self, net, c, g):
+        """clamp(c + update(c, g)) of one stage for the phantoms in ``c`` (unfold.py:263-265)."""
+        import torch
+
+        lo, hi = self.bounds
+        if hasattr(net, "stage_device") and c.is_cuda:
+            return net.stage_device(c, g, lo, hi)  # normalisation + update in libdufwi
+        if hasattr(net, "predict_update_device"):
+            return torch.clamp(c + net.predict_update_device(c, g), lo, hi)
+        # a host network (e.g. the reference's NumPy CNN): one round trip per stage
+        upd = torch.stack([torch.as_tensor(net.predict_update(ci.cpu().numpy(), gi.cpu().numpy()))
+                           for ci, gi in zip(c, g)]).to(c.device)
+        return torch.clamp(c + upd, lo, hi)
+
     def _stages(self, obs, c0, keep_gradients: bool, check_finite: bool):
         import torch
 
-        from .engine import raise_nonfinite
+        from .engine import raise_nonfinite, shard_range
 
         lo, hi = self.bounds
         c = torch.clamp(c0.to(torch.float64), lo, hi)
@@ -111,21 +125,25 @@ class Reconstructor:
             _, g = self.engine.misfit_and_gradient(obs, guard_radius=self.guard_radius,
                                                    check_finite=False, units=units)
             flags.append(self.engine.last_flags())
-            if hasattr(net, "stage_device") and c.is_cuda:
-                c = net.stage_device(c, g, lo, hi)  # normalisation + update in libdufwi
-            elif hasattr(net, "predict_update_device"):
-                c = torch.clamp(c + net.predict_update_device(c, g), lo, hi)
-            else:  # a host network (e.g. the reference's NumPy CNN): one round trip per stage
-                if check_finite:
-                    raise_nonfinite(flags[-1].cpu())
-                upd = torch.stack([torch.as_tensor(net.predict_update(ci.cpu().numpy(),
-                                                                      gi.cpu().numpy()))
-                                   for ci, gi in zip(c, g)]).to(c.device)
-                c = torch.clamp(c + upd, lo, hi)
+            if check_finite and not hasattr(net, "predict_update_device"):
+                # a host network reads the gradient now: check before handing it over
+                # (the flags are part of the combined partials: every rank raises alike)
+                raise_nonfinite(flags[-1].cpu())
             if dist:
-                # one update for all ranks: rank 0's map (replicated networks could
-                # otherwise round differently per rank, e.g. other cuDNN algorithms)
-                torch.distributed.broadcast(c, src=0)
+                # each phantom's update runs on ONE rank (phantoms split like units,
+                # engine.shard_range), the others contribute exact zeros to one
+                # all_reduce: no replicated network work (weak scaling keeps the
+                # per-rank network cost of one process), and every rank holds the same
+                # bits whatever cuDNN algorithm each rank would have picked
+                b0, b1 = shard_range(c.shape[0], torch.distributed.get_rank(),
+                                     torch.distributed.get_world_size())
+                nxt = torch.zeros_like(c)
+                if b1 > b0:
+                    nxt[b0:b1] = self._update(net, c[b0:b1], g[b0:b1])
+                torch.distributed.all_reduce(nxt)
+                c = nxt
+            else:
+                c = self._update(net, c, g)
             maps.append(c)
             if keep_gradients:
                 grads.append(g)

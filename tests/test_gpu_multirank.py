@@ -8,8 +8,11 @@ host-side all_reduce / broadcast couple them).
   gradient bit for bit.
 * The per-sample public misfit_and_gradient is NOT a collective: every rank
   gets the single-process value (not world_size times it).
-* unfold_infer_batch is a collective with rank 0's stage maps broadcast: all
-  ranks return the same maps, equal to the single-process call.
+* unfold_infer_batch is a collective: each phantom's update network runs on one
+  rank and the stage maps are combined with an all_reduce of exact zeros, so all
+  ranks return the same bits; against the single-process call the maps agree to
+  the rounding of the fp32 networks (cuDNN may pick another algorithm for a batch
+  of one than for the batch of all phantoms), the physics bit for bit.
 """
 
 from __future__ import annotations
@@ -96,5 +99,9 @@ def test_two_ranks_match_single_process(gpu):
         assert np.array_equal(out["mis"], single["mis"]), r
         assert np.array_equal(out["g"], single["g"]), r
         assert out["m1"] == single["m1"] and np.array_equal(out["g1"], single["g1"]), r
-        assert np.array_equal(out["maps"], single["maps"]), r
+        err = np.linalg.norm(out["maps"] - single["maps"]) / np.linalg.norm(single["maps"])
+        assert err <= 1e-6, (r, err)
+        # stage 1 sees the same gradient bits; only the network's batch shape differs
+        err1 = np.abs(out["maps"][:, 0] - single["maps"][:, 0]).max()
+        assert err1 <= 1e-3, (r, err1)  # m/s
     assert np.array_equal(got[0]["maps"], got[1]["maps"])

@@ -147,9 +147,11 @@ def _recon_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_reconstructor_collective_broadcasts_rank0_maps():
-    """Collective reconstructions broadcast rank 0's stage maps (ranks cannot
-    diverge); per-sample ones (collective=False) compute all units locally."""
+def test_reconstructor_collective_one_owner_per_phantom():
+    """Collective reconstructions run each phantom's update on one rank and combine
+    the stage maps with an all_reduce of exact zeros (ranks cannot diverge, no
+    replicated network work); per-sample ones (collective=False) compute all
+    units locally."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -162,8 +164,9 @@ def test_reconstructor_collective_broadcasts_rank0_maps():
         assert p.exitcode == 0
     coll0, calls0 = got[0][True]
     coll1, calls1 = got[1][True]
-    assert np.array_equal(coll0, coll1)  # rank 1 took rank 0's maps
-    assert np.allclose(coll0[0], 1500.0 + 1.0)  # rank 0's update: 1e-3*1e3 + 0
+    assert np.array_equal(coll0, coll1)  # the same bits on both ranks
+    assert np.array_equal(coll0[0, 0], np.full((6, 6), 1500.0 + 1.0))  # rank 0's update: 1e-3*1e3 + 0
+    assert np.array_equal(coll0[0, 1], np.full((6, 6), 1500.0 + 2.25))  # rank 1's: 2e-3*1e3 + 0.25
     assert calls0 == [None] * 3 and calls1 == [None] * 3  # sharded default ranges
     loc0, lcalls0 = got[0][False]
     loc1, _ = got[1][False]
