@@ -425,7 +425,11 @@ def run_ours(args, rank: int, world: int) -> None:
     for _ in range(args.warmup):
         rec.reconstruct(obs, c0)
     barrier()
-    launches0 = eng.launch_count + rec.replayed_launches
+    from paper_2603_04070_b200 import _lib as _dl
+
+    # the library's kernels: sweeps and epilogues (plan counter), the update-net glue
+    # (GLUE_LAUNCHES; eager stages, i.e. under torch.distributed), graph replays
+    launches0 = eng.launch_count + _dl.GLUE_LAUNCHES[0] + rec.replayed_launches
     clocks = ClockSampler(local).start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -439,7 +443,7 @@ def run_ours(args, rank: int, world: int) -> None:
     barrier()
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
-    launches = (eng.launch_count + rec.replayed_launches - launches0) // args.steps
+    launches = (eng.launch_count + _dl.GLUE_LAUNCHES[0] + rec.replayed_launches - launches0) // args.steps
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     t_max = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if world > 1:
